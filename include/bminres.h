@@ -1,0 +1,167 @@
+/*
+ * bminres.h -- C ABI of the B200-native banded-Lanczos block MINRES hot path.
+ *
+ * Method: K. M. Soodhalter, "A block MINRES algorithm based on the banded
+ * Lanczos method" (arXiv:1301.2102).  "P:L" cites PAPER.md line L.
+ *
+ * Problem: A (n x n) sparse symmetric indefinite, B (n x p).
+ * At iteration j every column x_j^(i) minimises ||b_i - A x|| over
+ * x_0^(i) + R(U_j), U_j = the first j banded-Lanczos vectors (eqn.min-resid,
+ * P:367-374).  Inputs of Alg. 2: A, B, X_0 (= 0 unless requested),
+ * eps (= tol), M (= maxit); the dependence tolerance gamma (= deflation_tol,
+ * P:562-570).
+ *
+ * Conventions for every entry point:
+ *  - All floating point is fp64.  Block vectors ("panels") are ROW-MAJOR n x p:
+ *    element (row r, column c) at ptr[r*p + c].
+ *  - Pointers may be device memory (cudaMalloc / torch CUDA tensors) or host
+ *    memory; the library detects which (cudaPointerGetAttributes) and, for host
+ *    memory, stages the data through device buffers it owns, copying results
+ *    back before returning.  The caller owns A, B, X; the library never frees
+ *    them and keeps no pointer to them after a call returns.
+ *  - Calls are synchronous with respect to the host: they return after the work
+ *    on the handle's stream is complete.  A handle is not re-entrant; distinct
+ *    handles may be used from distinct threads.
+ *  - Return codes: >= 0 success (BMINRES_OK / BMINRES_MAXIT), < 0 error; the
+ *    message is available from bminres_last_error().  There is no CPU
+ *    fallback: without a usable CUDA device bminres_create returns
+ *    BMINRES_ECUDA.
+ */
+#ifndef BMINRES_H
+#define BMINRES_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BMINRES_OK 0           /* all columns converged: max_i ||f_j^(i)||/||b_i|| < tol */
+#define BMINRES_MAXIT 1        /* j reached maxit first (Alg. 2); X holds X_maxit */
+#define BMINRES_EINVAL (-1)    /* bad argument: p out of range, n < p, malformed CSR, tol not finite */
+#define BMINRES_ECUDA (-2)     /* CUDA runtime error (message in bminres_last_error) */
+#define BMINRES_ENCCL (-3)     /* reserved: collective error (world > 1) */
+#define BMINRES_ENOMEM (-4)    /* device allocation failed */
+#define BMINRES_EPOOL (-5)     /* breakdown with the replacement pool empty, not converged */
+#define BMINRES_ESINGULAR_R (-6) /* |r_jj| <= eps_mach*||h_j||: R_j singular, X cannot be updated */
+
+#define BMINRES_MAX_P 32       /* block sizes 1..8, 16 and 32 are compiled */
+#define BMINRES_MAX_POOL 32
+
+typedef struct bminres_ctx *bminres_handle;
+
+/* Sparse symmetric operator A in CSR, both triangles stored.
+ * row_ptr: n_loc+1 int32 offsets into col_idx/values, row_ptr[0] = 0.
+ * col_idx: int32 GLOBAL column indices, strictly increasing within a row.
+ * values:  fp64.  nnz = row_ptr[n_loc] must be < 2^31.
+ * Rows [row_begin, row_begin+n_loc) of the global n x n matrix; at world = 1,
+ * row_begin = 0 and n_loc = n. */
+typedef struct {
+    int64_t n;
+    int64_t row_begin;
+    int64_t n_loc;
+    int64_t nnz;
+    const int32_t *row_ptr;
+    const int32_t *col_idx;
+    const double *values;
+} bminres_csr;
+
+typedef struct {
+    int32_t device;          /* CUDA device ordinal */
+    int32_t rank, world;     /* row partition; only world = 1 is implemented in this version */
+    void *stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
+    uint64_t seed;           /* random replacement vectors (reading C17), default 0 */
+    int32_t pool_size;       /* random vectors kept orthogonal to the basis, 0..32, default 1 */
+    int32_t use_x0;          /* 0: X is output only, X_0 = 0 (Alg. 2); 1: X holds X_0 on entry */
+    int32_t record_history;  /* 1: keep (iterations+1) x p computed relative residuals */
+    int32_t use_graphs;      /* 1: replay each block step as a CUDA graph (default); 0: plain launches */
+    int32_t timing;          /* 1: CUDA events around every kernel launch, per-phase totals in stats */
+    int32_t reserved[7];
+} bminres_options;
+
+/* One dependence event: candidate h_{j+p,j} <= gamma * ||A u_j||. */
+typedef struct {
+    int64_t j;       /* iteration (0 = the start block, eqn.init-QR) */
+    int32_t col;     /* 1-based block column ((j-1) mod p)+1, or RHS column at j = 0 */
+    int32_t kind;    /* 0 exact (h <= 1e-12*omega), 1 near */
+    int32_t action;  /* 1 replaced, 2 replaced + retained, 3 pool exhausted */
+    int32_t pad;
+    double ratio;    /* h / omega */
+} bminres_event;
+
+#define BMINRES_NPHASE 8   /* spmm, orth, smallqr, update, slowpath, start, resid, other */
+
+typedef struct {
+    int32_t status;           /* return code of the last solve */
+    int32_t p;
+    int64_t n;
+    int64_t iterations;       /* banded iterations j completed (one new basis vector each) */
+    int64_t block_steps;      /* operator applications to a block of p vectors */
+    int64_t n_events;
+    int64_t slow_blocks;      /* block steps that took the column-by-column path */
+    int64_t history_len;      /* rows available from bminres_get_history */
+    int64_t gpu_launches;     /* kernels this library launched during the last solve */
+    double comp_res[BMINRES_MAX_P];   /* final ||T(:,i)||/||b_i|| (eqn.comp-resid) */
+    double true_res[BMINRES_MAX_P];   /* final ||b_i - A x_i||/||b_i|| */
+    double solve_ms;          /* device time of the whole solve (CUDA events) */
+    double loop_ms;           /* device time of the block-step loop only */
+    double phase_ms[BMINRES_NPHASE];          /* timing = 1 only */
+    int64_t phase_launches[BMINRES_NPHASE];   /* timing = 1 only */
+    double bytes_per_block_step;  /* algorithmic bytes model: CSR A + 10 panels */
+    double spmm_bytes_per_launch; /* algorithmic bytes of one SpMM launch: CSR A + U_k + U_{k-1} + W */
+} bminres_stats_t;
+
+/* Default options (device 0, world 1, seed 0, pool_size 1, history on, graphs on). */
+void bminres_default_options(bminres_options *opt);
+
+/* Create a handle bound to opt->device; allocates nothing panel-sized yet. */
+int bminres_create(const bminres_options *opt, bminres_handle *out);
+
+/* Solve A X = B for the p columns of B (Alg. 2, with the readings
+ * of DESIGN.md).  B: n_loc x p row-major (read only).  X: n_loc x p row-major
+ * (output; input X_0 when opt.use_x0).  p in {1..8, 16, 32}; tol >= 0 finite;
+ * maxit >= 0; deflation_tol >= 0 (the paper's gamma; reading C14:
+ * relative to ||A u_j||).  Workspace (6 panels + pool) is allocated on the
+ * first call for a given (n_loc, p) and reused.
+ * Returns BMINRES_OK, BMINRES_MAXIT or an error code. */
+int bminres_solve(bminres_handle h, const bminres_csr *A, const double *B, double *X, int32_t p,
+                  double tol, int64_t maxit, double deflation_tol);
+
+/* Statistics of the last solve. */
+int bminres_stats(bminres_handle h, bminres_stats_t *out);
+
+/* Copy min(cap, history_len) rows of p doubles (row j = iteration j, j = 0 is
+ * the start block) into buf (host memory).  Returns the number of rows copied. */
+int64_t bminres_get_history(bminres_handle h, double *buf, int64_t cap);
+
+/* Copy min(cap, n_events) events into buf (host memory).  Returns the count copied. */
+int64_t bminres_get_events(bminres_handle h, bminres_event *buf, int64_t cap);
+
+/* Component entry points of the hot path (same kernels the solver runs),
+ * exported so each step can be checked on its own. */
+
+/* Y = A X (row a1's SpMM): X, Y n_loc x p row-major (Y rows local,
+ * X indexed by global column; at world = 1 both n x n).  Each output row is
+ * accumulated over the CSR row in stored order with fma. */
+int bminres_spmm(bminres_handle h, const bminres_csr *A, const double *X, double *Y, int32_t p);
+
+/* out[i*stride] = entry of random replacement vector (stream, event) at global
+ * row row_begin + i, i < n_loc (reading C17: splitmix64 counter hash, uniform
+ * [-1,1)); bitwise reproducible. */
+int bminres_random_vector(bminres_handle h, uint64_t seed, uint64_t stream, uint64_t event,
+                          int64_t row_begin, int64_t n_loc, double *out, int64_t stride);
+
+/* Bytes of device workspace bminres_solve allocates for (n_loc, p, pool_size). */
+size_t bminres_workspace_bytes(int64_t n_loc, int32_t p, int32_t pool_size);
+
+/* Message of the last error on this handle (or the last create error if h is NULL). */
+const char *bminres_last_error(bminres_handle h);
+
+/* Release the handle and its workspace. */
+void bminres_destroy(bminres_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BMINRES_H */

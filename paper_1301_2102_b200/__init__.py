@@ -1,0 +1,10 @@
+"""B200-native banded-Lanczos block MINRES (Soodhalter, arXiv:1301.2102) — hot path.
+
+The product is ``libbminres.so`` (C ABI, include/bminres.h; CUDA sm_100a kernels in
+``csrc/``).  This package only builds it (``_build``) and binds it (``binding``).
+"""
+from .binding import (BminresError, DeviceCsr, Solver, SolveResult, STATUS, SUPPORTED_P, lib,  # noqa: F401
+                      workspace_bytes)
+
+__all__ = ["BminresError", "DeviceCsr", "Solver", "SolveResult", "STATUS", "SUPPORTED_P", "lib",
+           "workspace_bytes"]

@@ -1,0 +1,258 @@
+"""Thin ctypes binding of include/bminres.h — argument marshalling only.
+
+Every step of the method runs in ``libbminres.so`` (CUDA, sm_100a).  There is no
+CPU fallback: if the library or a CUDA device is missing, these calls raise.
+PyTorch is used only to hold device memory and to hand raw pointers over.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _build
+
+MAX_P = 32
+NPHASE = 8
+PHASES = ["spmm", "orth", "smallqr", "update", "slowpath", "start", "resid", "other"]
+STATUS = {0: "OK", 1: "MAXIT", -1: "EINVAL", -2: "ECUDA", -3: "ENCCL", -4: "ENOMEM", -5: "EPOOL",
+          -6: "ESINGULAR_R"}
+SUPPORTED_P = (1, 2, 3, 4, 5, 6, 7, 8, 16, 32)
+
+
+class BminresError(RuntimeError):
+    pass
+
+
+class Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("stream", C.c_void_p),
+                ("seed", C.c_uint64), ("pool_size", C.c_int32), ("use_x0", C.c_int32),
+                ("record_history", C.c_int32), ("use_graphs", C.c_int32), ("timing", C.c_int32),
+                ("reserved", C.c_int32 * 7)]
+
+
+class CsrStruct(C.Structure):
+    _fields_ = [("n", C.c_int64), ("row_begin", C.c_int64), ("n_loc", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+class Event(C.Structure):
+    _fields_ = [("j", C.c_int64), ("col", C.c_int32), ("kind", C.c_int32), ("action", C.c_int32),
+                ("pad", C.c_int32), ("ratio", C.c_double)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("status", C.c_int32), ("p", C.c_int32), ("n", C.c_int64), ("iterations", C.c_int64),
+                ("block_steps", C.c_int64), ("n_events", C.c_int64), ("slow_blocks", C.c_int64),
+                ("history_len", C.c_int64), ("gpu_launches", C.c_int64),
+                ("comp_res", C.c_double * MAX_P), ("true_res", C.c_double * MAX_P),
+                ("solve_ms", C.c_double), ("loop_ms", C.c_double),
+                ("phase_ms", C.c_double * NPHASE), ("phase_launches", C.c_int64 * NPHASE),
+                ("bytes_per_block_step", C.c_double), ("spmm_bytes_per_launch", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libbminres.so (building it with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path) or _build.stale():
+            _build.build()
+        L = C.CDLL(path)
+        L.bminres_default_options.argtypes = [C.POINTER(Options)]
+        L.bminres_create.argtypes = [C.POINTER(Options), C.POINTER(C.c_void_p)]
+        L.bminres_solve.argtypes = [C.c_void_p, C.POINTER(CsrStruct), C.c_void_p, C.c_void_p, C.c_int32,
+                                    C.c_double, C.c_int64, C.c_double]
+        L.bminres_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
+        L.bminres_get_history.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.bminres_get_history.restype = C.c_int64
+        L.bminres_get_events.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.bminres_get_events.restype = C.c_int64
+        L.bminres_spmm.argtypes = [C.c_void_p, C.POINTER(CsrStruct), C.c_void_p, C.c_void_p, C.c_int32]
+        L.bminres_random_vector.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64,
+                                            C.c_int64, C.c_void_p, C.c_int64]
+        L.bminres_workspace_bytes.argtypes = [C.c_int64, C.c_int32, C.c_int32]
+        L.bminres_workspace_bytes.restype = C.c_size_t
+        L.bminres_last_error.argtypes = [C.c_void_p]
+        L.bminres_last_error.restype = C.c_char_p
+        L.bminres_destroy.argtypes = [C.c_void_p]
+        L.bminres_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["bminres_default_options", "bminres_create", "bminres_solve", "bminres_stats", "bminres_get_history",
+            "bminres_get_events", "bminres_spmm", "bminres_random_vector", "bminres_workspace_bytes",
+            "bminres_last_error", "bminres_destroy"]
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor (device or host) or a numpy array."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise BminresError("tensor must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise BminresError("array must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(type(x))
+
+
+@dataclass
+class DeviceCsr:
+    """CSR arrays resident on one CUDA device (torch tensors): int32 row_ptr/col_idx, fp64 values."""
+    n: int
+    row_ptr: object
+    col_idx: object
+    values: object
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.numel())
+
+    @classmethod
+    def from_host(cls, A, device="cuda"):
+        import torch
+        return cls(int(A.n), torch.from_numpy(np.ascontiguousarray(A.indptr, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(A.indices, dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(A.data, dtype=np.float64)).to(device))
+
+
+def _csr_struct(A) -> CsrStruct:
+    s = CsrStruct()
+    if isinstance(A, DeviceCsr):
+        s.n, s.nnz = A.n, A.nnz
+        s.row_ptr, s.col_idx, s.values = _ptr(A.row_ptr), _ptr(A.col_idx), _ptr(A.values)
+        keep = (A,)
+    else:  # host CSR (numpy): the library stages it
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+        dv = np.ascontiguousarray(A.data, dtype=np.float64)
+        s.n, s.nnz = int(A.n), int(ip[-1])
+        s.row_ptr, s.col_idx, s.values = ip.ctypes.data, ix.ctypes.data, dv.ctypes.data
+        keep = (ip, ix, dv)
+    s.row_begin, s.n_loc = 0, s.n
+    s._keep = keep
+    return s
+
+
+@dataclass
+class SolveResult:
+    status: int
+    iterations: int
+    X: object
+    history: np.ndarray
+    events: list
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def status_name(self) -> str:
+        return STATUS.get(self.status, str(self.status))
+
+
+class Solver:
+    """One handle of the C ABI (bminres_create ... bminres_destroy)."""
+
+    def __init__(self, device: int = 0, *, pool_size: int = 1, seed: int = 0, use_graphs: bool = True,
+                 timing: bool = False, record_history: bool = True, use_x0: bool = False, stream=None):
+        L = lib()
+        o = Options()
+        L.bminres_default_options(C.byref(o))
+        o.device, o.pool_size, o.seed = device, pool_size, seed
+        o.use_graphs, o.timing, o.record_history, o.use_x0 = int(use_graphs), int(timing), int(record_history), int(use_x0)
+        o.stream = stream
+        h = C.c_void_p()
+        rc = L.bminres_create(C.byref(o), C.byref(h))
+        if rc != 0:
+            raise BminresError(f"bminres_create: {STATUS.get(rc, rc)}: {L.bminres_last_error(None).decode()}")
+        self._h = h
+        self.options = o
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bminres_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def last_error(self) -> str:
+        return lib().bminres_last_error(self._h).decode()
+
+    def solve(self, A, B, X=None, *, tol=1e-8, maxit=1000, deflation_tol=1e-8, history=True, raise_on_error=True):
+        """Solve A X = B.  A: DeviceCsr or host CSR (n, indptr, indices, data); B/X: torch CUDA
+        tensors or numpy arrays (row-major n×p fp64).  Returns SolveResult (X is the array written)."""
+        L = lib()
+        p = int(B.shape[1])
+        if X is None:
+            if hasattr(B, "data_ptr"):
+                import torch
+                X = torch.zeros_like(B)
+            else:
+                X = np.zeros_like(B)
+        s = _csr_struct(A)
+        rc = L.bminres_solve(self._h, C.byref(s), _ptr(B), _ptr(X), p, float(tol), int(maxit), float(deflation_tol))
+        if rc < 0 and raise_on_error:
+            raise BminresError(f"bminres_solve: {STATUS.get(rc, rc)}: {self.last_error()}")
+        st = self.stats()
+        hist = None
+        if history and st["history_len"] > 0:
+            hist = np.zeros((st["history_len"], p))
+            L.bminres_get_history(self._h, hist.ctypes.data, st["history_len"])
+        evs = []
+        if st["n_events"] > 0:
+            buf = (Event * st["n_events"])()
+            c = L.bminres_get_events(self._h, C.addressof(buf), st["n_events"])
+            evs = [dict(j=int(e.j), col=int(e.col), kind=int(e.kind), action=int(e.action), ratio=float(e.ratio))
+                   for e in buf[:c]]
+        return SolveResult(rc, st["iterations"], X, hist, evs, st)
+
+    def stats(self) -> dict:
+        s = Stats()
+        lib().bminres_stats(self._h, C.byref(s))
+        p = s.p
+        return dict(status=s.status, p=p, n=s.n, iterations=s.iterations, block_steps=s.block_steps,
+                    n_events=s.n_events, slow_blocks=s.slow_blocks, history_len=s.history_len,
+                    gpu_launches=s.gpu_launches, comp_res=list(s.comp_res[:p]), true_res=list(s.true_res[:p]),
+                    solve_ms=s.solve_ms, loop_ms=s.loop_ms,
+                    phase_ms={PHASES[i]: s.phase_ms[i] for i in range(NPHASE)},
+                    phase_launches={PHASES[i]: s.phase_launches[i] for i in range(NPHASE)},
+                    bytes_per_block_step=s.bytes_per_block_step, spmm_bytes_per_launch=s.spmm_bytes_per_launch)
+
+    def spmm(self, A: DeviceCsr, X, Y=None):
+        """Y = A X through the solver's SpMM kernel (device tensors)."""
+        import torch
+        if Y is None:
+            Y = torch.empty_like(X)
+        s = _csr_struct(A)
+        rc = lib().bminres_spmm(self._h, C.byref(s), _ptr(X), _ptr(Y), int(X.shape[1]))
+        if rc != 0:
+            raise BminresError(f"bminres_spmm: {STATUS.get(rc, rc)}: {self.last_error()}")
+        return Y
+
+    def random_vector(self, seed, stream, event, row_begin, n, out, stride=1):
+        rc = lib().bminres_random_vector(self._h, seed, stream, event, row_begin, n, _ptr(out), stride)
+        if rc != 0:
+            raise BminresError(f"bminres_random_vector: {STATUS.get(rc, rc)}: {self.last_error()}")
+        return out
+
+
+def workspace_bytes(n: int, p: int, pool_size: int = 1) -> int:
+    return int(lib().bminres_workspace_bytes(n, p, pool_size))

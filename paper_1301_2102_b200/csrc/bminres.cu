@@ -1,0 +1,1033 @@
+// bminres.cu -- host driver and C ABI (include/bminres.h) of the B200 block-MINRES hot path.
+//
+// One block step k (p banded iterations) is four kernels on one stream:
+//   K1 SpMM+epilogue -> K2 orthogonalisation+Grams -> K3 small banded QR (one warp) -> K4 updates
+// replayed as a CUDA graph (two graphs, one per panel-slot parity).  The host never waits
+// per step: K3 publishes run/status flags into mapped pinned memory and the host polls the
+// flags of the step launched LAG steps earlier.  Rare events (a breakdown, a Cholesky
+// cancellation, live retained vectors) halt the step after K2 and
+// the host runs the column-by-column path (the paper's per-iteration order) with small
+// GPU kernels, then resumes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bminres.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace bmr;
+
+namespace {
+
+enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER };
+
+struct Retained {
+    double* v;
+    long long expiry;
+};
+
+struct Kfn {  // per-p kernel table
+    void (*k1)(K1Args);
+    void (*k1plain)(K1Args);
+    void (*k2)(K2Args);
+    void (*k3)(DevState*);
+    void (*k4)(K4Args);
+    size_t smem3, smem4;
+};
+
+template <int P>
+Kfn make_kfn() {
+    Kfn f;
+    f.k1 = k1_spmm<P, true>;
+    f.k1plain = k1_spmm<P, false>;
+    f.k2 = k2_orth<P>;
+    f.k3 = k3_smallqr<P>;
+    f.k4 = k4_update<P>;
+    constexpr int LD = P + 1, W2 = 2 * P + 1;
+    f.smem3 = sizeof(double) * (5 * P * LD + 4 * P * LD + W2 * (P + 2) + P);
+    f.smem4 = sizeof(double) * (5 * P * P + P * MAXQ + (NT / 32) * 6 * PC<P>::RPW * P);
+    return f;
+}
+
+bool kfn_for(int p, Kfn* out) {
+    switch (p) {
+        case 1: *out = make_kfn<1>(); return true;
+        case 2: *out = make_kfn<2>(); return true;
+        case 3: *out = make_kfn<3>(); return true;
+        case 4: *out = make_kfn<4>(); return true;
+        case 5: *out = make_kfn<5>(); return true;
+        case 6: *out = make_kfn<6>(); return true;
+        case 7: *out = make_kfn<7>(); return true;
+        case 8: *out = make_kfn<8>(); return true;
+        case 16: *out = make_kfn<16>(); return true;
+        case 32: *out = make_kfn<32>(); return true;
+        default: return false;
+    }
+}
+
+struct Err {
+    int code;
+};
+
+}  // namespace
+
+struct bminres_ctx {
+    bminres_options opt{};
+    int device = 0;
+    int n_sm = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    // workspace
+    long long n_ws = -1;
+    int p_ws = -1, q_ws = -1;
+    double* U[2] = {nullptr, nullptr};
+    double* M[2] = {nullptr, nullptr};
+    double* W = nullptr;
+    double* pool = nullptr;
+    double* part = nullptr;
+    size_t part_elems = 0;
+    double* dsc = nullptr;        // scratch for dot results (MAXREF+8)
+    unsigned* dcnt = nullptr;     // tickets of the generic kernels
+    DevState* st = nullptr;
+    HostFlags* hf = nullptr;      // host pointer (mapped)
+    HostFlags* hf_dev = nullptr;  // device alias
+    double* hist = nullptr;
+    long long hist_cap = 0;
+    // staged inputs (host-pointer calls)
+    int* a_rowptr = nullptr;
+    int* a_col = nullptr;
+    double* a_val = nullptr;
+    size_t a_rows_cap = 0, a_nnz_cap = 0;
+    double* bx = nullptr;         // staged B
+    double* xx = nullptr;         // staged X
+    size_t bx_cap = 0, xx_cap = 0;
+    // graphs
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    const void* gkey[8] = {};
+    // per-solve
+    std::vector<Retained> retained;
+    std::vector<bminres_event> events;
+    std::vector<double> hist_host;
+    bminres_stats_t stats{};
+    long long launches = 0;
+    // timing
+    std::vector<cudaEvent_t> evpool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> ev_marks;   // (phase, index of start event)
+    int nb1 = 0, nb4 = 0;
+    Kfn kf{};
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+#define CK(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            h->err = std::string(#call) + ": " + cudaGetErrorString(e_);               \
+            throw Err{e_ == cudaErrorMemoryAllocation ? BMINRES_ENOMEM : BMINRES_ECUDA}; \
+        }                                                                              \
+    } while (0)
+
+void fail(bminres_ctx* h, int code, const std::string& msg) {
+    h->err = msg;
+    throw Err{code};
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+void dalloc(bminres_ctx* h, T** p, size_t elems) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (elems == 0) return;
+    CK(cudaMalloc((void**)p, elems * sizeof(T)));
+}
+
+cudaEvent_t next_event(bminres_ctx* h) {
+    if (h->ev_used == h->evpool.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        h->evpool.push_back(e);
+    }
+    return h->evpool[h->ev_used++];
+}
+
+// record a timing mark around a launch (timing mode only)
+struct TimeMark {
+    bminres_ctx* h;
+    int phase;
+    size_t idx;
+    bool on;
+    TimeMark(bminres_ctx* h_, int ph) : h(h_), phase(ph), idx(0), on(h_->opt.timing != 0) {
+        if (on) {
+            idx = h->ev_used;
+            cudaEvent_t e = next_event(h);
+            CK(cudaEventRecord(e, h->stream));
+        }
+    }
+    ~TimeMark() noexcept(false) {
+        if (on) {
+            cudaEvent_t e = next_event(h);
+            CK(cudaEventRecord(e, h->stream));
+            h->ev_marks.push_back({phase, idx});
+        }
+    }
+};
+
+void check_launch(bminres_ctx* h, const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    h->launches++;
+}
+
+int grid_for(bminres_ctx* h, long long items, int per_block, int cap) {
+    long long g = (items + per_block - 1) / per_block;
+    g = std::max<long long>(1, std::min<long long>(g, cap));
+    return (int)g;
+}
+
+// ------------------------------------------------------------------ workspace
+
+void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
+    if (h->n_ws == n && h->p_ws == p && h->q_ws == q) return;
+    for (int s = 0; s < 2; ++s) {
+        if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
+        h->gexec[s] = nullptr;
+    }
+    size_t panel = (size_t)n * p;
+    dalloc(h, &h->U[0], panel);
+    dalloc(h, &h->U[1], panel);
+    dalloc(h, &h->M[0], panel);
+    dalloc(h, &h->M[1], panel);
+    dalloc(h, &h->W, panel);
+    dalloc(h, &h->pool, (size_t)n * std::max(q, 1));
+    h->part_elems = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8);
+    if (!h->part) CK(cudaMalloc((void**)&h->part, h->part_elems * sizeof(double)));
+    if (!h->dsc) CK(cudaMalloc((void**)&h->dsc, (MAXREF + 64) * sizeof(double)));
+    if (!h->dcnt) {
+        CK(cudaMalloc((void**)&h->dcnt, 16 * sizeof(unsigned)));
+        CK(cudaMemset(h->dcnt, 0, 16 * sizeof(unsigned)));
+    }
+    if (!h->st) CK(cudaMalloc((void**)&h->st, sizeof(DevState)));
+    if (!h->hf) {
+        CK(cudaHostAlloc((void**)&h->hf, sizeof(HostFlags), cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer((void**)&h->hf_dev, h->hf, 0));
+    }
+    h->n_ws = n;
+    h->p_ws = p;
+    h->q_ws = q;
+    // grid of the reducing panel kernels: up to 2 CTAs per SM (bounded partial count)
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->kf.k1, NT, 0);
+    occ = std::max(1, std::min(occ, 2));
+    long long rows_per_cta = (long long)(NT / 32) * (32 / std::max(1, (p % 2 == 0 ? p / 2 : p)));
+    h->nb1 = grid_for(h, n, (int)std::max<long long>(1, rows_per_cta), std::min(NB_MAX, h->n_sm * occ));
+    int occ4 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, (const void*)h->kf.k4, NT, h->kf.smem4);
+    occ4 = std::max(1, occ4);
+    h->nb4 = grid_for(h, n, (int)std::max<long long>(1, rows_per_cta), h->n_sm * occ4);
+}
+
+// ------------------------------------------------------------------ generic column ops
+
+struct Col {
+    const double* p;
+    long long s;
+};
+
+void launch_dots(bminres_ctx* h, long long n, const std::vector<Col>& v, Col t, double* out) {
+    DotArgs a{};
+    if ((int)v.size() > MAXREF) fail(h, BMINRES_EINVAL, "too many vectors in one dot launch");
+    for (size_t k = 0; k < v.size(); ++k) a.v[k] = {v[k].p, v[k].s};
+    a.K = (int)v.size();
+    a.t = t.p;
+    a.ts = t.s;
+    a.n = n;
+    a.nb = grid_for(h, n, 8 * 64, std::min(NB_MAX, 2 * h->n_sm));
+    a.part = h->part;
+    a.out = out;
+    a.cnt = h->dcnt;
+    k_dots<<<a.nb, 256, 0, h->stream>>>(a);
+    check_launch(h, "k_dots");
+}
+
+// host-visible dot products (synchronising)
+std::vector<double> dots_host(bminres_ctx* h, long long n, const std::vector<Col>& v, Col t) {
+    launch_dots(h, n, v, t, h->dsc);
+    std::vector<double> r(v.size());
+    CK(cudaMemcpyAsync(r.data(), h->dsc, v.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return r;
+}
+
+// t = scale*(t - sum_k c_k v_k)
+void launch_axpy(bminres_ctx* h, long long n, const std::vector<Col>& v, const double* cval, const double* cdev,
+                 double csign, Col t, double scale, const double* scale_dev = nullptr) {
+    AxpyArgs a{};
+    if ((int)v.size() > MAXREF) fail(h, BMINRES_EINVAL, "too many vectors in one axpy launch");
+    for (size_t k = 0; k < v.size(); ++k) {
+        a.v[k] = {v[k].p, v[k].s};
+        a.cval[k] = cval ? cval[k] : 0.0;
+    }
+    a.K = (int)v.size();
+    a.cdev = cdev;
+    a.csign = csign;
+    a.t = const_cast<double*>(t.p);
+    a.ts = t.s;
+    a.n = n;
+    a.scale = scale;
+    a.scale_dev = scale_dev;
+    int g = grid_for(h, n, 256, 8 * h->n_sm);
+    k_axpy<<<g, 256, 0, h->stream>>>(a);
+    check_launch(h, "k_axpy");
+}
+
+void launch_rand(bminres_ctx* h, double* out, long long stride, long long n, long long row_begin, uint64_t seed,
+                 uint64_t stream, uint64_t event) {
+    int g = grid_for(h, n, 256, 8 * h->n_sm);
+    k_rand<<<g, 256, 0, h->stream>>>(out, stride, n, row_begin, seed, stream, event);
+    check_launch(h, "k_rand");
+}
+
+// out[c] = ||X(:,c) - Y(:,c)||^2  (device result)
+void launch_colsq(bminres_ctx* h, const double* X, const double* Y, long long n, int p, double* out) {
+    int R = 256 / p;
+    int nb = grid_for(h, n, R * 16, std::min(NB_MAX, 2 * h->n_sm));
+    k_colsq<<<nb, 256, 0, h->stream>>>(X, Y, n, p, h->part, nb, out, h->dcnt + 1);
+    check_launch(h, "k_colsq");
+}
+
+// ------------------------------------------------------------------ block-step launches
+
+struct StepPtrs {
+    const int* rowptr;
+    const int* col;
+    const double* val;
+    double* X;
+};
+
+void launch_k1(bminres_ctx* h, const StepPtrs& sp, long long n, int slot) {
+    TimeMark tm(h, PH_SPMM);
+    K1Args a{sp.rowptr, sp.col, sp.val, h->U[slot], h->U[slot ^ 1], h->W, n, h->st, h->part, h->nb1};
+    h->kf.k1<<<h->nb1, NT, 0, h->stream>>>(a);
+    check_launch(h, "k1_spmm");
+}
+void launch_k2(bminres_ctx* h, long long n, int slot) {
+    TimeMark tm(h, PH_ORTH);
+    K2Args a{h->W, h->U[slot], h->pool, n, h->st, h->part, h->nb1};
+    h->kf.k2<<<h->nb1, NT, 0, h->stream>>>(a);
+    check_launch(h, "k2_orth");
+}
+void launch_k3(bminres_ctx* h) {
+    TimeMark tm(h, PH_SMALLQR);
+    h->kf.k3<<<1, 32, h->kf.smem3, h->stream>>>(h->st);
+    check_launch(h, "k3_smallqr");
+}
+void launch_k4(bminres_ctx* h, const StepPtrs& sp, long long n, int slot) {
+    TimeMark tm(h, PH_UPDATE);
+    K4Args a{h->W, h->U[slot], h->U[slot ^ 1], h->M[slot], h->M[slot ^ 1], sp.X, h->pool, n, h->st};
+    h->kf.k4<<<h->nb4, NT, h->kf.smem4, h->stream>>>(a);
+    check_launch(h, "k4_update");
+}
+
+void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
+    const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->U[0], h->W, (const void*)(intptr_t)n,
+                          (const void*)(intptr_t)h->p_ws};
+    bool same = h->gexec[0] && h->gexec[1] && std::equal(key, key + 8, h->gkey);
+    if (same) return;
+    for (int s = 0; s < 2; ++s) {
+        if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
+        h->gexec[s] = nullptr;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        long long saved = h->launches;
+        launch_k1(h, sp, n, s);
+        launch_k2(h, n, s);
+        launch_k3(h);
+        launch_k4(h, sp, n, s);
+        h->launches = saved;
+        CK(cudaStreamEndCapture(h->stream, &g));
+        CK(cudaGraphInstantiate(&h->gexec[s], g, 0));
+        cudaGraphDestroy(g);
+    }
+    std::copy(key, key + 8, h->gkey);
+}
+
+// write a few DevState fields from the host (stream-ordered)
+template <typename T>
+void set_state(bminres_ctx* h, size_t offset, T value) {
+    T* tmp;  // pinned staging is not needed for small values: use a synchronous copy after the stream drains
+    (void)tmp;
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy((char*)h->st + offset, &value, sizeof(T), cudaMemcpyHostToDevice));
+}
+#define SET_STATE(h, field, val) set_state(h, offsetof(DevState, field), (decltype(DevState::field))(val))
+
+template <typename T>
+T get_state(bminres_ctx* h, size_t offset) {
+    T v;
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(&v, (char*)h->st + offset, sizeof(T), cudaMemcpyDeviceToHost));
+    return v;
+}
+#define GET_STATE(h, field) get_state<decltype(DevState::field)>(h, offsetof(DevState, field))
+
+// ------------------------------------------------------------------ column-by-column path
+
+// The paper's per-iteration orthogonalisation for the p columns of block k (Alg. 1 P:286-293,
+// breakdown P:562-577, replacement P:690-729, retention P:797-805).  On entry W holds W' (the
+// candidates already orthogonalised against U_{k-1} and U_k by K1/K2).  On exit W holds
+// U_{k+1} (normalised), DevState.Ck = C_k, slow_given = 1.  Returns false if the pool was
+// exhausted (stop_after set).
+void slow_block(bminres_ctx* h, long long n, int p, long long k, int slot, const bminres_options& o, double tau,
+                long long maxit) {
+    TimeMark tm(h, PH_SLOW);
+    const long long j0 = GET_STATE(h, j_done) + 1;
+    std::vector<double> om2(MAXP);
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(om2.data(), (char*)h->st + offsetof(DevState, om2), MAXP * sizeof(double), cudaMemcpyDeviceToHost));
+    int q_first = GET_STATE(h, q_first), q_live = GET_STATE(h, q_live);
+    const int qc = h->q_ws;
+    std::vector<double> Ck(MAXP * MAXP, 0.0);
+    int stop_after = 0;
+    auto Wc = [&](int m) { return Col{h->W + m, p}; };
+    const double* Uprev = h->U[slot ^ 1];
+    const double* Ucur = h->U[slot];
+    for (int m = 0; m < p; ++m) {
+        const long long j = j0 + m;
+        if (j > maxit) break;
+        // MGS against the new vectors of this block (u_{kp+1} .. u_{kp+m})
+        for (int mp = 0; mp < m; ++mp) {
+            double c = dots_host(h, n, {Wc(mp)}, Wc(m))[0];
+            launch_axpy(h, n, {Wc(mp)}, &c, nullptr, 1.0, Wc(m), 1.0);
+            Ck[mp * MAXP + m] = c;
+        }
+        // retained near-dependent vectors
+        for (auto& r : h->retained) {
+            if (r.expiry < j) continue;
+            double c = dots_host(h, n, {Col{r.v, 1}}, Wc(m))[0];
+            launch_axpy(h, n, {Col{r.v, 1}}, &c, nullptr, 1.0, Wc(m), 1.0);
+        }
+        const double hh = std::sqrt(dots_host(h, n, {Wc(m)}, Wc(m))[0]);
+        const double omega = std::sqrt(om2[m]);
+        if (hh <= tau * omega) {
+            bminres_event ev{};
+            ev.j = j;
+            ev.col = m + 1;
+            ev.kind = hh <= 1e-12 * omega ? 0 : 1;
+            ev.action = 1;
+            ev.ratio = omega > 0 ? hh / omega : 0.0;
+            if (ev.kind == 1) {
+                Retained r{nullptr, j + 2 * p};
+                CK(cudaMalloc((void**)&r.v, n * sizeof(double)));
+                CK(cudaMemsetAsync(r.v, 0, n * sizeof(double), h->stream));
+                double mone = -1.0;
+                // v = w / h  (t = (0 - (-1) w) / h)
+                launch_axpy(h, n, {Wc(m)}, &mone, nullptr, 1.0, Col{r.v, 1}, 1.0 / hh);
+                h->retained.push_back(r);
+                ev.action = 2;
+            }
+            if (q_live > 0) {
+                // replacement: pool vector (already orthogonal to u_1..u_{j+p-1}),
+                // orthogonalised twice more against retained + window, normalised
+                // W(:,m) := pool(:,q_first)  (zero it, then subtract -1 * pool)
+                std::vector<Col> src = {Col{h->pool + q_first, qc}};
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Wc(m), 0.0);
+                double mone = -1.0;
+                launch_axpy(h, n, src, &mone, nullptr, 1.0, Wc(m), 1.0);
+                q_first++;
+                q_live--;
+                std::vector<Col> win;
+                for (auto& r : h->retained)
+                    if (r.expiry >= j) win.push_back(Col{r.v, 1});
+                if (k > 1)
+                    for (int mp = m; mp < p; ++mp) win.push_back(Col{Uprev + mp, p});
+                for (int mp = 0; mp < p; ++mp) win.push_back(Col{Ucur + mp, p});
+                for (int mp = 0; mp < m; ++mp) win.push_back(Wc(mp));
+                for (int pass = 0; pass < 2; ++pass)
+                    for (auto& v : win) {
+                        double c = dots_host(h, n, {v}, Wc(m))[0];
+                        launch_axpy(h, n, {v}, &c, nullptr, 1.0, Wc(m), 1.0);
+                    }
+                const double rn = std::sqrt(dots_host(h, n, {Wc(m)}, Wc(m))[0]);
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Wc(m), 1.0 / rn);
+            } else {
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Wc(m), 0.0);
+                ev.action = 3;
+                stop_after = m + 1;
+            }
+            h->events.push_back(ev);
+            Ck[m * MAXP + m] = 0.0;   // h_{j+p,j} := 0
+        } else {
+            launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Wc(m), 1.0 / hh);
+            Ck[m * MAXP + m] = hh;
+        }
+        // pool vectors orthogonalised against the new Lanczos vector
+        for (int q = q_first; q < q_first + q_live; ++q) {
+            Col r{h->pool + q, qc};
+            double c = dots_host(h, n, {Wc(m)}, r)[0];
+            launch_axpy(h, n, {Wc(m)}, &c, nullptr, 1.0, r, 1.0);
+        }
+        if (stop_after) break;
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy((char*)h->st + offsetof(DevState, Ck), Ck.data(), MAXP * MAXP * sizeof(double),
+                  cudaMemcpyHostToDevice));
+    SET_STATE(h, q_first, q_first);
+    SET_STATE(h, q_live, q_live);
+    SET_STATE(h, stop_after, stop_after);
+    SET_STATE(h, slow_given, 1);
+    SET_STATE(h, need_slow, 0);
+    SET_STATE(h, run, 1);
+    (void)o;
+}
+
+// ------------------------------------------------------------------ the solve
+
+struct Inputs {
+    StepPtrs sp;
+    const double* B;
+    long long n;
+};
+
+int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xin, int p, double tol, long long maxit,
+             double tau) {
+    const bminres_options& o = h->opt;
+    if (!A || !Bin || !Xin) fail(h, BMINRES_EINVAL, "null argument");
+    if (o.world != 1) fail(h, BMINRES_EINVAL, "world > 1 is not implemented in this version");
+    const long long n = A->n_loc;
+    if (A->n != A->n_loc || A->row_begin != 0) fail(h, BMINRES_EINVAL, "world = 1 needs n_loc = n, row_begin = 0");
+    if (p < 1 || p > BMINRES_MAX_P || !kfn_for(p, &h->kf)) fail(h, BMINRES_EINVAL, "unsupported block size p");
+    if (n < p) fail(h, BMINRES_EINVAL, "n < p");
+    if (!std::isfinite(tol) || tol < 0 || maxit < 0 || !std::isfinite(tau) || tau < 0)
+        fail(h, BMINRES_EINVAL, "tol / maxit / deflation_tol out of range");
+    if (A->nnz < 0 || A->nnz >= (1ll << 31)) fail(h, BMINRES_EINVAL, "nnz must be < 2^31");
+    const int q = std::max(0, std::min(o.pool_size, MAXQ));
+    if (o.pool_size > MAXQ) fail(h, BMINRES_EINVAL, "pool_size > 8");
+
+    CK(cudaSetDevice(h->device));
+    cudaEvent_t e_solve0, e_solve1, e_loop0, e_loop1;
+    CK(cudaEventCreate(&e_solve0));
+    CK(cudaEventCreate(&e_solve1));
+    CK(cudaEventCreate(&e_loop0));
+    CK(cudaEventCreate(&e_loop1));
+    h->events.clear();
+    for (auto& r : h->retained) cudaFree(r.v);
+    h->retained.clear();
+    h->launches = 0;
+    h->ev_used = 0;
+    h->ev_marks.clear();
+    h->stats = bminres_stats_t{};
+    CK(cudaEventRecord(e_solve0, h->stream));
+
+    // ---- inputs: device pointers are used in place; host pointers are staged
+    StepPtrs sp{};
+    const size_t panel = (size_t)n * p;
+    bool x_host = false;
+    {
+        TimeMark tm(h, PH_OTHER);
+        const bool a_dev = is_device_ptr(A->row_ptr) && is_device_ptr(A->col_idx) && is_device_ptr(A->values);
+        if (a_dev) {
+            sp.rowptr = A->row_ptr;
+            sp.col = A->col_idx;
+            sp.val = A->values;
+        } else {
+            if (h->a_rows_cap < (size_t)n + 1) {
+                dalloc(h, &h->a_rowptr, n + 1);
+                h->a_rows_cap = n + 1;
+            }
+            if (h->a_nnz_cap < (size_t)std::max<long long>(A->nnz, 1)) {
+                dalloc(h, &h->a_col, std::max<long long>(A->nnz, 1));
+                dalloc(h, &h->a_val, std::max<long long>(A->nnz, 1));
+                h->a_nnz_cap = std::max<long long>(A->nnz, 1);
+            }
+            CK(cudaMemcpyAsync(h->a_rowptr, A->row_ptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(h->a_col, A->col_idx, A->nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(h->a_val, A->values, A->nnz * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            sp.rowptr = h->a_rowptr;
+            sp.col = h->a_col;
+            sp.val = h->a_val;
+        }
+        if (!is_device_ptr(Bin)) {
+            if (h->bx_cap < panel) {
+                dalloc(h, &h->bx, panel);
+                h->bx_cap = panel;
+            }
+            CK(cudaMemcpyAsync(h->bx, Bin, panel * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            Bin = h->bx;
+        }
+        if (!is_device_ptr(Xin)) {
+            x_host = true;
+            if (h->xx_cap < panel) {
+                dalloc(h, &h->xx, panel);
+                h->xx_cap = panel;
+            }
+            if (o.use_x0) CK(cudaMemcpyAsync(h->xx, Xin, panel * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            sp.X = h->xx;
+        } else {
+            sp.X = Xin;
+        }
+        if ((((uintptr_t)Bin) | ((uintptr_t)sp.X)) & 15) fail(h, BMINRES_EINVAL, "B and X must be 16-byte aligned");
+    }
+    ensure_workspace(h, n, p, q);
+    const double* B = Bin;
+
+    // ---- history buffer
+    long long hist_cap = o.record_history ? std::min<long long>(maxit + 1, std::max<long long>(1, (8ll << 20) / p)) : 0;
+    if (hist_cap > h->hist_cap) {
+        dalloc(h, &h->hist, (size_t)hist_cap * p);
+        h->hist_cap = hist_cap;
+    }
+
+    // ---- state init
+    DevState init{};
+    init.run = 1;
+    init.status = 1;
+    init.q_first = 0;
+    init.q_live = q;
+    init.pool_cap = std::max(q, 1);
+    init.k = 1;
+    init.j_done = 0;
+    init.maxit = maxit;
+    init.hist_cap = hist_cap;
+    init.tol = tol;
+    init.tau = tau;
+    init.hist = hist_cap ? h->hist : nullptr;
+    init.hflags = h->hf_dev;
+    std::vector<double> S(MAXP * MAXP, 0.0), beta(p, 0.0), f0n(p, 0.0);
+
+    {
+        TimeMark tm(h, PH_START);
+        CK(cudaMemsetAsync(h->M[0], 0, panel * sizeof(double), h->stream));
+        CK(cudaMemsetAsync(h->M[1], 0, panel * sizeof(double), h->stream));
+        if (!o.use_x0) CK(cudaMemsetAsync(sp.X, 0, panel * sizeof(double), h->stream));
+        // beta_i = ||b_i||
+        launch_colsq(h, B, nullptr, n, p, h->dsc);
+        std::vector<double> b2(p);
+        CK(cudaMemcpyAsync(b2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        // F0 = B - A X0 (C6) into the slot of U_1 (k = 1 -> slot 1)
+        double* F = h->U[1];
+        if (o.use_x0) {
+            K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0};
+            h->kf.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
+            check_launch(h, "k1_spmm(plain)");
+            k_sub_from<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(B, F, (long long)panel);
+            check_launch(h, "k_sub_from");
+        } else {
+            CK(cudaMemcpyAsync(F, B, panel * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+        }
+        launch_colsq(h, F, nullptr, n, p, h->dsc);
+        std::vector<double> f2(p);
+        CK(cudaMemcpyAsync(f2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        for (int c = 0; c < p; ++c) {
+            beta[c] = std::sqrt(b2[c]);
+            f0n[c] = std::sqrt(f2[c]);
+        }
+        // thin QR F0 = U_p S with one re-orthogonalisation (classical GS, two passes) and
+        // step-0 deflation (eqn.init-QR; reading C13)
+        long long nrep0 = 0;
+        for (int i = 0; i < p; ++i) {
+            Col fi{F + i, p};
+            std::vector<Col> prev;
+            for (int l = 0; l < i; ++l) prev.push_back(Col{F + l, p});
+            if (i > 0) {
+                for (int pass = 0; pass < 2; ++pass) {
+                    launch_dots(h, n, prev, fi, h->dsc + 8 + pass * MAXP);
+                    launch_axpy(h, n, prev, nullptr, h->dsc + 8 + pass * MAXP, 1.0, fi, 1.0);
+                }
+            }
+            std::vector<double> c2(2 * MAXP, 0.0);
+            if (i > 0)
+                CK(cudaMemcpyAsync(c2.data(), h->dsc + 8, 2 * MAXP * sizeof(double), cudaMemcpyDeviceToHost,
+                                   h->stream));
+            const double hh = std::sqrt(dots_host(h, n, {fi}, fi)[0]);
+            for (int l = 0; l < i; ++l) S[l * MAXP + i] = c2[l] + c2[MAXP + l];
+            if (hh <= tau * f0n[i]) {
+                bminres_event ev{};
+                ev.j = 0;
+                ev.col = i + 1;
+                ev.kind = hh <= 1e-12 * f0n[i] ? 0 : 1;
+                ev.action = 1;
+                ev.ratio = f0n[i] > 0 ? hh / f0n[i] : 0.0;
+                h->events.push_back(ev);
+                S[i * MAXP + i] = 0.0;
+                launch_rand(h, F + i, p, n, A->row_begin, o.seed, 0, (uint64_t)nrep0++);
+                if (i > 0)
+                    for (int pass = 0; pass < 2; ++pass) {
+                        launch_dots(h, n, prev, fi, h->dsc + 8);
+                        launch_axpy(h, n, prev, nullptr, h->dsc + 8, 1.0, fi, 1.0);
+                    }
+                const double rn = std::sqrt(dots_host(h, n, {fi}, fi)[0]);
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, fi, 1.0 / rn);
+            } else {
+                S[i * MAXP + i] = hh;
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, fi, 1.0 / hh);
+            }
+        }
+        // replacement pool (reading C18): drawn now, orthogonalised twice against U_p
+        std::vector<Col> ucols;
+        for (int l = 0; l < p; ++l) ucols.push_back(Col{F + l, p});
+        for (int qq = 0; qq < q; ++qq) {
+            Col r{h->pool + qq, std::max(q, 1)};
+            launch_rand(h, h->pool + qq, std::max(q, 1), n, A->row_begin, o.seed, 1, (uint64_t)qq);
+            for (int pass = 0; pass < 2; ++pass) {
+                launch_dots(h, n, ucols, r, h->dsc + 8);
+                launch_axpy(h, n, ucols, nullptr, h->dsc + 8, 1.0, r, 1.0);
+            }
+        }
+    }
+    // T = S, history[0], while-test (Alg. 2, reading C7)
+    double mx0 = 0.0;
+    std::vector<double> h0(p);
+    for (int c = 0; c < p; ++c) {
+        double s = 0.0;
+        for (int r = 0; r < p; ++r) s += S[r * MAXP + c] * S[r * MAXP + c];
+        h0[c] = beta[c] > 0 ? std::sqrt(s) / beta[c] : 0.0;
+        mx0 = std::max(mx0, h0[c]);
+    }
+    for (int r = 0; r < p; ++r)
+        for (int c = 0; c < p; ++c) init.T[r * MAXP + c] = S[r * MAXP + c];
+    for (int c = 0; c < p; ++c) {
+        init.beta[c] = beta[c];
+        init.res[c] = h0[c];
+    }
+    if (mx0 < tol) {
+        init.status = 0;
+        init.run = 0;
+    }
+    if (maxit == 0 && init.run) {
+        init.status = 1;
+        init.run = 0;
+    }
+    CK(cudaMemcpyAsync(h->st, &init, sizeof(DevState), cudaMemcpyHostToDevice, h->stream));
+    if (hist_cap) CK(cudaMemcpyAsync(h->hist, h0.data(), p * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    h->hf->run = init.run;
+    h->hf->status = init.status;
+    h->hf->need_slow = 0;
+    h->hf->k = 1;
+    h->hf->j_done = 0;
+    CK(cudaStreamSynchronize(h->stream));
+
+    // ---- block-step loop
+    const bool graphs = o.use_graphs && !o.timing;
+    if (graphs && init.run) build_graphs(h, sp, n);
+    CK(cudaEventRecord(e_loop0, h->stream));
+    long long k = 1;               // host mirror of the block index
+    long long block_steps = 0, slow_blocks = 0;
+    const int LAG = 6;
+    std::vector<cudaEvent_t> lag_ev(LAG);
+    for (auto& e : lag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    bool running = init.run != 0;
+    while (running) {
+        // blocks whose iterations meet a live retained vector take the column path
+        const long long j_next = (k - 1) * p + 1;  // valid while no partial block happened
+        bool retained_live = false;
+        for (auto& r : h->retained)
+            if (r.expiry >= j_next) retained_live = true;
+        if (retained_live) {
+            const int slot = (int)(k & 1);
+            launch_k1(h, sp, n, slot);
+            launch_k2(h, n, slot);
+            block_steps++;
+            CK(cudaStreamSynchronize(h->stream));
+            slow_block(h, n, p, k, slot, o, tau, maxit);
+            slow_blocks++;
+            launch_k3(h);
+            launch_k4(h, sp, n, slot);
+            CK(cudaStreamSynchronize(h->stream));
+            k++;
+            if (!h->hf->run) running = false;
+            continue;
+        }
+        // fast path: launch steps ahead, poll flags LAG steps behind
+        long long launched = 0;
+        const long long steps_left = (maxit - (k - 1) * p + p - 1) / p;
+        long long kk = k;
+        bool stop_seen = false;
+        while (launched < steps_left) {
+            const int slot = (int)(kk & 1);
+            if (graphs) {
+                CK(cudaGraphLaunch(h->gexec[slot], h->stream));
+                h->launches += 4;
+            } else {
+                launch_k1(h, sp, n, slot);
+                launch_k2(h, n, slot);
+                launch_k3(h);
+                launch_k4(h, sp, n, slot);
+            }
+            CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
+            launched++;
+            kk++;
+            if (launched >= LAG) {
+                CK(cudaEventSynchronize(lag_ev[launched % LAG]));
+                if (!h->hf->run) {
+                    stop_seen = true;
+                    break;
+                }
+            }
+        }
+        (void)stop_seen;
+        CK(cudaStreamSynchronize(h->stream));
+        const long long kdev = GET_STATE(h, k);
+        const int need_slow = GET_STATE(h, need_slow);
+        const int run = GET_STATE(h, run);
+        block_steps += (kdev - k) + (need_slow ? 1 : 0);
+        k = kdev;
+        if (need_slow) {
+            const int slot = (int)(k & 1);
+            slow_block(h, n, p, k, slot, o, tau, maxit);
+            slow_blocks++;
+            launch_k3(h);
+            launch_k4(h, sp, n, slot);
+            CK(cudaStreamSynchronize(h->stream));
+            k = GET_STATE(h, k);
+            if (!GET_STATE(h, run)) running = false;
+            continue;
+        }
+        if (!run) running = false;
+    }
+    CK(cudaEventRecord(e_loop1, h->stream));
+    for (auto& e : lag_ev) cudaEventDestroy(e);
+
+    // ---- exit: status, true residuals (K7), history, copy-back
+    DevState fin;
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(&fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    {
+        TimeMark tm(h, PH_RESID);
+        K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->W, n, h->st, nullptr, 0};
+        h->kf.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
+        check_launch(h, "k1_spmm(plain)");
+        launch_colsq(h, B, h->W, n, p, h->dsc);
+    }
+    std::vector<double> r2(p);
+    CK(cudaMemcpyAsync(r2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    if (x_host) CK(cudaMemcpyAsync(Xin, sp.X, panel * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaEventRecord(e_solve1, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    bminres_stats_t& s = h->stats;
+    s.status = fin.status;
+    s.p = p;
+    s.n = n;
+    s.iterations = fin.j_done;
+    s.block_steps = block_steps;
+    s.slow_blocks = slow_blocks;
+    s.n_events = (int64_t)h->events.size();
+    for (int c = 0; c < p; ++c) {
+        s.comp_res[c] = fin.res[c];
+        s.true_res[c] = beta[c] > 0 ? std::sqrt(r2[c]) / beta[c] : 0.0;
+    }
+    s.history_len = std::min<long long>(fin.j_done + 1, hist_cap);
+    h->hist_host.assign((size_t)s.history_len * p, 0.0);
+    if (s.history_len)
+        CK(cudaMemcpy(h->hist_host.data(), h->hist, h->hist_host.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e_solve0, e_solve1));
+    s.solve_ms = ms;
+    CK(cudaEventElapsedTime(&ms, e_loop0, e_loop1));
+    s.loop_ms = ms;
+    for (auto& mk : h->ev_marks) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, h->evpool[mk.second], h->evpool[mk.second + 1]));
+        s.phase_ms[mk.first] += t;
+        s.phase_launches[mk.first] += 1;
+    }
+    s.gpu_launches = h->launches;
+    const double abytes = 12.0 * A->nnz + 4.0 * (n + 1);
+    s.bytes_per_block_step = abytes + 10.0 * 8.0 * (double)panel;
+    s.spmm_bytes_per_launch = abytes + 3.0 * 8.0 * (double)panel;
+    cudaEventDestroy(e_solve0);
+    cudaEventDestroy(e_solve1);
+    cudaEventDestroy(e_loop0);
+    cudaEventDestroy(e_loop1);
+    for (auto& r : h->retained) cudaFree(r.v);
+    h->retained.clear();
+    return fin.status;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+
+extern "C" {
+
+void bminres_default_options(bminres_options* opt) {
+    if (!opt) return;
+    std::memset(opt, 0, sizeof(*opt));
+    opt->device = 0;
+    opt->rank = 0;
+    opt->world = 1;
+    opt->stream = nullptr;
+    opt->seed = 0;
+    opt->pool_size = 1;
+    opt->use_x0 = 0;
+    opt->record_history = 1;
+    opt->use_graphs = 1;
+    opt->timing = 0;
+}
+
+int bminres_create(const bminres_options* opt, bminres_handle* out) {
+    if (!out) return BMINRES_EINVAL;
+    *out = nullptr;
+    bminres_options o;
+    if (opt)
+        o = *opt;
+    else
+        bminres_default_options(&o);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        g_create_err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        return BMINRES_ECUDA;
+    }
+    if (o.device < 0 || o.device >= ndev) {
+        g_create_err = "bad device ordinal";
+        return BMINRES_EINVAL;
+    }
+    auto* h = new bminres_ctx();
+    h->opt = o;
+    h->device = o.device;
+    try {
+        CK(cudaSetDevice(o.device));
+        CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, o.device));
+        if (o.stream) {
+            h->stream = (cudaStream_t)o.stream;
+        } else {
+            CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->own_stream = true;
+        }
+        // large dynamic shared memory for the p = 32 kernels
+        for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 16, 32}) {
+            Kfn f;
+            kfn_for(p, &f);
+            CK(cudaFuncSetAttribute((const void*)f.k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
+            CK(cudaFuncSetAttribute((const void*)f.k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4));
+        }
+    } catch (Err& x) {
+        g_create_err = h->err;
+        delete h;
+        return x.code;
+    }
+    *out = h;
+    return BMINRES_OK;
+}
+
+int bminres_solve(bminres_handle h, const bminres_csr* A, const double* B, double* X, int32_t p, double tol,
+                  int64_t maxit, double deflation_tol) {
+    if (!h) return BMINRES_EINVAL;
+    try {
+        int r = do_solve(h, A, B, X, p, tol, maxit, deflation_tol);
+        h->stats.status = r;
+        return r;
+    } catch (Err& x) {
+        h->stats.status = x.code;
+        return x.code;
+    }
+}
+
+int bminres_stats(bminres_handle h, bminres_stats_t* out) {
+    if (!h || !out) return BMINRES_EINVAL;
+    *out = h->stats;
+    return BMINRES_OK;
+}
+
+int64_t bminres_get_history(bminres_handle h, double* buf, int64_t cap) {
+    if (!h || !buf || cap <= 0) return 0;
+    int64_t rows = std::min<int64_t>(cap, h->stats.history_len);
+    std::memcpy(buf, h->hist_host.data(), (size_t)rows * h->stats.p * sizeof(double));
+    return rows;
+}
+
+int64_t bminres_get_events(bminres_handle h, bminres_event* buf, int64_t cap) {
+    if (!h || !buf || cap <= 0) return 0;
+    int64_t c = std::min<int64_t>(cap, (int64_t)h->events.size());
+    std::memcpy(buf, h->events.data(), (size_t)c * sizeof(bminres_event));
+    return c;
+}
+
+int bminres_spmm(bminres_handle h, const bminres_csr* A, const double* X, double* Y, int32_t p) {
+    if (!h || !A || !X || !Y) return BMINRES_EINVAL;
+    try {
+        Kfn f;
+        if (!kfn_for(p, &f)) fail(h, BMINRES_EINVAL, "unsupported block size p");
+        if (!is_device_ptr(A->row_ptr) || !is_device_ptr(A->col_idx) || !is_device_ptr(A->values) ||
+            !is_device_ptr(X) || !is_device_ptr(Y))
+            fail(h, BMINRES_EINVAL, "bminres_spmm takes device pointers");
+        if ((((uintptr_t)X) | ((uintptr_t)Y)) & 15) fail(h, BMINRES_EINVAL, "X and Y must be 16-byte aligned");
+        CK(cudaSetDevice(h->device));
+        const long long n = A->n_loc;
+        K1Args a{A->row_ptr, A->col_idx, A->values, X, nullptr, Y, n, nullptr, nullptr, 0};
+        f.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
+        check_launch(h, "k1_spmm(plain)");
+        CK(cudaStreamSynchronize(h->stream));
+        return BMINRES_OK;
+    } catch (Err& x) {
+        return x.code;
+    }
+}
+
+int bminres_random_vector(bminres_handle h, uint64_t seed, uint64_t stream, uint64_t event, int64_t row_begin,
+                          int64_t n_loc, double* out, int64_t stride) {
+    if (!h || !out) return BMINRES_EINVAL;
+    try {
+        if (!is_device_ptr(out)) fail(h, BMINRES_EINVAL, "bminres_random_vector takes a device pointer");
+        CK(cudaSetDevice(h->device));
+        launch_rand(h, out, stride, n_loc, row_begin, seed, stream, event);
+        CK(cudaStreamSynchronize(h->stream));
+        return BMINRES_OK;
+    } catch (Err& x) {
+        return x.code;
+    }
+}
+
+size_t bminres_workspace_bytes(int64_t n_loc, int32_t p, int32_t pool_size) {
+    return sizeof(double) * ((size_t)n_loc * p * 5 + (size_t)n_loc * std::max(pool_size, 1)) +
+           sizeof(double) * (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8) + sizeof(DevState);
+}
+
+const char* bminres_last_error(bminres_handle h) {
+    if (!h) return g_create_err.c_str();
+    return h->err.c_str();
+}
+
+void bminres_destroy(bminres_handle h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    for (int s = 0; s < 2; ++s)
+        if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
+    for (double* p : {h->U[0], h->U[1], h->M[0], h->M[1], h->W, h->pool, h->part, h->dsc, h->a_val, h->bx, h->xx,
+                      h->hist})
+        if (p) cudaFree(p);
+    if (h->a_rowptr) cudaFree(h->a_rowptr);
+    if (h->a_col) cudaFree(h->a_col);
+    if (h->dcnt) cudaFree(h->dcnt);
+    if (h->st) cudaFree(h->st);
+    if (h->hf) cudaFreeHost(h->hf);
+    for (auto& r : h->retained) cudaFree(r.v);
+    for (auto& e : h->evpool) cudaEventDestroy(e);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // extern "C"

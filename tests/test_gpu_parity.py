@@ -1,0 +1,270 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle — needs a B200.
+
+Bars (north star, BASELINE.json): per-iteration residual histories agree to relative
+1e-9 over the first 50 iterations; iteration counts within +-2% or +-2; dependence events
+at the same steps; final true residual <= tol where the problem allows it.  Integer /
+bit-level work (the SpMM summation order, the replacement RNG) is compared bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+HIST_RTOL = 1e-9
+HIST_ATOL = 1e-14   # residuals that are rounding noise (e.g. a converged column at 1e-17)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@pytest.fixture(scope="module")
+def solver():
+    from paper_1301_2102_b200 import Solver
+    s = Solver(0, pool_size=1)
+    yield s
+    s.close()
+
+
+def gpu_solve(A, B, *, pool_size=1, use_graphs=True, X0=None, **kw):
+    torch = _torch()
+    from paper_1301_2102_b200 import DeviceCsr, Solver
+    dA = DeviceCsr.from_host(A, "cuda:0")
+    dB = torch.from_numpy(np.ascontiguousarray(B)).to("cuda:0")
+    X = None if X0 is None else torch.from_numpy(np.ascontiguousarray(X0)).to("cuda:0")
+    with Solver(0, pool_size=pool_size, use_graphs=use_graphs, use_x0=X0 is not None) as s:
+        r = s.solve(dA, dB, X, raise_on_error=False, **kw)
+    r.X = r.X.cpu().numpy()
+    return r
+
+
+def assert_hist_close(h_gpu, h_ref, upto=50):
+    k = min(upto + 1, len(h_gpu), len(h_ref))
+    a, b = h_gpu[:k], h_ref[:k]
+    bad = np.abs(a - b) > HIST_RTOL * np.abs(b) + HIST_ATOL
+    assert not bad.any(), f"history mismatch at {np.argwhere(bad)[:5].tolist()}: " \
+                          f"max rel {np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)):.3e}"
+
+
+def assert_counts_close(it_gpu, it_ref):
+    assert abs(it_gpu - it_ref) <= max(2, 0.02 * it_ref), (it_gpu, it_ref)
+
+
+def same_events(eg, er):
+    key = lambda e: (e["j"], e["col"], e["kind"], e["action"])
+    assert [key(e) for e in eg] == [key(e) for e in er], (eg, er)
+
+
+# ----------------------------------------------------------------------------- component parity
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 16, 32])
+def test_spmm_bitwise(solver, p):
+    """Row a1's SpMM: each output row summed over the CSR row in stored order with fma — bitwise."""
+    torch = _torch()
+    from paper_1301_2102_b200 import DeviceCsr
+    for A in (synth.laplacian_3d(13, 11, 9, shift=3.0), synth.random_sym_sparse(777, 0.02, seed=p)):
+        X = np.random.default_rng(p).standard_normal((A.n, p))
+        Y = solver.spmm(DeviceCsr.from_host(A, "cuda:0"), torch.from_numpy(X).cuda()).cpu().numpy()
+        np.testing.assert_array_equal(Y, oracle.csr_block(A, X))
+
+
+@pytest.mark.parametrize("cfg,p", [(2, 8), (3, 16)])
+def test_spmm_full_size_bitwise(solver, cfg, p):
+    torch = _torch()
+    from paper_1301_2102_b200 import DeviceCsr
+    A = synth.laplacian_3d(64, shift=3.0) if cfg == 2 else synth.laplacian_2d(512, shift=2.5)
+    X = np.random.default_rng(1).standard_normal((A.n, p))
+    Y = solver.spmm(DeviceCsr.from_host(A, "cuda:0"), torch.from_numpy(X).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(Y, oracle.csr_block(A, X))
+
+
+def test_random_vector_bitwise(solver):
+    """Reading C17: the replacement vectors are an integer hash -> bitwise equal to the oracle's."""
+    torch = _torch()
+    n = 5000
+    out = torch.empty(n, dtype=torch.float64, device="cuda:0")
+    for (seed, stream, event, rb) in ((0, 0, 0, 0), (0, 1, 3, 0), (7, 1, 2, 123456)):
+        solver.random_vector(seed, stream, event, rb, n, out)
+        want = np.array([oracle.rand_entry(seed, stream, event, rb + i) for i in range(n)])
+        np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+# ----------------------------------------------------------------------------- solve parity
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 16, 32])
+def test_history_parity_small(p):
+    A = synth.laplacian_2d(40, 37, shift=1.7)
+    B = synth.gaussian_rhs(A.n, p, seed=p)
+    r = gpu_solve(A, B, tol=0.0, maxit=60)
+    ref = oracle.solve(A, B, tol=0.0, maxit=60)
+    assert r.status_name == ref.status_name == "MAXIT"
+    assert r.iterations == ref.iterations == 60
+    assert_hist_close(r.history, ref.history)
+    np.testing.assert_allclose(r.X, ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+
+
+def test_companion_converges_like_oracle():
+    """Config 1' (non-singular companion): counts within +-2%, true residual <= tol."""
+    P = synth.config("1c")
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=P.maxit)
+    ref = oracle.solve(P.A, P.B, tol=P.tol, maxit=P.maxit)
+    assert r.status_name == ref.status_name == "OK"
+    assert_counts_close(r.iterations, ref.iterations)
+    assert_hist_close(r.history, ref.history)
+    assert max(r.stats["true_res"]) <= P.tol * 1.5
+
+
+def test_config1_singular():
+    """Config 1 is singular: both run to maxit; histories agree over 50 iterations;
+    the residual reaches the null-space floor (pin P14)."""
+    P = synth.config(1)
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=P.maxit)
+    ref = oracle.solve(P.A, P.B, tol=P.tol, maxit=P.maxit)
+    assert r.status_name == ref.status_name == "MAXIT"
+    assert r.iterations == ref.iterations == P.maxit
+    assert_hist_close(r.history, ref.history)
+    np.testing.assert_allclose(r.history[1100], [0.04458, 0.03019, 0.003486, 0.01999], rtol=1e-3)
+
+
+def test_x0_path():
+    P = synth.config("1c")
+    X0 = np.random.default_rng(3).standard_normal(P.B.shape) * 0.1
+    r = gpu_solve(P.A, P.B, X0=X0, tol=0.0, maxit=40)
+    ref = oracle.solve(P.A, P.B, X0=X0, tol=0.0, maxit=40)
+    assert_hist_close(r.history, ref.history)
+    np.testing.assert_allclose(r.X, ref.X, rtol=1e-8, atol=1e-10)
+
+
+# ----------------------------------------------------------------------------- dependence handling
+
+
+def test_fig3_dependence_at_first_iteration():
+    """Fig. 3: B = [e1, A e1] -> exact dependence at j = 1, system 2 converged."""
+    P = synth.config(1)
+    D = synth.csr_to_dense(P.A)
+    e1 = np.zeros(P.n)
+    e1[0] = 1.0
+    B = np.stack([e1, D @ e1], axis=1)
+    r = gpu_solve(P.A, B, tol=1e-8, maxit=300, pool_size=1)
+    ref = oracle.solve(P.A, B, tol=1e-8, maxit=300, pool_size=1)
+    same_events(r.events, ref.events)
+    assert r.events[0]["j"] == 1
+    assert_hist_close(r.history, ref.history)
+    assert r.history[1:, 1].max() < 1e-14
+
+
+def test_step0_deflation_events():
+    """Config-3 recipe (small): step-0 events for the dependent columns, as the oracle."""
+    A = synth.laplacian_2d(30, shift=2.5)
+    for eps in (0.0, 1e-10, 1e-6):
+        B = synth.dependent_rhs(A.n, 4, eps, seed=0)
+        r = gpu_solve(A, B, tol=1e-8, maxit=80)
+        ref = oracle.solve(A, B, tol=1e-8, maxit=80)
+        same_events(r.events, ref.events)
+        assert_hist_close(r.history, ref.history)
+
+
+def test_near_dependence_retention():
+    """Near dependence (1e-12 < h/omega <= tau): replaced + retained for 2p iterations."""
+    P = synth.config("1c")
+    D = synth.csr_to_dense(P.A)
+    rng = np.random.default_rng(1)
+    b = rng.standard_normal(P.n)
+    B = np.stack([b, D @ b + 1e-10 * rng.standard_normal(P.n)], axis=1)
+    r = gpu_solve(P.A, B, tol=1e-8, maxit=30, pool_size=1)
+    ref = oracle.solve(P.A, B, tol=1e-8, maxit=30, pool_size=1)
+    same_events(r.events, ref.events)
+    assert r.events[0]["action"] == 2
+    assert_hist_close(r.history, ref.history, upto=30)
+
+
+def test_block_grade_stall():
+    """Pin P9 on the GPU: dependent candidates at j = (d-1)p+1..dp, convergence at dp."""
+    d, p, mult = 4, 2, 10
+    A = synth.diag_csr(np.repeat([-2.0, -0.5, 1.0, 3.0], mult))
+    B = np.random.default_rng(9).standard_normal((d * mult, p))
+    r = gpu_solve(A, B, tol=1e-12, maxit=40, pool_size=p)
+    ref = oracle.solve(A, B, tol=1e-12, maxit=40, pool_size=p)
+    same_events(r.events, ref.events)
+    assert r.status_name == ref.status_name == "OK" and r.iterations == ref.iterations == d * p
+
+
+def test_pool_exhausted():
+    P = synth.config(1)
+    D = synth.csr_to_dense(P.A)
+    e1 = np.zeros(P.n)
+    e1[0] = 1.0
+    B = np.stack([e1, D @ e1], axis=1)
+    r = gpu_solve(P.A, B, tol=1e-8, maxit=10, pool_size=0)
+    ref = oracle.solve(P.A, B, tol=1e-8, maxit=10, pool_size=0)
+    assert r.status_name == ref.status_name == "EPOOL"
+    assert r.iterations == ref.iterations == 1
+
+
+def test_predicted_dependence_steps():
+    """Pin P8 on the GPU: B = [b, A^t b] -> first event at j = 2t-1."""
+    for t in (1, 2, 3):
+        rng = np.random.default_rng(40 + t)
+        n = 12
+        M = rng.integers(-3, 4, (n, n))
+        Aint = np.triu(M) + np.triu(M, 1).T
+        b = rng.integers(-2, 3, n)
+        bt = b.copy()
+        for _ in range(t):
+            bt = Aint @ bt
+        B = np.stack([b, bt], axis=1).astype(float)
+        A = synth.dense_to_csr(Aint.astype(float))
+        r = gpu_solve(A, B, tol=0.0, maxit=2 * t + 1, pool_size=2)
+        assert r.events and r.events[0]["j"] == 2 * t - 1
+
+
+# ----------------------------------------------------------------------------- full-size configs
+
+
+def test_config2_first_50():
+    """Config 2 (BASELINE configs[1], the bench workload) at full size: 50 iterations vs oracle."""
+    P = synth.config(2)
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=50)
+    ref = oracle.solve(P.A, P.B, tol=P.tol, maxit=50)
+    assert r.iterations == ref.iterations == 50
+    assert_hist_close(r.history, ref.history)
+    np.testing.assert_allclose(r.X, ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-10, 1e-6])
+def test_config3_first_50(eps):
+    """Config 3 (dependent RHS, BASELINE configs[2]) at full size: step-0 events + 50 iterations."""
+    P = synth.config(3, eps=eps)
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=50)
+    ref = oracle.solve(P.A, P.B, tol=P.tol, maxit=50)
+    same_events(r.events, ref.events)
+    assert len([e for e in r.events if e["j"] == 0]) == (8 if eps < 1e-8 else 0)
+    assert_hist_close(r.history, ref.history)
+
+
+# ----------------------------------------------------------------------------- API properties
+
+
+def test_graphs_plain_and_host_pointers_bitwise():
+    """Graph replay, plain launches and the host-pointer (e2e) path give bitwise-identical results."""
+    from paper_1301_2102_b200 import Solver
+    P = synth.config("1c")
+    r1 = gpu_solve(P.A, P.B, tol=0.0, maxit=100, use_graphs=True)
+    r2 = gpu_solve(P.A, P.B, tol=0.0, maxit=100, use_graphs=False)
+    with Solver(0) as s:
+        r3 = s.solve(P.A, P.B, np.zeros_like(P.B), tol=0.0, maxit=100)
+    np.testing.assert_array_equal(r1.history, r2.history)
+    np.testing.assert_array_equal(r1.X, r2.X)
+    np.testing.assert_array_equal(r1.X, r3.X)
+
+
+def test_invalid_arguments():
+    P = synth.config("1c")
+    assert gpu_solve(P.A, np.ones((P.n, 9)), tol=1e-8, maxit=10).status_name == "EINVAL"  # p = 9 not compiled
+    assert gpu_solve(P.A, P.B, tol=float("nan"), maxit=10).status_name == "EINVAL"
