@@ -42,10 +42,10 @@ def gpu_solve(A, B, *, pool_size=1, use_graphs=True, X0=None, **kw):
     return r
 
 
-def assert_hist_close(h_gpu, h_ref, upto=50):
+def assert_hist_close(h_gpu, h_ref, upto=50, rtol=HIST_RTOL):
     k = min(upto + 1, len(h_gpu), len(h_ref))
     a, b = h_gpu[:k], h_ref[:k]
-    bad = np.abs(a - b) > HIST_RTOL * np.abs(b) + HIST_ATOL
+    bad = np.abs(a - b) > rtol * np.abs(b) + HIST_ATOL
     assert not bad.any(), f"history mismatch at {np.argwhere(bad)[:5].tolist()}: " \
                           f"max rel {np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)):.3e}"
 
@@ -181,7 +181,11 @@ def test_near_dependence_retention():
     ref = oracle.solve(P.A, B, tol=1e-8, maxit=30, pool_size=1)
     same_events(r.events, ref.events)
     assert r.events[0]["action"] == 2
-    assert_hist_close(r.history, ref.history, upto=30)
+    # The retained vector v = w/h is the normalised remainder of a cancellation of relative
+    # size h/omega ~ 4e-11: any two correct implementations (CGS vs MGS order) agree on v only
+    # to eps_mach/(h/omega) ~ 6e-6, and the histories to about that (reading R3).
+    ratio = r.events[0]["ratio"]
+    assert_hist_close(r.history, ref.history, upto=30, rtol=10 * 2.2e-16 / ratio)
 
 
 def test_block_grade_stall():
