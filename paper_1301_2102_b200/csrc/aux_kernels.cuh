@@ -1,0 +1,156 @@
+// aux_kernels.cuh -- generic column kernels: start block (eqn.init-QR), the column-by-column
+// path of a block with a dependent candidate, norms, replacement RNG.
+// Rare or once per solve; deterministic reductions.
+#pragma once
+#include "common.cuh"
+
+namespace bmr {
+
+// ------------------------------------------------------------------ generic column kernels
+// (start block, column-by-column path, norms).  Rare or once per solve.
+
+constexpr int MAXREF = 80;
+struct VecRef {
+    const double* p;
+    long long stride;
+};
+
+// out[k] = sum_i v_k[i] * t[i], k < K (deterministic)
+struct DotArgs {
+    VecRef v[MAXREF];
+    int K;
+    const double* t;
+    long long ts;
+    long long n;
+    double* part;
+    int nb;
+    double* out;
+    unsigned* cnt;
+};
+
+__global__ void __launch_bounds__(256) k_dots(DotArgs a) {
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    __shared__ double sred[8][33];
+    for (int k0 = 0; k0 < a.K; k0 += 32) {
+        const int k = k0 + tx;
+        double s = 0.0;
+        if (k < a.K) {
+            const double* vp = a.v[k].p;
+            const long long vs = a.v[k].stride;
+            for (long long i = (long long)blockIdx.x * 8 + ty; i < a.n; i += (long long)gridDim.x * 8)
+                s = fma(vp[i * vs], a.t[i * a.ts], s);
+        }
+        sred[ty][tx] = s;
+        __syncthreads();
+        if (ty == 0 && k < a.K) {
+            double r = 0.0;
+            for (int y = 0; y < 8; ++y) r += sred[y][tx];
+            a.part[(size_t)k * a.nb + blockIdx.x] = r;
+        }
+        __syncthreads();
+    }
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.cnt, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int e = ty; e < a.K; e += 8) {
+        double s = 0.0;
+        for (int b = tx; b < a.nb; b += 32) s += __ldcg(a.part + (size_t)e * a.nb + b);
+        s = warp_sum(s);
+        if (tx == 0) a.out[e] = s;
+    }
+    if (threadIdx.x == 0) *a.cnt = 0u;
+}
+
+// t[i] = scale * (t[i] - sum_k c_k v_k[i]); c_k from cdev (times csign) if non-null else cval
+struct AxpyArgs {
+    VecRef v[MAXREF];
+    double cval[MAXREF];
+    const double* cdev;
+    double csign;
+    int K;
+    double* t;
+    long long ts;
+    long long n;
+    const double* scale_dev;   // if non-null: scale = 1/sqrt(*scale_dev) (normalisation)
+    double scale;
+};
+
+__global__ void __launch_bounds__(256) k_axpy(AxpyArgs a) {
+    __shared__ double sc[MAXREF];
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) sc[k] = a.cdev ? a.csign * a.cdev[k] : a.cval[k];
+    __syncthreads();
+    const double scale = a.scale_dev ? 1.0 / sqrt(*a.scale_dev) : a.scale;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (long long)gridDim.x * blockDim.x) {
+        double t = a.t[i * a.ts];
+        for (int k = 0; k < a.K; ++k) t = fma(-sc[k], a.v[k].p[i * a.v[k].stride], t);
+        a.t[i * a.ts] = scale == 0.0 ? 0.0 : t * scale;
+    }
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+    unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// random replacement vector (reading C17): integer hash, one exact scaling -> bitwise reproducible
+__global__ void k_rand(double* out, long long stride, long long n, long long row_begin, unsigned long long seed,
+                       unsigned long long stream, unsigned long long event) {
+    const unsigned long long key = splitmix64(seed ^ (stream << 56) ^ (event << 32));
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long x = splitmix64(key ^ (unsigned long long)(row_begin + i));
+        out[i * stride] = 2.0 * ((double)(x >> 11) * 0x1.0p-53) - 1.0;
+    }
+}
+
+// out[c] = sum_i (X[i,c] - Y[i,c])^2 for a row-major n x P panel pair (Y may be null)
+__global__ void __launch_bounds__(256) k_colsq(const double* X, const double* Y, long long n, int P, double* part,
+                                               int nb, double* out, unsigned* cnt) {
+    __shared__ double sred[256];
+    const int R = 256 / P;
+    const int c = threadIdx.x % P, r0 = threadIdx.x / P;
+    double s = 0.0;
+    if (r0 < R) {
+        for (long long i = (long long)blockIdx.x * R + r0; i < n; i += (long long)gridDim.x * R) {
+            const double d = X[i * P + c] - (Y ? Y[i * P + c] : 0.0);
+            s = fma(d, d, s);
+        }
+    }
+    sred[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < P) {
+        double r = 0.0;
+        for (int y = 0; y < R; ++y) r += sred[y * P + threadIdx.x];
+        part[(size_t)threadIdx.x * nb + blockIdx.x] = r;
+    }
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int e = warp; e < P; e += 8) {
+        double t = 0.0;
+        for (int b = lane; b < nb; b += 32) t += __ldcg(part + (size_t)e * nb + b);
+        t = warp_sum(t);
+        if (lane == 0) out[e] = t;
+    }
+    if (threadIdx.x == 0) *cnt = 0u;
+}
+
+// Y = B - Y (row-major panels, same shape)
+__global__ void k_sub_from(const double* B, double* Y, long long total) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        Y[e] = B[e] - Y[e];
+}
+
+
+
+}  // namespace bmr

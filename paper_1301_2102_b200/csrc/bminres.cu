@@ -1,13 +1,15 @@
 // bminres.cu -- host driver and C ABI (include/bminres.h) of the B200 block-MINRES hot path.
 //
-// One block step k (p banded iterations) is four kernels on one stream:
-//   K1 SpMM+epilogue -> K2 orthogonalisation+Grams -> K3 small banded QR (one warp) -> K4 updates
-// replayed as a CUDA graph (two graphs, one per panel-slot parity).  The host never waits
-// per step: K3 publishes run/status flags into mapped pinned memory and the host polls the
-// flags of the step launched LAG steps earlier.  Rare events (a breakdown, a Cholesky
-// cancellation, live retained vectors) halt the step after K2 and
-// the host runs the column-by-column path (the paper's per-iteration order) with small
-// GPU kernels, then resumes.
+// One block step k (p banded iterations) is a main branch and a side branch:
+//   main  K1 SpMM+epilogue -> K2 orthogonalisation, Grams, Cholesky (C_k) -> K4a U_{k+1}
+//   side  K3b small banded QR (z_j, residuals, stop) -> K4b directions M_k and X
+// In steady state one CUDA graph per block runs {main of block s+1} || {side of block s} and
+// joins before K4a (two graphs, one per panel-slot parity), so the serial small QR hides
+// behind the next SpMM.  The host never waits per step: kernels publish flags into mapped
+// pinned memory and the host polls the flags of the graph launched LAG graphs earlier.  Rare
+// events (a breakdown, a Cholesky cancellation, live retained vectors; P:562-577,
+// P:791-801) stop the main branch after K2 and the host runs the column-by-column path (the
+// paper's per-iteration order) with small GPU kernels, then resumes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,8 +20,9 @@
 #include <vector>
 
 #include "../../include/bminres.h"
+#include "aux_kernels.cuh"
 #include "common.cuh"
-#include "kernels.cuh"
+#include "step_kernels.cuh"
 
 using namespace bmr;
 
@@ -36,9 +39,10 @@ struct Kfn {  // per-p kernel table
     void (*k1)(K1Args);
     void (*k1plain)(K1Args);
     void (*k2)(K2Args);
-    void (*k3)(DevState*);
-    void (*k4)(K4Args);
-    size_t smem3, smem4;
+    void (*k3b)(DevState*);
+    void (*k4a)(K4aArgs);
+    void (*k4b)(K4bArgs);
+    size_t smem2, smem3, smem4b;
 };
 
 template <int P>
@@ -47,11 +51,12 @@ Kfn make_kfn() {
     f.k1 = k1_spmm<P, true>;
     f.k1plain = k1_spmm<P, false>;
     f.k2 = k2_orth<P>;
-    f.k3 = k3_smallqr<P>;
-    f.k4 = k4_update<P>;
-    constexpr int LD = P + 1, W2 = 2 * P + 1;
-    f.smem3 = sizeof(double) * (5 * P * LD + 4 * P * LD + W2 * (P + 2) + P);
-    f.smem4 = sizeof(double) * (5 * P * P + P * MAXQ + (NT / 32) * 6 * PC<P>::RPW * P);
+    f.k3b = k3b_smallqr<P>;
+    f.k4a = k4a_basis<P>;
+    f.k4b = k4b_update<P>;
+    f.smem2 = K2Smem<P>::bytes;
+    f.smem3 = K3Smem<P>::bytes;
+    f.smem4b = K4bSmem<P>::bytes;
     return f;
 }
 
@@ -82,6 +87,8 @@ struct bminres_ctx {
     int device = 0;
     int n_sm = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;   // side branch during graph capture
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     std::string err;
     // workspace
@@ -121,7 +128,8 @@ struct bminres_ctx {
     std::vector<cudaEvent_t> evpool;
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> ev_marks;   // (phase, index of start event)
-    int nb1 = 0, nb4 = 0;
+    int nb1 = 0, nb2 = 0, nb4 = 0;
+    long long side_blocks = 0, slow_blocks = 0;
     Kfn kf{};
 };
 
@@ -207,6 +215,49 @@ int grid_for(bminres_ctx* h, long long items, int per_block, int cap) {
 
 // ------------------------------------------------------------------ workspace
 
+int cluster_grid(bminres_ctx* h, const void* fn, size_t smem, long long n, long long rows_per_cta) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL * 64);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl <= 0) {
+        cudaGetLastError();
+        ncl = std::max(1, h->n_sm / CL);
+    }
+    long long need = (n + rows_per_cta - 1) / std::max<long long>(1, rows_per_cta);
+    long long cl_need = std::max<long long>(1, (need + CL - 1) / CL);
+    ncl = (int)std::min<long long>(ncl, cl_need);
+    ncl = std::min(ncl, NB_MAX / CL);
+    return ncl * CL;
+}
+
+template <typename K, typename A>
+void launch_cluster(bminres_ctx* h, K kern, int grid, size_t smem, A args, const char* what) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
+    if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    h->launches++;
+}
+
 void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     if (h->n_ws == n && h->p_ws == p && h->q_ws == q) return;
     for (int s = 0; s < 2; ++s) {
@@ -235,14 +286,12 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     h->n_ws = n;
     h->p_ws = p;
     h->q_ws = q;
-    // grid of the reducing panel kernels: up to 2 CTAs per SM (bounded partial count)
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)h->kf.k1, NT, 0);
-    occ = std::max(1, std::min(occ, 2));
+    // grids of the reducing panel kernels: as many whole clusters of CL CTAs as can be resident
     long long rows_per_cta = (long long)(NT / 32) * (32 / std::max(1, (p % 2 == 0 ? p / 2 : p)));
-    h->nb1 = grid_for(h, n, (int)std::max<long long>(1, rows_per_cta), std::min(NB_MAX, h->n_sm * occ));
+    h->nb1 = cluster_grid(h, (const void*)h->kf.k1, 0, n, rows_per_cta);
+    h->nb2 = cluster_grid(h, (const void*)h->kf.k2, h->kf.smem2, n, rows_per_cta);
     int occ4 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, (const void*)h->kf.k4, NT, h->kf.smem4);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, (const void*)h->kf.k4b, NT, h->kf.smem4b);
     occ4 = std::max(1, occ4);
     h->nb4 = grid_for(h, n, (int)std::max<long long>(1, rows_per_cta), h->n_sm * occ4);
 }
@@ -325,58 +374,74 @@ struct StepPtrs {
     double* X;
 };
 
-void launch_k1(bminres_ctx* h, const StepPtrs& sp, long long n, int slot) {
+// main branch, block with parity par: U_k = U[par], U_{k-1} = U[par^1], U_{k+1} -> U[par^1]
+void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, int par) {
     TimeMark tm(h, PH_SPMM);
-    K1Args a{sp.rowptr, sp.col, sp.val, h->U[slot], h->U[slot ^ 1], h->W, n, h->st, h->part, h->nb1};
-    h->kf.k1<<<h->nb1, NT, 0, h->stream>>>(a);
-    check_launch(h, "k1_spmm");
+    K1Args a{sp.rowptr, sp.col, sp.val, h->U[par], h->U[par ^ 1], h->W, n, h->st, h->part, par};
+    cudaStream_t keep = h->stream;
+    h->stream = s;
+    launch_cluster(h, h->kf.k1, h->nb1, 0, a, "k1_spmm");
+    h->stream = keep;
 }
-void launch_k2(bminres_ctx* h, long long n, int slot) {
+void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, int par) {
     TimeMark tm(h, PH_ORTH);
-    K2Args a{h->W, h->U[slot], h->pool, n, h->st, h->part, h->nb1};
-    h->kf.k2<<<h->nb1, NT, 0, h->stream>>>(a);
-    check_launch(h, "k2_orth");
+    K2Args a{h->W, h->U[par], h->pool, n, h->st, h->part + (size_t)NB_MAX * (MAXP * MAXP + MAXP), par};
+    cudaStream_t keep = h->stream;
+    h->stream = s;
+    launch_cluster(h, h->kf.k2, h->nb2, h->kf.smem2, a, "k2_orth");
+    h->stream = keep;
 }
-void launch_k3(bminres_ctx* h) {
-    TimeMark tm(h, PH_SMALLQR);
-    h->kf.k3<<<1, 32, h->kf.smem3, h->stream>>>(h->st);
-    check_launch(h, "k3_smallqr");
-}
-void launch_k4(bminres_ctx* h, const StepPtrs& sp, long long n, int slot) {
+void launch_k4a(bminres_ctx* h, cudaStream_t s, long long n, int par) {
     TimeMark tm(h, PH_UPDATE);
-    K4Args a{h->W, h->U[slot], h->U[slot ^ 1], h->M[slot], h->M[slot ^ 1], sp.X, h->pool, n, h->st};
-    h->kf.k4<<<h->nb4, NT, h->kf.smem4, h->stream>>>(a);
-    check_launch(h, "k4_update");
+    K4aArgs a{h->W, h->U[par ^ 1], h->pool, n, h->st, par};
+    h->kf.k4a<<<h->nb4, NT, 0, s>>>(a);
+    check_launch(h, "k4a_basis");
+}
+// side branch, block with parity par: U_k = U[par], M_k -> M[par] (over M_{k-2}), M_{k-1} = M[par^1]
+void launch_k3b(bminres_ctx* h, cudaStream_t s) {
+    TimeMark tm(h, PH_SMALLQR);
+    h->kf.k3b<<<1, K3T, h->kf.smem3, s>>>(h->st);
+    check_launch(h, "k3b_smallqr");
+}
+void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, int par) {
+    TimeMark tm(h, PH_UPDATE);
+    K4bArgs a{h->U[par], h->M[par], h->M[par ^ 1], sp.X, n, h->st};
+    h->kf.k4b<<<h->nb4, NT, h->kf.smem4b, s>>>(a);
+    check_launch(h, "k4b_update");
 }
 
+// Graph for side block s (parity q): {K1, K2 of block s+1} || {K3b, K4b of block s}, then K4a(s+1).
 void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
     const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->U[0], h->W, (const void*)(intptr_t)n,
                           (const void*)(intptr_t)h->p_ws};
     bool same = h->gexec[0] && h->gexec[1] && std::equal(key, key + 8, h->gkey);
     if (same) return;
-    for (int s = 0; s < 2; ++s) {
-        if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
-        h->gexec[s] = nullptr;
+    for (int q = 0; q < 2; ++q) {
+        if (h->gexec[q]) cudaGraphExecDestroy(h->gexec[q]);
+        h->gexec[q] = nullptr;
         cudaGraph_t g;
-        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         long long saved = h->launches;
-        launch_k1(h, sp, n, s);
-        launch_k2(h, n, s);
-        launch_k3(h);
-        launch_k4(h, sp, n, s);
-        h->launches = saved;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        CK(cudaEventRecord(h->ev_fork, h->stream));
+        CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+        launch_k1(h, h->stream, sp, n, q ^ 1);
+        launch_k2(h, h->stream, n, q ^ 1);
+        launch_k3b(h, h->side);
+        launch_k4b(h, h->side, sp, n, q);
+        CK(cudaEventRecord(h->ev_join, h->side));
+        CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+        launch_k4a(h, h->stream, n, q ^ 1);
         CK(cudaStreamEndCapture(h->stream, &g));
-        CK(cudaGraphInstantiate(&h->gexec[s], g, 0));
+        h->launches = saved;
+        CK(cudaGraphInstantiate(&h->gexec[q], g, 0));
         cudaGraphDestroy(g);
     }
     std::copy(key, key + 8, h->gkey);
 }
 
-// write a few DevState fields from the host (stream-ordered)
+// write a few DevState fields from the host (after draining the stream)
 template <typename T>
 void set_state(bminres_ctx* h, size_t offset, T value) {
-    T* tmp;  // pinned staging is not needed for small values: use a synchronous copy after the stream drains
-    (void)tmp;
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaMemcpy((char*)h->st + offset, &value, sizeof(T), cudaMemcpyHostToDevice));
 }
@@ -393,29 +458,28 @@ T get_state(bminres_ctx* h, size_t offset) {
 
 // ------------------------------------------------------------------ column-by-column path
 
-// The paper's per-iteration orthogonalisation for the p columns of block k (Alg. 1 P:286-293,
+// The paper's per-iteration orthogonalisation for the p columns of block b (Alg. 1 P:286-293,
 // breakdown P:562-577, replacement P:690-729, retention P:797-805).  On entry W holds W' (the
-// candidates already orthogonalised against U_{k-1} and U_k by K1/K2).  On exit W holds
-// U_{k+1} (normalised), DevState.Ck = C_k, slow_given = 1.  Returns false if the pool was
-// exhausted (stop_after set).
-void slow_block(bminres_ctx* h, long long n, int p, long long k, int slot, const bminres_options& o, double tau,
-                long long maxit) {
+// candidates already orthogonalised against U_{b-1} and U_b by K1/K2) and om2[par] the raw
+// candidate norms.  On exit W holds U_{b+1} (normalised) and DevState.Ck[par] = C_b.
+void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, long long maxit) {
     TimeMark tm(h, PH_SLOW);
+    const int par = (int)(b & 1);
     const long long j0 = GET_STATE(h, j_done) + 1;
     std::vector<double> om2(MAXP);
-    CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy(om2.data(), (char*)h->st + offsetof(DevState, om2), MAXP * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(om2.data(), (char*)h->st + offsetof(DevState, om2) + par * MAXP * sizeof(double),
+                  MAXP * sizeof(double), cudaMemcpyDeviceToHost));
     int q_first = GET_STATE(h, q_first), q_live = GET_STATE(h, q_live);
     const int qc = h->q_ws;
     std::vector<double> Ck(MAXP * MAXP, 0.0);
     int stop_after = 0;
     auto Wc = [&](int m) { return Col{h->W + m, p}; };
-    const double* Uprev = h->U[slot ^ 1];
-    const double* Ucur = h->U[slot];
+    const double* Uprev = h->U[par ^ 1];
+    const double* Ucur = h->U[par];
     for (int m = 0; m < p; ++m) {
         const long long j = j0 + m;
         if (j > maxit) break;
-        // MGS against the new vectors of this block (u_{kp+1} .. u_{kp+m})
+        // MGS against the new vectors of this block (u_{bp+1} .. u_{bp+m})
         for (int mp = 0; mp < m; ++mp) {
             double c = dots_host(h, n, {Wc(mp)}, Wc(m))[0];
             launch_axpy(h, n, {Wc(mp)}, &c, nullptr, 1.0, Wc(m), 1.0);
@@ -449,7 +513,6 @@ void slow_block(bminres_ctx* h, long long n, int p, long long k, int slot, const
             if (q_live > 0) {
                 // replacement: pool vector (already orthogonal to u_1..u_{j+p-1}),
                 // orthogonalised twice more against retained + window, normalised
-                // W(:,m) := pool(:,q_first)  (zero it, then subtract -1 * pool)
                 std::vector<Col> src = {Col{h->pool + q_first, qc}};
                 launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Wc(m), 0.0);
                 double mone = -1.0;
@@ -459,7 +522,7 @@ void slow_block(bminres_ctx* h, long long n, int p, long long k, int slot, const
                 std::vector<Col> win;
                 for (auto& r : h->retained)
                     if (r.expiry >= j) win.push_back(Col{r.v, 1});
-                if (k > 1)
+                if (b > 1)
                     for (int mp = m; mp < p; ++mp) win.push_back(Col{Uprev + mp, p});
                 for (int mp = 0; mp < p; ++mp) win.push_back(Col{Ucur + mp, p});
                 for (int mp = 0; mp < m; ++mp) win.push_back(Wc(mp));
@@ -490,24 +553,38 @@ void slow_block(bminres_ctx* h, long long n, int p, long long k, int slot, const
         if (stop_after) break;
     }
     CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy((char*)h->st + offsetof(DevState, Ck), Ck.data(), MAXP * MAXP * sizeof(double),
-                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy((char*)h->st + offsetof(DevState, Ck) + par * MAXP * MAXP * sizeof(double), Ck.data(),
+                  MAXP * MAXP * sizeof(double), cudaMemcpyHostToDevice));
     SET_STATE(h, q_first, q_first);
     SET_STATE(h, q_live, q_live);
     SET_STATE(h, stop_after, stop_after);
-    SET_STATE(h, slow_given, 1);
     SET_STATE(h, need_slow, 0);
-    SET_STATE(h, run, 1);
-    (void)o;
+    SET_STATE(h, bd_at, KINF);
+    SET_STATE(h, run_main, 1);
+    SET_STATE(h, k_main, b + 1);
+    h->hf->need_slow = 0;
+    h->slow_blocks++;
+}
+
+// Finish block b after the column path: side branch (K3b, K4b) then K4a copying the
+// materialised U_{b+1} out of W.
+void finish_given_block(bminres_ctx* h, const StepPtrs& sp, long long n, long long b) {
+    const int par = (int)(b & 1);
+    launch_k3b(h, h->stream);
+    launch_k4b(h, h->stream, sp, n, par);
+    SET_STATE(h, given_main, 1);
+    launch_k4a(h, h->stream, n, par);
+    SET_STATE(h, given_main, 0);
+    CK(cudaStreamSynchronize(h->stream));
+}
+
+bool retained_live(bminres_ctx* h, long long jfirst) {
+    for (auto& r : h->retained)
+        if (r.expiry >= jfirst) return true;
+    return false;
 }
 
 // ------------------------------------------------------------------ the solve
-
-struct Inputs {
-    StepPtrs sp;
-    const double* B;
-    long long n;
-};
 
 int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xin, int p, double tol, long long maxit,
              double tau) {
@@ -521,8 +598,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     if (!std::isfinite(tol) || tol < 0 || maxit < 0 || !std::isfinite(tau) || tau < 0)
         fail(h, BMINRES_EINVAL, "tol / maxit / deflation_tol out of range");
     if (A->nnz < 0 || A->nnz >= (1ll << 31)) fail(h, BMINRES_EINVAL, "nnz must be < 2^31");
-    const int q = std::max(0, std::min(o.pool_size, MAXQ));
-    if (o.pool_size > MAXQ) fail(h, BMINRES_EINVAL, "pool_size > 8");
+    if (o.pool_size > MAXQ || o.pool_size < 0) fail(h, BMINRES_EINVAL, "pool_size must be in 0..8");
+    const int q = o.pool_size;
 
     CK(cudaSetDevice(h->device));
     cudaEvent_t e_solve0, e_solve1, e_loop0, e_loop1;
@@ -537,6 +614,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     h->ev_used = 0;
     h->ev_marks.clear();
     h->stats = bminres_stats_t{};
+    h->slow_blocks = 0;
     CK(cudaEventRecord(e_solve0, h->stream));
 
     // ---- inputs: device pointers are used in place; host pointers are staged
@@ -599,13 +677,17 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     }
 
     // ---- state init
-    DevState init{};
-    init.run = 1;
-    init.status = 1;
+    static DevState init;
+    std::memset(&init, 0, sizeof(init));
+    init.run_main = 1;
+    init.k_main = 1;
+    init.bd_at = KINF;
     init.q_first = 0;
     init.q_live = q;
     init.pool_cap = std::max(q, 1);
-    init.k = 1;
+    init.status = 1;
+    init.k_side = 1;
+    init.stop_side_at = KINF;
     init.j_done = 0;
     init.maxit = maxit;
     init.hist_cap = hist_cap;
@@ -619,12 +701,13 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         TimeMark tm(h, PH_START);
         CK(cudaMemsetAsync(h->M[0], 0, panel * sizeof(double), h->stream));
         CK(cudaMemsetAsync(h->M[1], 0, panel * sizeof(double), h->stream));
+        CK(cudaMemsetAsync(h->U[0], 0, panel * sizeof(double), h->stream));
         if (!o.use_x0) CK(cudaMemsetAsync(sp.X, 0, panel * sizeof(double), h->stream));
         // beta_i = ||b_i||
         launch_colsq(h, B, nullptr, n, p, h->dsc);
         std::vector<double> b2(p);
         CK(cudaMemcpyAsync(b2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        // F0 = B - A X0 (C6) into the slot of U_1 (k = 1 -> slot 1)
+        // F0 = B - A X0 (C6) into the slot of U_1 (block 1 -> slot 1)
         double* F = h->U[1];
         if (o.use_x0) {
             K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0};
@@ -711,108 +794,96 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         init.beta[c] = beta[c];
         init.res[c] = h0[c];
     }
+    bool finished = false;
     if (mx0 < tol) {
         init.status = 0;
-        init.run = 0;
-    }
-    if (maxit == 0 && init.run) {
+        finished = true;
+    } else if (maxit == 0) {
         init.status = 1;
-        init.run = 0;
+        finished = true;
     }
     CK(cudaMemcpyAsync(h->st, &init, sizeof(DevState), cudaMemcpyHostToDevice, h->stream));
     if (hist_cap) CK(cudaMemcpyAsync(h->hist, h0.data(), p * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    h->hf->run = init.run;
+    h->hf->side_done = finished ? 1 : 0;
     h->hf->status = init.status;
     h->hf->need_slow = 0;
-    h->hf->k = 1;
+    h->hf->bd_at = KINF;
     h->hf->j_done = 0;
+    h->hf->k_side = 1;
+    h->hf->k_main = 1;
     CK(cudaStreamSynchronize(h->stream));
 
-    // ---- block-step loop
+    // ---- block loop
     const bool graphs = o.use_graphs && !o.timing;
-    if (graphs && init.run) build_graphs(h, sp, n);
+    if (graphs && !finished) build_graphs(h, sp, n);
     CK(cudaEventRecord(e_loop0, h->stream));
-    long long k = 1;               // host mirror of the block index
-    long long block_steps = 0, slow_blocks = 0;
+    const long long nblocks = (maxit + p - 1) / p;
     const int LAG = 6;
     std::vector<cudaEvent_t> lag_ev(LAG);
     for (auto& e : lag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    bool running = init.run != 0;
-    while (running) {
-        // blocks whose iterations meet a live retained vector take the column path
-        const long long j_next = (k - 1) * p + 1;  // valid while no partial block happened
-        bool retained_live = false;
-        for (auto& r : h->retained)
-            if (r.expiry >= j_next) retained_live = true;
-        if (retained_live) {
-            const int slot = (int)(k & 1);
-            launch_k1(h, sp, n, slot);
-            launch_k2(h, n, slot);
-            block_steps++;
-            CK(cudaStreamSynchronize(h->stream));
-            slow_block(h, n, p, k, slot, o, tau, maxit);
-            slow_blocks++;
-            launch_k3(h);
-            launch_k4(h, sp, n, slot);
-            CK(cudaStreamSynchronize(h->stream));
-            k++;
-            if (!h->hf->run) running = false;
-            continue;
-        }
-        // fast path: launch steps ahead, poll flags LAG steps behind
-        long long launched = 0;
-        const long long steps_left = (maxit - (k - 1) * p + p - 1) / p;
-        long long kk = k;
-        bool stop_seen = false;
-        while (launched < steps_left) {
-            const int slot = (int)(kk & 1);
-            if (graphs) {
-                CK(cudaGraphLaunch(h->gexec[slot], h->stream));
-                h->launches += 4;
-            } else {
-                launch_k1(h, sp, n, slot);
-                launch_k2(h, n, slot);
-                launch_k3(h);
-                launch_k4(h, sp, n, slot);
+    long long b = 1;          // next block of the side branch
+    bool main_ahead = false;  // K1, K2, K4a of block b already done
+    while (!h->hf->side_done) {
+        const bool expl = !graphs || retained_live(h, (b - 1) * p + 1);
+        if (expl || !main_ahead) {
+            const int par = (int)(b & 1);
+            if (!main_ahead) {
+                launch_k1(h, h->stream, sp, n, par);
+                launch_k2(h, h->stream, n, par);
+                CK(cudaStreamSynchronize(h->stream));
             }
+            if (h->hf->need_slow || retained_live(h, (b - 1) * p + 1)) {
+                slow_block(h, n, p, b, tau, maxit);
+                finish_given_block(h, sp, n, b);
+                b++;
+                main_ahead = false;
+                continue;
+            }
+            if (expl) {
+                launch_k3b(h, h->stream);
+                launch_k4b(h, h->stream, sp, n, par);
+                launch_k4a(h, h->stream, n, par);
+                b++;
+                main_ahead = false;
+                if (!o.timing) CK(cudaStreamSynchronize(h->stream));
+                else if (b % 64 == 0) CK(cudaStreamSynchronize(h->stream));
+                continue;
+            }
+            launch_k4a(h, h->stream, n, par);
+            main_ahead = true;
+        }
+        // pipelined graphs: side block s with main block s+1
+        long long launched = 0;
+        for (long long s = b; s <= nblocks; ++s) {
+            CK(cudaGraphLaunch(h->gexec[s & 1], h->stream));
+            h->launches += 5;
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
-            kk++;
             if (launched >= LAG) {
                 CK(cudaEventSynchronize(lag_ev[launched % LAG]));
-                if (!h->hf->run) {
-                    stop_seen = true;
-                    break;
-                }
+                if (h->hf->side_done || h->hf->need_slow) break;
             }
         }
-        (void)stop_seen;
         CK(cudaStreamSynchronize(h->stream));
-        const long long kdev = GET_STATE(h, k);
-        const int need_slow = GET_STATE(h, need_slow);
-        const int run = GET_STATE(h, run);
-        block_steps += (kdev - k) + (need_slow ? 1 : 0);
-        k = kdev;
-        if (need_slow) {
-            const int slot = (int)(k & 1);
-            slow_block(h, n, p, k, slot, o, tau, maxit);
-            slow_blocks++;
-            launch_k3(h);
-            launch_k4(h, sp, n, slot);
-            CK(cudaStreamSynchronize(h->stream));
-            k = GET_STATE(h, k);
-            if (!GET_STATE(h, run)) running = false;
+        if (h->hf->side_done) break;
+        b = GET_STATE(h, k_side);
+        if (h->hf->need_slow) {
+            // main stopped at block bd_at == b after K2; the side finished block b-1
+            slow_block(h, n, p, b, tau, maxit);
+            finish_given_block(h, sp, n, b);
+            b++;
+            main_ahead = false;
             continue;
         }
-        if (!run) running = false;
+        main_ahead = true;
     }
+    CK(cudaStreamSynchronize(h->stream));
     CK(cudaEventRecord(e_loop1, h->stream));
     for (auto& e : lag_ev) cudaEventDestroy(e);
 
     // ---- exit: status, true residuals (K7), history, copy-back
-    DevState fin;
-    CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy(&fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    DevState* fin = &init;   // reuse the static buffer
+    CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
     {
         TimeMark tm(h, PH_RESID);
         K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->W, n, h->st, nullptr, 0};
@@ -826,18 +897,18 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     CK(cudaEventRecord(e_solve1, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     bminres_stats_t& s = h->stats;
-    s.status = fin.status;
+    s.status = fin->status;
     s.p = p;
     s.n = n;
-    s.iterations = fin.j_done;
-    s.block_steps = block_steps;
-    s.slow_blocks = slow_blocks;
+    s.iterations = fin->j_done;
+    s.block_steps = fin->k_side - 1;
+    s.slow_blocks = h->slow_blocks;
     s.n_events = (int64_t)h->events.size();
     for (int c = 0; c < p; ++c) {
-        s.comp_res[c] = fin.res[c];
+        s.comp_res[c] = fin->res[c];
         s.true_res[c] = beta[c] > 0 ? std::sqrt(r2[c]) / beta[c] : 0.0;
     }
-    s.history_len = std::min<long long>(fin.j_done + 1, hist_cap);
+    s.history_len = std::min<long long>(fin->j_done + 1, hist_cap);
     h->hist_host.assign((size_t)s.history_len * p, 0.0);
     if (s.history_len)
         CK(cudaMemcpy(h->hist_host.data(), h->hist, h->hist_host.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -862,7 +933,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     cudaEventDestroy(e_loop1);
     for (auto& r : h->retained) cudaFree(r.v);
     h->retained.clear();
-    return fin.status;
+    return fin->status;
 }
 
 }  // namespace
@@ -917,12 +988,16 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
             CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
             h->own_stream = true;
         }
+        CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
         // large dynamic shared memory for the p = 32 kernels
         for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 16, 32}) {
             Kfn f;
             kfn_for(p, &f);
-            CK(cudaFuncSetAttribute((const void*)f.k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
-            CK(cudaFuncSetAttribute((const void*)f.k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4));
+            CK(cudaFuncSetAttribute((const void*)f.k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem2));
+            CK(cudaFuncSetAttribute((const void*)f.k3b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
+            CK(cudaFuncSetAttribute((const void*)f.k4b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4b));
         }
     } catch (Err& x) {
         g_create_err = h->err;
@@ -1026,6 +1101,9 @@ void bminres_destroy(bminres_handle h) {
     if (h->hf) cudaFreeHost(h->hf);
     for (auto& r : h->retained) cudaFree(r.v);
     for (auto& e : h->evpool) cudaEventDestroy(e);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->side) cudaStreamDestroy(h->side);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
 }

@@ -6,18 +6,31 @@
 // paper's banded recurrence (eqn.block-Lanczos-recurr) with the
 // operator applied to p vectors every p iterations and the known
 // coefficients reused by symmetry.
+//
+// Two branches per block:
+//   main  K1 (SpMM+epilogue) -> K2 (orthogonalise, Grams, Cholesky = C_k) -> K4a (U_{k+1})
+//   side  K3b (banded QR, z_j, residuals, stop) -> K4b (M_k, X)
+// The side branch of block k runs concurrently with the main branch of block k+1.
 #pragma once
-#include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 namespace bmr {
+
+namespace cg = cooperative_groups;
 
 constexpr int MAXP = 32;      // largest compiled block size
 constexpr int MAXQ = 8;       // largest replacement pool
 constexpr int NB_MAX = 1024;  // largest grid of the reducing kernels
+constexpr int CL = 8;         // thread-block cluster size of the reducing kernels
+constexpr int NT = 256;       // threads of the panel kernels
+constexpr long long KINF = 1ll << 62;
+constexpr unsigned FULL = 0xffffffffu;
 
-// Panel-row mapping of a warp: a row of p doubles is split over LANES lanes,
-// VEC contiguous doubles (16 B when VEC = 2) each; RPW rows per warp.
+// Panel-row mapping of a warp: a row of p doubles is split over LANES lanes of VEC
+// contiguous doubles (16 B when VEC = 2); RPW rows per warp instruction.
 template <int P>
 struct PC {
     static constexpr int VEC = (P % 2 == 0) ? 2 : 1;
@@ -26,57 +39,152 @@ struct PC {
     static constexpr int RPW = 32 / LP;
 };
 
-// Mapped (pinned, host-visible) flags the small-QR kernel publishes each block step.
+// Mapped (pinned, host-visible) flags the kernels publish; the host polls them.
 struct HostFlags {
-    volatile int run;
+    volatile int side_done;      // the solve ended (converged / maxit / error)
     volatile int status;
-    volatile int need_slow;
+    volatile int need_slow;      // the main branch stopped at block bd_at (breakdown / guard)
     volatile int pad;
-    volatile long long k;
+    volatile long long bd_at;
     volatile long long j_done;
+    volatile long long k_side;
+    volatile long long k_main;
 };
 
-// Device-resident solver state (one per handle).  Small dense p x p matrices
-// are row-major [a*MAXP + b] with leading dimension MAXP.
+// Device-resident solver state.  p x p matrices are row-major [a*MAXP + b].
 struct DevState {
-    // control
-    int run;           // 1: block steps proceed; 0: every kernel of a step is a no-op
-    int k4_pending;    // the small QR ended the solve; the update kernel still applies this step
-    int need_slow;     // breakdown or Cholesky cancellation: host runs the column path
-    int slow_given;    // host provided C_k and wrote U_{k+1} (normalised) into W
-    int status;        // BMINRES_* code (1 = MAXIT while running)
-    int q_first;       // first live pool vector
-    int q_live;        // number of live pool vectors
-    int pool_cap;      // pool panel row stride
-    int stop_after;    // >0: the small QR stops after block column stop_after-1 (pool exhausted)
+    // ---- main branch (K1, K2, K4a)
+    int run_main;       // main-branch kernels run
+    int need_slow;      // K2: breakdown or Cholesky cancellation at block bd_at
+    int given_main;     // K4a: U_{k+1} is already materialised in W (host column path)
+    int q_first;        // first live pool vector
+    int q_live;         // number of live pool vectors
+    int pool_cap;       // pool panel row stride
+    long long k_main;   // block of the next K1/K2
+    long long bd_at;    // block with a pending breakdown (KINF: none)
+    // ---- side branch (K3b, K4b)
+    int side_go;        // K3b -> K4b: apply this block's update
+    int status;         // BMINRES_* (1 while running)
+    int stop_after;     // >0: K3b stops after block column stop_after-1 (pool exhausted)
     int pad0;
-    long long k;       // current block index (1-based)
-    long long j_done;  // completed iterations
+    long long k_side;        // block of the next K3b
+    long long stop_side_at;  // side kernels of blocks >= this are no-ops
+    long long j_done;        // completed iterations
     long long maxit;
     long long hist_cap;
     double tol, tau;
-    unsigned int cnt1, cnt2, cnt3, cnt4;   // last-CTA tickets
-    // reductions (written by the last CTA of K1 / K2)
-    double G[MAXP * MAXP];       // G(a,m) = u_{(k-1)p+a}^T w_m   (K1, after the known subtraction)
-    double om2[MAXP];            // ||A u_j||^2, raw candidate norms (C14)
-    double Gram2[MAXP * MAXP];   // W'^T W'
-    double pdot[MAXQ * MAXP];    // pdot(q,m) = r_q^T w'_m
-    // small dense state
-    double Cprev[MAXP * MAXP];   // C_{k-1}: W'_{k-1} = U_k C_{k-1}, upper triangular
-    double Ck[MAXP * MAXP];      // C_k (from Cholesky, or from the host column path)
-    double Cinv[MAXP * MAXP];    // C_k^{-1}
-    double coef[MAXP * MAXQ];    // coef(a,q) = u_{kp+a}^T r_q
-    double T[MAXP * MAXP];       // tail of \bar Z (rows j..j+p-1), T(r,c)
-    double Z[MAXP * MAXP];       // Z_k: row m = z_{(k-1)p+m+1}^T (rows past the stop are 0)
-    double Ainv[MAXP * MAXP];    // R_kk^{-1}
-    double B1[MAXP * MAXP];      // R_{k-1,k} R_kk^{-1}
-    double B2[MAXP * MAXP];      // R_{k-2,k} R_kk^{-1}
+    unsigned cnt1, cnt2, cnt3, cnt4;   // tickets of the cluster reductions
+    // ---- written by the main branch, double-buffered by block parity
+    double G[2][MAXP * MAXP];      // G(a,m) = u_{(k-1)p+a}^T w_m (K1, after the known subtraction)
+    double om2[2][MAXP];           // ||A u_j||^2, raw candidate norms (C14)
+    double Ck[2][MAXP * MAXP];     // C_k: W' = U_{k+1} C_k (upper triangular)
+    double Cinv[2][MAXP * MAXP];   // C_k^{-1}
+    double coef[2][MAXP * MAXQ];   // coef(a,q) = u_{kp+a}^T r_q
+    double Gram2[MAXP * MAXP];     // W'^T W' (K2 only)
+    double pdot[MAXQ * MAXP];      // pdot(q,m) = r_q^T w'_m (K2 only)
+    // ---- side-branch state
+    double CprevS[MAXP * MAXP];    // C_{k-1} for the Hessenberg assembly
+    double T[MAXP * MAXP];         // tail of \bar Z (rows j..j+p-1), T(r,c)
+    double Z[MAXP * MAXP];         // Z_k: row m = z_{(k-1)p+m+1}^T (rows past the stop are 0)
+    double Ainv[MAXP * MAXP];      // R_kk^{-1}
+    double B1[MAXP * MAXP];        // R_{k-1,k} R_kk^{-1}
+    double B2[MAXP * MAXP];        // R_{k-2,k} R_kk^{-1}
     double rv[(2 * MAXP + 1) * (MAXP + 1)];   // Householder ring, slot = i mod (2p+1)
     double rtau[2 * MAXP + 1];
-    double beta[MAXP];           // ||b_i||
-    double res[MAXP];            // latest computed relative residuals
-    double* hist;                // (hist_cap) x p computed relative residuals, or null
-    HostFlags* hflags;           // device alias of the mapped host flags
+    double beta[MAXP];             // ||b_i||
+    double res[MAXP];              // latest computed relative residuals
+    double* hist;                  // (hist_cap) x p computed relative residuals, or null
+    HostFlags* hflags;             // device alias of the mapped host flags
 };
+
+// ------------------------------------------------------------------ small helpers
+
+template <int VEC>
+__device__ __forceinline__ void ldv(const double* p, double (&r)[VEC]) {
+    if constexpr (VEC == 2) {
+        double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        r[0] = t.x;
+        r[1] = t.y;
+    } else {
+        r[0] = __ldg(p);
+    }
+}
+// coherent load (data written by a previous kernel that this kernel also writes)
+template <int VEC>
+__device__ __forceinline__ void ldc(const double* p, double (&r)[VEC]) {
+    if constexpr (VEC == 2) {
+        double2 t = *reinterpret_cast<const double2*>(p);
+        r[0] = t.x;
+        r[1] = t.y;
+    } else {
+        r[0] = *p;
+    }
+}
+template <int VEC>
+__device__ __forceinline__ void stv(double* p, const double (&r)[VEC]) {
+    if constexpr (VEC == 2) {
+        *reinterpret_cast<double2*>(p) = make_double2(r[0], r[1]);
+    } else {
+        *p = r[0];
+    }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+
+// Cluster reduction.  Every CTA of a reducing panel kernel ends with its sums in shared
+// memory sAcc[E].  The CTAs of a thread-block cluster are combined through distributed
+// shared memory by the cluster's rank-0 CTA (fixed rank order), which writes one partial
+// per cluster; the last cluster leader to arrive sums the per-cluster partials in fixed
+// order into outA (entries e < P*P, at [(e/P)*MAXP + e%P]) and outB (the rest, at
+// [((e-P*P)/P)*MAXP + (e-P*P)%P]).  Returns true in the CTA that produced the totals.
+// Deterministic: no floating-point atomics.
+__device__ __forceinline__ bool cluster_reduce(double* sAcc, int E, int P, double* part, double* outA,
+                                               double* outB, unsigned* cnt) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    const unsigned rank = cl.block_rank();
+    const int ncl = gridDim.x / CL, cid = blockIdx.x / CL;
+    if (rank == 0) {
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            double s = 0.0;
+#pragma unroll
+            for (int r = 0; r < CL; ++r) s += cl.map_shared_rank(sAcc, r)[e];
+            part[(size_t)e * ncl + cid] = s;
+        }
+    }
+    cl.sync();  // remote shared memory must outlive the leader's reads
+    if (rank != 0) return false;
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1u) == (unsigned)ncl - 1);
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int e = warp; e < E; e += nw) {
+        double s = 0.0;
+        for (int b = lane; b < ncl; b += 32) s += __ldcg(part + (size_t)e * ncl + b);
+        s = warp_sum(s);
+        if (lane == 0) {
+            if (e < P * P)
+                outA[(e / P) * MAXP + e % P] = s;
+            else
+                outB[((e - P * P) / P) * MAXP + (e - P * P) % P] = s;
+        }
+    }
+    if (threadIdx.x == 0) *cnt = 0u;
+    __syncthreads();
+    return true;
+}
 
 }  // namespace bmr
