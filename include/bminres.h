@@ -47,7 +47,7 @@ extern "C" {
 #define BMINRES_ESINGULAR_R (-6) /* |r_jj| <= eps_mach*||h_j||: R_j singular, X cannot be updated */
 
 #define BMINRES_MAX_P 32       /* block sizes 1..8, 16 and 32 are compiled */
-#define BMINRES_MAX_POOL 32
+#define BMINRES_MAX_POOL 8
 
 typedef struct bminres_ctx *bminres_handle;
 
@@ -72,7 +72,7 @@ typedef struct {
     int32_t rank, world;     /* row partition; only world = 1 is implemented in this version */
     void *stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
     uint64_t seed;           /* random replacement vectors (reading C17), default 0 */
-    int32_t pool_size;       /* random vectors kept orthogonal to the basis, 0..32, default 1 */
+    int32_t pool_size;       /* random vectors kept orthogonal to the basis, 0..8, default 1 */
     int32_t use_x0;          /* 0: X is output only, X_0 = 0 (Alg. 2); 1: X holds X_0 on entry */
     int32_t record_history;  /* 1: keep (iterations+1) x p computed relative residuals */
     int32_t use_graphs;      /* 1: replay each block step as a CUDA graph (default); 0: plain launches */
@@ -90,7 +90,7 @@ typedef struct {
     double ratio;    /* h / omega */
 } bminres_event;
 
-#define BMINRES_NPHASE 8   /* spmm, orth, smallqr, update, slowpath, start, resid, other */
+#define BMINRES_NPHASE 10  /* spmm, orth, smallqr, update, slowpath, start, resid, other, basis, spare */
 
 typedef struct {
     int32_t status;           /* return code of the last solve */

@@ -28,7 +28,7 @@ using namespace bmr;
 
 namespace {
 
-enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER };
+enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER, PH_BASIS };
 
 struct Retained {
     double* v;
@@ -392,7 +392,7 @@ void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, int par) {
     h->stream = keep;
 }
 void launch_k4a(bminres_ctx* h, cudaStream_t s, long long n, int par) {
-    TimeMark tm(h, PH_UPDATE);
+    TimeMark tm(h, PH_BASIS);
     K4aArgs a{h->W, h->U[par ^ 1], h->pool, n, h->st, par};
     h->kf.k4a<<<h->nb4, NT, 0, s>>>(a);
     check_launch(h, "k4a_basis");
