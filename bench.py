@@ -33,7 +33,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PHASE_BYTES_PANELS = {"spmm": 3, "orth": 3, "basis": 2, "update": 6}   # panels per launch
+PHASE_BYTES_PANELS = {"spmm": 3, "orth": 3, "update": 6}   # panels per launch
 
 
 def load_peaks():

@@ -145,6 +145,18 @@ __global__ void __launch_bounds__(256) k_colsq(const double* X, const double* Y,
     if (threadIdx.x == 0) *cnt = 0u;
 }
 
+// out = V Tr (row-major n x P panels; Tr P x P with leading dimension MAXP): materialises
+// U_k = V_k Tr_k for the column-by-column path
+__global__ void k_materialize(const double* V, const double* Tr, double* out, long long n, int P) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n * P; e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / P;
+        const int c = (int)(e % P);
+        double s = 0.0;
+        for (int b = 0; b < P; ++b) s = fma(V[i * P + b], Tr[b * MAXP + c], s);
+        out[e] = s;
+    }
+}
+
 // Y = B - Y (row-major panels, same shape)
 __global__ void k_sub_from(const double* B, double* Y, long long total) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)

@@ -28,7 +28,7 @@ using namespace bmr;
 
 namespace {
 
-enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER, PH_BASIS };
+enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER };
 
 struct Retained {
     double* v;
@@ -40,9 +40,8 @@ struct Kfn {  // per-p kernel table
     void (*k1plain)(K1Args);
     void (*k2)(K2Args);
     void (*k3b)(DevState*);
-    void (*k4a)(K4aArgs);
     void (*k4b)(K4bArgs);
-    size_t smem2, smem3, smem4b;
+    size_t smem1, smem2, smem3, smem4b;
 };
 
 template <int P>
@@ -52,8 +51,8 @@ Kfn make_kfn() {
     f.k1plain = k1_spmm<P, false>;
     f.k2 = k2_orth<P>;
     f.k3b = k3b_smallqr<P>;
-    f.k4a = k4a_basis<P>;
     f.k4b = k4b_update<P>;
+    f.smem1 = K1Smem<P>::bytes;
     f.smem2 = K2Smem<P>::bytes;
     f.smem3 = K3Smem<P>::bytes;
     f.smem4b = K4bSmem<P>::bytes;
@@ -94,9 +93,9 @@ struct bminres_ctx {
     // workspace
     long long n_ws = -1;
     int p_ws = -1, q_ws = -1;
-    double* U[2] = {nullptr, nullptr};
-    double* M[2] = {nullptr, nullptr};
-    double* W = nullptr;
+    double* V[3] = {nullptr, nullptr, nullptr};   // V_k in slot k mod 3 (U_k = V_k Tr_k)
+    double* M[2] = {nullptr, nullptr};            // M_k in slot k mod 2
+    double* scr[2] = {nullptr, nullptr};          // column path: materialised U_{k-1}, U_k (lazy)
     double* pool = nullptr;
     double* part = nullptr;
     size_t part_elems = 0;
@@ -116,7 +115,7 @@ struct bminres_ctx {
     double* xx = nullptr;         // staged X
     size_t bx_cap = 0, xx_cap = 0;
     // graphs
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaGraphExec_t gexec[6] = {};
     const void* gkey[8] = {};
     // per-solve
     std::vector<Retained> retained;
@@ -260,16 +259,18 @@ void launch_cluster(bminres_ctx* h, K kern, int grid, size_t smem, A args, const
 
 void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     if (h->n_ws == n && h->p_ws == p && h->q_ws == q) return;
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 6; ++s) {
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
         h->gexec[s] = nullptr;
     }
     size_t panel = (size_t)n * p;
-    dalloc(h, &h->U[0], panel);
-    dalloc(h, &h->U[1], panel);
+    for (int s = 0; s < 3; ++s) dalloc(h, &h->V[s], panel);
     dalloc(h, &h->M[0], panel);
     dalloc(h, &h->M[1], panel);
-    dalloc(h, &h->W, panel);
+    for (int s = 0; s < 2; ++s) {
+        if (h->scr[s]) cudaFree(h->scr[s]);
+        h->scr[s] = nullptr;
+    }
     dalloc(h, &h->pool, (size_t)n * std::max(q, 1));
     h->part_elems = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8);
     if (!h->part) CK(cudaMalloc((void**)&h->part, h->part_elems * sizeof(double)));
@@ -288,7 +289,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     h->q_ws = q;
     // grids of the reducing panel kernels: as many whole clusters of CL CTAs as can be resident
     long long rows_per_cta = (long long)(NT / 32) * (32 / std::max(1, (p % 2 == 0 ? p / 2 : p)));
-    h->nb1 = cluster_grid(h, (const void*)h->kf.k1, 0, n, rows_per_cta);
+    h->nb1 = cluster_grid(h, (const void*)h->kf.k1, h->kf.smem1, n, rows_per_cta);
     h->nb2 = cluster_grid(h, (const void*)h->kf.k2, h->kf.smem2, n, rows_per_cta);
     int occ4 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, (const void*)h->kf.k4b, NT, h->kf.smem4b);
@@ -374,63 +375,63 @@ struct StepPtrs {
     double* X;
 };
 
-// main branch, block with parity par: U_k = U[par], U_{k-1} = U[par^1], U_{k+1} -> U[par^1]
-void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, int par) {
+// main branch of block k: gathers V_k (slot k%3), reads V_{k-1} (slot (k-1)%3), writes W and
+// then W' into slot (k+1)%3 (= V_{k+1}); parity k%2 selects the double-buffered small state
+void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k) {
     TimeMark tm(h, PH_SPMM);
-    K1Args a{sp.rowptr, sp.col, sp.val, h->U[par], h->U[par ^ 1], h->W, n, h->st, h->part, par};
+    const int sk = (int)(k % 3), par = (int)(k & 1);
+    K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
+             par, sk};
     cudaStream_t keep = h->stream;
     h->stream = s;
-    launch_cluster(h, h->kf.k1, h->nb1, 0, a, "k1_spmm");
+    launch_cluster(h, h->kf.k1, h->nb1, h->kf.smem1, a, "k1_spmm");
     h->stream = keep;
 }
-void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, int par) {
+void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k) {
     TimeMark tm(h, PH_ORTH);
-    K2Args a{h->W, h->U[par], h->pool, n, h->st, h->part + (size_t)NB_MAX * (MAXP * MAXP + MAXP), par};
+    const int sk = (int)(k % 3), par = (int)(k & 1);
+    K2Args a{h->V[(sk + 1) % 3], h->V[sk], h->pool, n, h->st, h->part + (size_t)NB_MAX * (MAXP * MAXP + MAXP),
+             par, sk};
     cudaStream_t keep = h->stream;
     h->stream = s;
     launch_cluster(h, h->kf.k2, h->nb2, h->kf.smem2, a, "k2_orth");
     h->stream = keep;
 }
-void launch_k4a(bminres_ctx* h, cudaStream_t s, long long n, int par) {
-    TimeMark tm(h, PH_BASIS);
-    K4aArgs a{h->W, h->U[par ^ 1], h->pool, n, h->st, par};
-    h->kf.k4a<<<h->nb4, NT, 0, s>>>(a);
-    check_launch(h, "k4a_basis");
-}
-// side branch, block with parity par: U_k = U[par], M_k -> M[par] (over M_{k-2}), M_{k-1} = M[par^1]
+// side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
 void launch_k3b(bminres_ctx* h, cudaStream_t s) {
     TimeMark tm(h, PH_SMALLQR);
     h->kf.k3b<<<1, K3T, h->kf.smem3, s>>>(h->st);
     check_launch(h, "k3b_smallqr");
 }
-void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, int par) {
+void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k) {
     TimeMark tm(h, PH_UPDATE);
-    K4bArgs a{h->U[par], h->M[par], h->M[par ^ 1], sp.X, n, h->st};
+    const int sk = (int)(k % 3), par = (int)(k & 1);
+    K4bArgs a{h->V[sk], h->M[par], h->M[par ^ 1], sp.X, n, h->st, sk};
     h->kf.k4b<<<h->nb4, NT, h->kf.smem4b, s>>>(a);
     check_launch(h, "k4b_update");
 }
 
-// Graph for side block s (parity q): {K1, K2 of block s+1} || {K3b, K4b of block s}, then K4a(s+1).
+// Graph for side block s (s mod 6): {K1, K2 of block s+1} || {K3b, K4b of block s}.
 void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
-    const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->U[0], h->W, (const void*)(intptr_t)n,
+    const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->V[0], h->M[0], (const void*)(intptr_t)n,
                           (const void*)(intptr_t)h->p_ws};
-    bool same = h->gexec[0] && h->gexec[1] && std::equal(key, key + 8, h->gkey);
+    bool same = h->gexec[0] && std::equal(key, key + 8, h->gkey);
     if (same) return;
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < 6; ++q) {
         if (h->gexec[q]) cudaGraphExecDestroy(h->gexec[q]);
         h->gexec[q] = nullptr;
         cudaGraph_t g;
         long long saved = h->launches;
+        const long long sblk = 6 + q;   // any block with this residue mod 6
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         CK(cudaEventRecord(h->ev_fork, h->stream));
         CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-        launch_k1(h, h->stream, sp, n, q ^ 1);
-        launch_k2(h, h->stream, n, q ^ 1);
+        launch_k1(h, h->stream, sp, n, sblk + 1);
+        launch_k2(h, h->stream, n, sblk + 1);
         launch_k3b(h, h->side);
-        launch_k4b(h, h->side, sp, n, q);
+        launch_k4b(h, h->side, sp, n, sblk);
         CK(cudaEventRecord(h->ev_join, h->side));
         CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
-        launch_k4a(h, h->stream, n, q ^ 1);
         CK(cudaStreamEndCapture(h->stream, &g));
         h->launches = saved;
         CK(cudaGraphInstantiate(&h->gexec[q], g, 0));
@@ -459,9 +460,11 @@ T get_state(bminres_ctx* h, size_t offset) {
 // ------------------------------------------------------------------ column-by-column path
 
 // The paper's per-iteration orthogonalisation for the p columns of block b (Alg. 1 P:286-293,
-// breakdown P:562-577, replacement P:690-729, retention P:797-805).  On entry W holds W' (the
-// candidates already orthogonalised against U_{b-1} and U_b by K1/K2) and om2[par] the raw
-// candidate norms.  On exit W holds U_{b+1} (normalised) and DevState.Ck[par] = C_b.
+// breakdown P:562-577, replacement P:690-729, retention P:797-805).  On entry the V slot of
+// block b+1 holds W' (the candidates already orthogonalised against U_{b-1} and U_b by
+// K1/K2) and om2[par] the raw candidate norms.  On exit it holds U_{b+1} (normalised) with
+// Tr_{b+1} = I, DevState.Ck[par] = C_b and the pool coefficients of block b are zero (the
+// pool was updated here, column by column).
 void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, long long maxit) {
     TimeMark tm(h, PH_SLOW);
     const int par = (int)(b & 1);
@@ -473,9 +476,26 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
     const int qc = h->q_ws;
     std::vector<double> Ck(MAXP * MAXP, 0.0);
     int stop_after = 0;
-    auto Wc = [&](int m) { return Col{h->W + m, p}; };
-    const double* Uprev = h->U[par ^ 1];
-    const double* Ucur = h->U[par];
+    const int sk = (int)(b % 3);
+    double* Wp = h->V[(sk + 1) % 3];
+    auto Wc = [&](int m) { return Col{Wp + m, p}; };
+    // U_{b-1}, U_b are materialised (V Tr) only if a replacement needs them as a window
+    bool have_window = false;
+    auto materialise = [&]() {
+        if (have_window) return;
+        for (int s2 = 0; s2 < 2; ++s2)
+            if (!h->scr[s2]) CK(cudaMalloc((void**)&h->scr[s2], (size_t)n * p * sizeof(double)));
+        const int slots[2] = {(sk + 2) % 3, sk};
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const double* Tr = (const double*)((char*)h->st + offsetof(DevState, Tr)) + (size_t)slots[s2] * MAXP * MAXP;
+            k_materialize<<<grid_for(h, n * p, 256, 8 * h->n_sm), 256, 0, h->stream>>>(h->V[slots[s2]], Tr,
+                                                                                          h->scr[s2], n, p);
+            check_launch(h, "k_materialize");
+        }
+        have_window = true;
+    };
+    const double* Uprev = nullptr;
+    const double* Ucur = nullptr;
     for (int m = 0; m < p; ++m) {
         const long long j = j0 + m;
         if (j > maxit) break;
@@ -519,6 +539,9 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
                 launch_axpy(h, n, src, &mone, nullptr, 1.0, Wc(m), 1.0);
                 q_first++;
                 q_live--;
+                materialise();
+                Uprev = h->scr[0];
+                Ucur = h->scr[1];
                 std::vector<Col> win;
                 for (auto& r : h->retained)
                     if (r.expiry >= j) win.push_back(Col{r.v, 1});
@@ -562,19 +585,21 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
     SET_STATE(h, bd_at, KINF);
     SET_STATE(h, run_main, 1);
     SET_STATE(h, k_main, b + 1);
+    // Tr_{b+1} = I (V_{b+1} is the normalised basis block); pool coefficients of block b = 0
+    std::vector<double> I(MAXP * MAXP, 0.0), Z0(MAXP * MAXQ, 0.0);
+    for (int c = 0; c < MAXP; ++c) I[c * MAXP + c] = 1.0;
+    CK(cudaMemcpy((char*)h->st + offsetof(DevState, Tr) + (size_t)((sk + 1) % 3) * MAXP * MAXP * sizeof(double),
+                  I.data(), MAXP * MAXP * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy((char*)h->st + offsetof(DevState, coef) + (size_t)par * MAXP * MAXQ * sizeof(double), Z0.data(),
+                  MAXP * MAXQ * sizeof(double), cudaMemcpyHostToDevice));
     h->hf->need_slow = 0;
     h->slow_blocks++;
 }
 
-// Finish block b after the column path: side branch (K3b, K4b) then K4a copying the
-// materialised U_{b+1} out of W.
+// Finish block b after the column path: its side branch (K3b, K4b).
 void finish_given_block(bminres_ctx* h, const StepPtrs& sp, long long n, long long b) {
-    const int par = (int)(b & 1);
     launch_k3b(h, h->stream);
-    launch_k4b(h, h->stream, sp, n, par);
-    SET_STATE(h, given_main, 1);
-    launch_k4a(h, h->stream, n, par);
-    SET_STATE(h, given_main, 0);
+    launch_k4b(h, h->stream, sp, n, b);
     CK(cudaStreamSynchronize(h->stream));
 }
 
@@ -695,22 +720,24 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     init.tau = tau;
     init.hist = hist_cap ? h->hist : nullptr;
     init.hflags = h->hf_dev;
+    for (int t = 0; t < 3; ++t)
+        for (int c = 0; c < MAXP; ++c) init.Tr[t][c * MAXP + c] = 1.0;
     std::vector<double> S(MAXP * MAXP, 0.0), beta(p, 0.0), f0n(p, 0.0);
 
     {
         TimeMark tm(h, PH_START);
         CK(cudaMemsetAsync(h->M[0], 0, panel * sizeof(double), h->stream));
         CK(cudaMemsetAsync(h->M[1], 0, panel * sizeof(double), h->stream));
-        CK(cudaMemsetAsync(h->U[0], 0, panel * sizeof(double), h->stream));
+        CK(cudaMemsetAsync(h->V[0], 0, panel * sizeof(double), h->stream));
         if (!o.use_x0) CK(cudaMemsetAsync(sp.X, 0, panel * sizeof(double), h->stream));
         // beta_i = ||b_i||
         launch_colsq(h, B, nullptr, n, p, h->dsc);
         std::vector<double> b2(p);
         CK(cudaMemcpyAsync(b2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        // F0 = B - A X0 (C6) into the slot of U_1 (block 1 -> slot 1)
-        double* F = h->U[1];
+        // F0 = B - A X0 (C6) into the V slot of block 1 (U_1 = V_1, Tr_1 = I)
+        double* F = h->V[1];
         if (o.use_x0) {
-            K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0};
+            K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0, 0};
             h->kf.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
             check_launch(h, "k1_spmm(plain)");
             k_sub_from<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(B, F, (long long)panel);
@@ -822,14 +849,13 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     std::vector<cudaEvent_t> lag_ev(LAG);
     for (auto& e : lag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     long long b = 1;          // next block of the side branch
-    bool main_ahead = false;  // K1, K2, K4a of block b already done
+    bool main_ahead = false;  // K1, K2 of block b already done (V_{b+1} ready)
     while (!h->hf->side_done) {
         const bool expl = !graphs || retained_live(h, (b - 1) * p + 1);
         if (expl || !main_ahead) {
-            const int par = (int)(b & 1);
             if (!main_ahead) {
-                launch_k1(h, h->stream, sp, n, par);
-                launch_k2(h, h->stream, n, par);
+                launch_k1(h, h->stream, sp, n, b);
+                launch_k2(h, h->stream, n, b);
                 CK(cudaStreamSynchronize(h->stream));
             }
             if (h->hf->need_slow || retained_live(h, (b - 1) * p + 1)) {
@@ -841,22 +867,18 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             }
             if (expl) {
                 launch_k3b(h, h->stream);
-                launch_k4b(h, h->stream, sp, n, par);
-                launch_k4a(h, h->stream, n, par);
+                launch_k4b(h, h->stream, sp, n, b);
                 b++;
                 main_ahead = false;
-                if (!o.timing) CK(cudaStreamSynchronize(h->stream));
-                else if (b % 64 == 0) CK(cudaStreamSynchronize(h->stream));
                 continue;
             }
-            launch_k4a(h, h->stream, n, par);
             main_ahead = true;
         }
         // pipelined graphs: side block s with main block s+1
         long long launched = 0;
         for (long long s = b; s <= nblocks; ++s) {
-            CK(cudaGraphLaunch(h->gexec[s & 1], h->stream));
-            h->launches += 5;
+            CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
+            h->launches += 4;
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -886,10 +908,10 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
     {
         TimeMark tm(h, PH_RESID);
-        K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->W, n, h->st, nullptr, 0};
+        K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->M[0], n, h->st, nullptr, 0, 0};
         h->kf.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
         check_launch(h, "k1_spmm(plain)");
-        launch_colsq(h, B, h->W, n, p, h->dsc);
+        launch_colsq(h, B, h->M[0], n, p, h->dsc);
     }
     std::vector<double> r2(p);
     CK(cudaMemcpyAsync(r2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -925,7 +947,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     }
     s.gpu_launches = h->launches;
     const double abytes = 12.0 * A->nnz + 4.0 * (n + 1);
-    s.bytes_per_block_step = abytes + 10.0 * 8.0 * (double)panel;
+    s.bytes_per_block_step = abytes + 10.0 * 8.0 * (double)panel;   // SURVEY §8(d) algorithmic model
     s.spmm_bytes_per_launch = abytes + 3.0 * 8.0 * (double)panel;
     cudaEventDestroy(e_solve0);
     cudaEventDestroy(e_solve1);
@@ -995,6 +1017,7 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
         for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 16, 32}) {
             Kfn f;
             kfn_for(p, &f);
+            CK(cudaFuncSetAttribute((const void*)f.k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem1));
             CK(cudaFuncSetAttribute((const void*)f.k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem2));
             CK(cudaFuncSetAttribute((const void*)f.k3b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
             CK(cudaFuncSetAttribute((const void*)f.k4b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4b));
@@ -1052,7 +1075,7 @@ int bminres_spmm(bminres_handle h, const bminres_csr* A, const double* X, double
         if ((((uintptr_t)X) | ((uintptr_t)Y)) & 15) fail(h, BMINRES_EINVAL, "X and Y must be 16-byte aligned");
         CK(cudaSetDevice(h->device));
         const long long n = A->n_loc;
-        K1Args a{A->row_ptr, A->col_idx, A->values, X, nullptr, Y, n, nullptr, nullptr, 0};
+        K1Args a{A->row_ptr, A->col_idx, A->values, X, nullptr, Y, n, nullptr, nullptr, 0, 0};
         f.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
         check_launch(h, "k1_spmm(plain)");
         CK(cudaStreamSynchronize(h->stream));
@@ -1089,10 +1112,10 @@ const char* bminres_last_error(bminres_handle h) {
 void bminres_destroy(bminres_handle h) {
     if (!h) return;
     cudaSetDevice(h->device);
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < 6; ++s)
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
-    for (double* p : {h->U[0], h->U[1], h->M[0], h->M[1], h->W, h->pool, h->part, h->dsc, h->a_val, h->bx, h->xx,
-                      h->hist})
+    for (double* p : {h->V[0], h->V[1], h->V[2], h->M[0], h->M[1], h->scr[0], h->scr[1], h->pool, h->part, h->dsc,
+                      h->a_val, h->bx, h->xx, h->hist})
         if (p) cudaFree(p);
     if (h->a_rowptr) cudaFree(h->a_rowptr);
     if (h->a_col) cudaFree(h->a_col);

@@ -8,9 +8,12 @@
 // coefficients reused by symmetry.
 //
 // Two branches per block:
-//   main  K1 (SpMM+epilogue) -> K2 (orthogonalise, Grams, Cholesky = C_k) -> K4a (U_{k+1})
+//   main  K1 (SpMM+epilogue) -> K2 (orthogonalise, Grams, Cholesky = C_k)
 //   side  K3b (banded QR, z_j, residuals, stop) -> K4b (M_k, X)
 // The side branch of block k runs concurrently with the main branch of block k+1.
+// The basis is never normalised in memory: U_k = V_k Tr_k row by row, where V_k is the
+// orthogonalised candidate block W'_{k-1} and Tr_k = C_{k-1}^{-1} (SURVEY design D2), or
+// V_k = U_k, Tr_k = I after the column path / for the start block.
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -56,7 +59,7 @@ struct DevState {
     // ---- main branch (K1, K2, K4a)
     int run_main;       // main-branch kernels run
     int need_slow;      // K2: breakdown or Cholesky cancellation at block bd_at
-    int given_main;     // K4a: U_{k+1} is already materialised in W (host column path)
+    int pad_m;
     int q_first;        // first live pool vector
     int q_live;         // number of live pool vectors
     int pool_cap;       // pool panel row stride
@@ -78,8 +81,8 @@ struct DevState {
     double G[2][MAXP * MAXP];      // G(a,m) = u_{(k-1)p+a}^T w_m (K1, after the known subtraction)
     double om2[2][MAXP];           // ||A u_j||^2, raw candidate norms (C14)
     double Ck[2][MAXP * MAXP];     // C_k: W' = U_{k+1} C_k (upper triangular)
-    double Cinv[2][MAXP * MAXP];   // C_k^{-1}
-    double coef[2][MAXP * MAXQ];   // coef(a,q) = u_{kp+a}^T r_q
+    double Tr[3][MAXP * MAXP];     // Tr_k (slot k mod 3): U_k = V_k Tr_k
+    double coef[2][MAXP * MAXQ];   // coef(a,q) = u_{kp+a}^T r_q, applied to the pool by K2(k+1)
     double Gram2[MAXP * MAXP];     // W'^T W' (K2 only)
     double pdot[MAXQ * MAXP];      // pdot(q,m) = r_q^T w'_m (K2 only)
     // ---- side-branch state

@@ -1,17 +1,20 @@
 // step_kernels.cuh -- sm_100a kernels of one block step of banded-Lanczos block MINRES.
 //
+// The basis is kept as U_k = V_k Tr_k (V_k = the unnormalised W'_{k-1}, Tr_k = C_{k-1}^{-1});
+// every p x p factor is folded into a per-CTA combined matrix, so rows only see V.
 // main branch (critical path), block k:
-//   K1  k1_spmm     W = A U_k; ||A u_j||; W -= U_{k-1} C_{k-1}^T; G = U_k^T W
-//                   (row a1; Alg. 2; symmetric reuse P:270-272)
-//   K2  k2_orth     W' = W - U_k G_s; W'^T W'; r_q^T W'; last CTA: Cholesky W' = U_{k+1} C_k,
-//                   breakdown test h_{j+p,j} <= tau ||A u_j||, C_k^{-1}, pool coefficients
-//                   (rows a2/a3; Alg. 1)
-//   K4a k4a_basis   U_{k+1} = W' C_k^{-1}; pool r_q -= U_{k+1} coef
+//   K1  k1_spmm     W = (A V_k) Tr_k = A U_k; ||A u_j||; W -= V_{k-1} (Tr_{k-1} C_{k-1}^T);
+//                   G = Tr_k^T (V_k^T W) = U_k^T W   (row a1; Alg. 2)
+//   K2  k2_orth     pool r_q -= V_k (Tr_k coef_{k-1}); W' = W - V_k (Tr_k G_s);
+//                   W'^T W'; r_q^T W'; last CTA: Cholesky W' = U_{k+1} C_k, breakdown test
+//                   h_{j+p,j} <= tau ||A u_j||, Tr_{k+1} = C_k^{-1}, pool coefficients
+//                   (rows a2/a3/a5; Alg. 1); W' stays as V_{k+1}
 // side branch, block k (runs beside the main branch of block k+1):
 //   K3b k3b_smallqr one warp: p Hessenberg columns, <= 2p Householder reflectors each,
 //                   z_j, residuals, stop test, direction matrices (row a4; P:424-468,
 //                   Alg. 2)
-//   K4b k4b_update  M_k = (U_k - M_{k-2}R_{k-2,k} - M_{k-1}R_{k-1,k})R_kk^{-1}; X += M_k Z_k
+//   K4b k4b_update  M_k = V_k (Tr_k R_kk^{-1}) - M_{k-2}R_{k-2,k}R_kk^{-1} - M_{k-1}R_{k-1,k}R_kk^{-1};
+//                   X += M_k Z_k
 //                   (row a5; eqn.search-dir-comp, eqn.approx-update)
 //
 // Panels are row-major n x p fp64.  A warp splits a panel row over LANES lanes of VEC
@@ -29,27 +32,57 @@ struct K1Args {
     const int* rowptr;
     const int* col;
     const double* val;
-    const double* X;      // U_k (gathered by global column)
-    const double* Uprev;  // U_{k-1}
-    double* Y;            // W
+    const double* X;      // V_k (gathered by global column); plain mode: the SpMM input
+    const double* Vprev;  // V_{k-1}
+    double* Y;            // W (written into the V slot of block k+1); plain mode: the output
     long long n;
     DevState* st;
     double* part;
     int par;              // k mod 2
+    int sk;               // k mod 3
 };
 
 template <int P>
 constexpr int k1_min_blocks() { return P <= 8 ? 3 : 1; }
 
+template <int P>
+struct K1Smem {   // dynamic shared memory of the epilogue variant
+    static constexpr size_t bytes =
+        sizeof(double) * (4 * P * P + (NT / 32) * 3 * PC<P>::RPW * P + P * P + P);
+};
+
+// C = A^T B for P x P row-major (leading dimensions lda/ldb/ldc), all threads of the CTA.
+template <int P>
+__device__ __forceinline__ void cta_matmul_tn(const double* Am, int lda, const double* Bm, int ldb, double* Cm,
+                                              int ldc, bool transB = false) {
+    for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+        const int r = t / P, c = t % P;
+        double s = 0.0;
+        for (int i = 0; i < P; ++i) s = fma(Am[i * lda + r], transB ? Bm[c * ldb + i] : Bm[i * ldb + c], s);
+        Cm[r * ldc + c] = s;
+    }
+}
+// C = A B
+template <int P>
+__device__ __forceinline__ void cta_matmul_nn(const double* Am, int lda, const double* Bm, int ldb, double* Cm,
+                                              int ldc, bool transB = false) {
+    for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+        const int r = t / P, c = t % P;
+        double s = 0.0;
+        for (int i = 0; i < P; ++i) s = fma(Am[r * lda + i], transB ? Bm[c * ldb + i] : Bm[i * ldb + c], s);
+        Cm[r * ldc + c] = s;
+    }
+}
+
 // W = A X.  Each row's sum runs over its CSR entries in stored order with fma (bitwise equal
-// to the oracle's product); the entries of a row are fetched CH at a time (all column
-// indices, then all gathers) so that a lane has CH independent loads in flight.
+// to the oracle's product in plain mode); the entries of a row are fetched CH at a time (all
+// column indices, then all gathers) so that a lane has CH independent loads in flight.
 template <int P, bool EPI>
 __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
     using C = PC<P>;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW, WARPS = NT / 32;
     constexpr int E = P * P + P;
-    constexpr int CH = P <= 8 ? 4 : 4;
+    constexpr int CH = 4;
     DevState* st = a.st;
     if constexpr (EPI) {
         if (!st->run_main) return;
@@ -58,15 +91,28 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
     const int c0 = sub * VEC;
-    __shared__ double sC[EPI ? P * P : 1];
-    __shared__ __align__(16) double sU[WARPS][EPI ? RPW * P : 2];
-    __shared__ __align__(16) double sV[WARPS][EPI ? RPW * P : 2];
-    __shared__ double sAcc[EPI ? E : 1];
+    constexpr int SR = EPI ? RPW * P : 2;
+    extern __shared__ __align__(16) double dyn1[];
+    double* sTk = dyn1;                  // Tr_k
+    double* sD = sTk + P * P;            // Tr_{k-1} C_{k-1}^T
+    double* sTp = sD + P * P;            // scratch: Tr_{k-1}, later the V_k^T W totals
+    double* sCp = sTp + P * P;           // scratch: C_{k-1}
+    double(*sRow)[3][SR] = reinterpret_cast<double(*)[3][SR]>(sCp + P * P);   // A V_k, V_k, V_{k-1} rows
+    double* sAcc = sCp + P * P + WARPS * 3 * SR;
     bool has_prev = false;
     if constexpr (EPI) {
         has_prev = st->k_main > 1;
+        const double* Tk = st->Tr[a.sk];
+        const double* Tp = st->Tr[(a.sk + 2) % 3];
         const double* Cp = st->Ck[a.par ^ 1];   // C_{k-1}
-        for (int t = threadIdx.x; t < P * P; t += NT) sC[t] = Cp[(t / P) * MAXP + t % P];
+        for (int t = threadIdx.x; t < P * P; t += NT) {
+            const int g = (t / P) * MAXP + t % P;
+            sTk[t] = Tk[g];
+            sTp[t] = Tp[g];
+            sCp[t] = Cp[g];
+        }
+        __syncthreads();
+        cta_matmul_nn<P>(sTp, P, sCp, P, sD, P, true);   // D = Tr_{k-1} C_{k-1}^T
         __syncthreads();
     }
     double g[EPI ? P : 1][VEC];
@@ -90,7 +136,7 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
             k1 = __ldg(a.rowptr + i + 1);
             if constexpr (EPI) {
                 ldv<VEC>(a.X + i * P + c0, u);
-                if (has_prev) ldv<VEC>(a.Uprev + i * P + c0, up);
+                if (has_prev) ldv<VEC>(a.Vprev + i * P + c0, up);
             }
         }
         for (int kb = k0; kb < k1; kb += CH) {
@@ -120,33 +166,49 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
                 }
         }
         if constexpr (EPI) {
+            double* rA = sRow[warp][0] + rsub * P;
+            double* rU = sRow[warp][1] + rsub * P;
+            double* rP = sRow[warp][2] + rsub * P;
             if (act) {
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) {
-                    sU[warp][rsub * P + c0 + v] = u[v];
-                    sV[warp][rsub * P + c0 + v] = up[v];
+                    rA[c0 + v] = acc[v];
+                    rU[c0 + v] = u[v];
+                    rP[c0 + v] = up[v];
                 }
             }
             __syncwarp();
             if (valid) {
+                // W = (A V_k) Tr_k = A U_k: the raw candidates, ||A u_j|| (C14)
+                double w[VEC];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) om[v] = fma(acc[v], acc[v], om[v]);
-                if (has_prev) {
-                    // W(:,m) -= sum_b U_{k-1}(:,b) C_{k-1}(m,b)  (h_{i,j} = h_{j,i})
-#pragma unroll
-                    for (int b = 0; b < P; ++b) {
-                        const double x = sV[warp][rsub * P + b];
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) acc[v] = fma(-x, sC[(c0 + v) * P + b], acc[v]);
-                    }
-                }
-                // G(b,m) += U_k(i,b) W(i,m)
+                for (int v = 0; v < VEC; ++v) w[v] = 0.0;
 #pragma unroll
                 for (int b = 0; b < P; ++b) {
-                    const double x = sU[warp][rsub * P + b];
+                    const double x = rA[b];
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v) g[b][v] = fma(x, acc[v], g[b][v]);
+                    for (int v = 0; v < VEC; ++v) w[v] = fma(x, sTk[b * P + c0 + v], w[v]);
                 }
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) om[v] = fma(w[v], w[v], om[v]);
+                if (has_prev) {
+                    // W -= U_{k-1} C_{k-1}^T = V_{k-1} D  (h_{i,j} = h_{j,i})
+#pragma unroll
+                    for (int b = 0; b < P; ++b) {
+                        const double x = rP[b];
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) w[v] = fma(-x, sD[b * P + c0 + v], w[v]);
+                    }
+                }
+                // (V_k^T W)(b,m) += V_k(i,b) W(i,m)
+#pragma unroll
+                for (int b = 0; b < P; ++b) {
+                    const double x = rU[b];
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) g[b][v] = fma(x, w[v], g[b][v]);
+                }
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[v] = w[v];
             }
             __syncwarp();
         }
@@ -177,35 +239,42 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
             }
             __syncthreads();
         }
-        cluster_reduce(sAcc, E, P, a.part, st->G[a.par], st->om2[a.par], &st->cnt1);
+        // totals of V_k^T W land in Gram2 (free until K2 of this block), then G = Tr_k^T (V_k^T W)
+        if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->om2[a.par], &st->cnt1)) {
+            double* sGv = sTp;
+            for (int t = threadIdx.x; t < P * P; t += NT) sGv[t] = st->Gram2[(t / P) * MAXP + t % P];
+            __syncthreads();
+            cta_matmul_tn<P>(sTk, P, sGv, P, st->G[a.par], MAXP);
+        }
     }
 }
 
 // ------------------------------------------------------------------ K2: W' = W - U_k G_s, Grams, C_k
 
 struct K2Args {
-    double* W;
-    const double* U;      // U_k
-    const double* pool;   // n x pool_cap row-major
+    double* W;            // W in, W' out (the V slot of block k+1)
+    const double* V;      // V_k
+    double* pool;         // n x pool_cap row-major
     long long n;
     DevState* st;
     double* part;
-    int par;
+    int par;              // k mod 2
+    int sk;               // k mod 3
 };
 
-// Cholesky W'^T W' = C_k^T C_k (right-looking, warp 0 of the CTA holding the totals), the
-// breakdown / cancellation test, C_k^{-1} and the pool coefficients.  Returns false on a
-// breakdown (the main branch stops at this block and the host runs the column path).
 template <int P>
 struct K2Smem {
     static constexpr int LD = P + 1;
-    static constexpr int loop = P * P + 2 * (NT / 32) * PC<P>::RPW * P + P * P + MAXQ * P;
-    static constexpr int tail = 3 * P * LD + 2 * P;
+    static constexpr int loop = 2 * P * P + P * MAXQ + 2 * (NT / 32) * PC<P>::RPW * P + P * P + MAXQ * P;
+    static constexpr int tail = (3 * P * LD + 2 * P) > (P * P + P * MAXQ) ? (3 * P * LD + 2 * P) : (P * P + P * MAXQ);
     static constexpr size_t bytes = sizeof(double) * (loop + tail);
 };
 
+// Cholesky W'^T W' = C_k^T C_k (right-looking, warp 0 of the CTA holding the totals), the
+// breakdown / cancellation test, C_k^{-1} (= Tr_{k+1}) and the pool coefficients.  Returns
+// false on a breakdown (the main branch stops at this block; the host runs the column path).
 template <int P>
-__device__ bool k3a_factor(DevState* st, int par, double* scratch) {
+__device__ bool k3a_factor(DevState* st, int par, int sk, double* scratch) {
     constexpr int LD = P + 1;
     double* sA = scratch;
     double* sC = sA + P * LD;
@@ -230,7 +299,7 @@ __device__ bool k3a_factor(DevState* st, int par, double* scratch) {
         for (int m = 0; m < P; ++m) {
             const double d = sA[m * LD + m];
             // breakdown: h_{j+p,j}^2 = d <= tau^2 ||A u_j||^2; cancellation guard: the pivot kept
-            // < 1e-4 of ||w'_m||^2 (more than 4 digits lost) -> column path
+            // < 1e-4 of ||w'_m||^2 (more than 4 digits lost) -> column path (R2)
             if (!(d > tau * tau * sOm[m]) || !(d >= 1e-4 * sD[m])) {
                 bad = true;
                 break;
@@ -282,10 +351,11 @@ __device__ bool k3a_factor(DevState* st, int par, double* scratch) {
         }
         return false;
     }
+    double* Tn = st->Tr[(sk + 1) % 3];
     for (int t = tid; t < P * P; t += NT) {
         const int r = t / P, c = t % P;
         st->Ck[par][r * MAXP + c] = sC[r * LD + c];
-        st->Cinv[par][r * MAXP + c] = sCi[r * LD + c];
+        Tn[r * MAXP + c] = sCi[r * LD + c];
     }
     if (tid == 0) {
         st->k_main = st->k_main + 1;
@@ -307,18 +377,36 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
     const int E = P * P + Q * P;
     extern __shared__ __align__(16) double dyn2[];
-    double* sG = dyn2;
-    double(*sU)[RPW * P] = reinterpret_cast<double(*)[RPW * P]>(sG + P * P);
-    double(*sW)[RPW * P] = reinterpret_cast<double(*)[RPW * P]>(sG + P * P + WARPS * RPW * P);
-    double* sAcc = sG + P * P + 2 * WARPS * RPW * P;
+    double* sE = dyn2;                 // Tr_k G_s
+    double* sTk = sE + P * P;          // Tr_k, then scratch
+    double* sF = sTk + P * P;          // Tr_k coef_{k-1} (P x MAXQ)
+    double(*sV)[RPW * P] = reinterpret_cast<double(*)[RPW * P]>(sF + P * MAXQ);
+    double(*sW)[RPW * P] = reinterpret_cast<double(*)[RPW * P]>(sF + P * MAXQ + WARPS * RPW * P);
+    double* sAcc = sF + P * MAXQ + 2 * WARPS * RPW * P;
     double* sTail = sAcc + P * P + MAXQ * P;
-    // G_s: lower triangle of G mirrored (the paper computes h_{i,j} for i >= j)
-    const double* Gp = st->G[a.par];
-    for (int t = threadIdx.x; t < P * P; t += NT) {
-        const int r = t / P, c = t % P;
-        sG[t] = r >= c ? Gp[r * MAXP + c] : Gp[c * MAXP + r];
+    {
+        // G_s: lower triangle of G mirrored (the paper computes h_{i,j} for i >= j)
+        double* sGs = sTail;
+        double* sCo = sTail + P * P;
+        const double* Gp = st->G[a.par];
+        const double* Tk = st->Tr[a.sk];
+        const double* Co = st->coef[a.par ^ 1];
+        for (int t = threadIdx.x; t < P * P; t += NT) {
+            const int r = t / P, c = t % P;
+            sGs[t] = r >= c ? Gp[r * MAXP + c] : Gp[c * MAXP + r];
+            sTk[t] = Tk[r * MAXP + c];
+        }
+        for (int t = threadIdx.x; t < P * MAXQ; t += NT) sCo[t] = Co[t];
+        __syncthreads();
+        cta_matmul_nn<P>(sTk, P, sGs, P, sE, P);
+        for (int t = threadIdx.x; t < P * MAXQ; t += NT) {
+            const int r = t / MAXQ, q = t % MAXQ;
+            double s = 0.0;
+            for (int i = 0; i < P; ++i) s = fma(sTk[r * P + i], sCo[i * MAXQ + q], s);
+            sF[t] = s;
+        }
+        __syncthreads();
     }
-    __syncthreads();
     double g[P][VEC], pq[MAXQ][VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
@@ -334,24 +422,42 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
         double w[VEC], u[VEC], r[MAXQ];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) w[v] = u[v] = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) r[q] = 0.0;
         if (valid) {
             ldc<VEC>(a.W + i * P + c0, w);
-            ldv<VEC>(a.U + i * P + c0, u);
+            ldv<VEC>(a.V + i * P + c0, u);
 #pragma unroll
             for (int q = 0; q < MAXQ; ++q)
                 if (q < Q) r[q] = a.pool[i * qc + qf + q];
         }
         if (act) {
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) sU[warp][rsub * P + c0 + v] = u[v];
+            for (int v = 0; v < VEC; ++v) sV[warp][rsub * P + c0 + v] = u[v];
         }
         __syncwarp();
         if (valid) {
+            // pool r_q -= U_k coef_{k-1}(:,q) = V_k F(:,q)   (orthogonal to the newest block)
+            if (Q > 0) {
+#pragma unroll
+                for (int b = 0; b < P; ++b) {
+                    const double x = sV[warp][rsub * P + b];
+#pragma unroll
+                    for (int q = 0; q < MAXQ; ++q)
+                        if (q < Q) r[q] = fma(-x, sF[b * MAXQ + q], r[q]);
+                }
+                if (sub == 0) {
+#pragma unroll
+                    for (int q = 0; q < MAXQ; ++q)
+                        if (q < Q) a.pool[i * qc + qf + q] = r[q];
+                }
+            }
+            // W' = W - U_k G_s = W - V_k (Tr_k G_s)
 #pragma unroll
             for (int b = 0; b < P; ++b) {
-                const double x = sU[warp][rsub * P + b];
+                const double x = sV[warp][rsub * P + b];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) w[v] = fma(-x, sG[b * P + c0 + v], w[v]);
+                for (int v = 0; v < VEC; ++v) w[v] = fma(-x, sE[b * P + c0 + v], w[v]);
             }
             stv<VEC>(a.W + i * P + c0, w);
         }
@@ -408,95 +514,7 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
         }
         __syncthreads();
     }
-    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->pdot, &st->cnt2)) k3a_factor<P>(st, a.par, sTail);
-}
-
-// ------------------------------------------------------------------ K4a: U_{k+1} = W' C_k^{-1}
-
-struct K4aArgs {
-    const double* W;      // W' (or the materialised U_{k+1} when given_main)
-    double* Unext;        // U_{k+1} (the slot of U_{k-1})
-    double* pool;
-    long long n;
-    DevState* st;
-    int par;
-};
-
-template <int P>
-__global__ void __launch_bounds__(NT) k4a_basis(K4aArgs a) {
-    using C = PC<P>;
-    constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW, WARPS = NT / 32;
-    constexpr int RG = 2;
-    DevState* st = a.st;
-    if (!st->run_main) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane % LP, rsub = lane / LP;
-    const bool act = sub < LANES;
-    const int c0 = sub * VEC;
-    const bool given = st->given_main != 0;
-    const int Q = given ? 0 : st->q_live, qf = st->q_first, qc = st->pool_cap;
-    __shared__ double sCi[P * P];
-    __shared__ double sCo[P * MAXQ];
-    __shared__ __align__(16) double sRow[WARPS][RG][RPW * P];
-    for (int t = threadIdx.x; t < P * P; t += NT) sCi[t] = st->Cinv[a.par][(t / P) * MAXP + t % P];
-    for (int t = threadIdx.x; t < P * MAXQ; t += NT) sCo[t] = st->coef[a.par][t];
-    __syncthreads();
-    const long long stride = (long long)gridDim.x * WARPS * RPW * RG;
-    for (long long base = ((long long)blockIdx.x * WARPS + warp) * RPW * RG; base < a.n; base += stride) {
-        double w[RG][VEC];
-        bool valid[RG];
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            const long long i = base + g * RPW + rsub;
-            valid[g] = act && i < a.n;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) w[g][v] = 0.0;
-            if (valid[g]) ldc<VEC>(a.W + i * P + c0, w[g]);
-            if (act) {
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) sRow[warp][g][rsub * P + c0 + v] = w[g][v];
-            }
-        }
-        __syncwarp();
-        double un[RG][VEC];
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) un[g][v] = given ? w[g][v] : 0.0;
-            if (!given) {
-#pragma unroll
-                for (int b = 0; b < P; ++b) {
-                    const double xw = sRow[warp][g][rsub * P + b];
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) un[g][v] = fma(xw, sCi[b * P + c0 + v], un[g][v]);
-                }
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            const long long i = base + g * RPW + rsub;
-            if (valid[g]) stv<VEC>(a.Unext + i * P + c0, un[g]);
-            if (act) {
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) sRow[warp][g][rsub * P + c0 + v] = un[g][v];
-            }
-        }
-        if (Q > 0) {
-            __syncwarp();
-#pragma unroll
-            for (int g = 0; g < RG; ++g) {
-                const long long i = base + g * RPW + rsub;
-                if (valid[g])
-                    for (int q = sub; q < Q; q += LANES) {
-                        double r = a.pool[i * qc + qf + q];
-                        for (int b = 0; b < P; ++b) r = fma(-sRow[warp][g][rsub * P + b], sCo[b * MAXQ + q], r);
-                        a.pool[i * qc + qf + q] = r;
-                    }
-            }
-        }
-        __syncwarp();
-    }
+    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->pdot, &st->cnt2)) k3a_factor<P>(st, a.par, a.sk, sTail);
 }
 
 // ------------------------------------------------------------------ K3b: small banded QR (side)
@@ -760,12 +778,13 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
 // ------------------------------------------------------------------ K4b: directions and X (side)
 
 struct K4bArgs {
-    const double* U;      // U_k
+    const double* U;      // V_k (U_k = V_k Tr_k)
     double* M2;           // M_{k-2} in, M_k out
     const double* M1;     // M_{k-1}
     double* X;
     long long n;
     DevState* st;
+    int sk;               // k mod 3
 };
 
 template <int P>
@@ -790,14 +809,29 @@ __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
     double* sB2 = sB1 + P * P;
     double* sZ = sB2 + P * P;
     double(*sRow)[RG][3][RPW * P] = reinterpret_cast<double(*)[RG][3][RPW * P]>(sZ + P * P);
-    for (int t = threadIdx.x; t < P * P; t += NT) {
-        const int g = (t / P) * MAXP + t % P;
-        sAi[t] = st->Ainv[g];
-        sB1[t] = st->B1[g];
-        sB2[t] = st->B2[g];
-        sZ[t] = st->Z[g];
+    {
+        // sAi = Tr_k R_kk^{-1} (built in sZ's space first)
+        double* sT = sAi;
+        double* sR = sB1;
+        const double* Tk = st->Tr[a.sk];
+        for (int t = threadIdx.x; t < P * P; t += NT) {
+            const int g = (t / P) * MAXP + t % P;
+            sT[t] = Tk[g];
+            sR[t] = st->Ainv[g];
+        }
+        __syncthreads();
+        cta_matmul_nn<P>(sT, P, sR, P, sZ, P);
+        __syncthreads();
+        for (int t = threadIdx.x; t < P * P; t += NT) {
+            const int g = (t / P) * MAXP + t % P;
+            sAi[t] = sZ[t];
+            sB1[t] = st->B1[g];
+            sB2[t] = st->B2[g];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < P * P; t += NT) sZ[t] = st->Z[(t / P) * MAXP + t % P];
+        __syncthreads();
     }
-    __syncthreads();
     const long long stride = (long long)gridDim.x * WARPS * RPW * RG;
     for (long long base = ((long long)blockIdx.x * WARPS + warp) * RPW * RG; base < a.n; base += stride) {
         double u[RG][VEC], m2[RG][VEC], m1[RG][VEC], x[RG][VEC];
