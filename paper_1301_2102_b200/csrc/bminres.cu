@@ -23,6 +23,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "step_kernels.cuh"
+#include "dmma_kernels.cuh"
 
 using namespace bmr;
 
@@ -42,20 +43,38 @@ struct Kfn {  // per-p kernel table
     void (*k3b)(DevState*);
     void (*k4b)(K4bArgs);
     size_t smem1, smem2, smem3, smem4b;
+    int nt1, nt2, nt4b;
 };
 
 template <int P>
 Kfn make_kfn() {
     Kfn f;
     f.k1 = k1_spmm<P, true>;
+    f.nt1 = NT;
+    f.smem1 = K1Smem<P>::bytes;
     f.k1plain = k1_spmm<P, false>;
     f.k2 = k2_orth<P>;
-    f.k3b = k3b_smallqr<P>;
-    f.k4b = k4b_update<P>;
-    f.smem1 = K1Smem<P>::bytes;
+    f.nt2 = NT;
     f.smem2 = K2Smem<P>::bytes;
+    f.k3b = k3b_smallqr<P>;
+    if constexpr (P % 8 == 0) {
+        if (!getenv("BMINRES_NO_DMMA")) {
+            f.k1 = k1_dmma<P>;
+            f.smem1 = K1DSmem<P>::bytes;
+            f.nt1 = 256;
+            f.k2 = k2_dmma<P>;
+            f.smem2 = K2DSmem<P>::bytes;
+            f.nt2 = 128;
+        }
+        f.k4b = k4b_dmma<P>;
+        f.smem4b = K4bDSmem<P>::bytes;
+        f.nt4b = 128;
+    } else {
+        f.k4b = k4b_update<P>;
+        f.smem4b = K4bSmem<P>::bytes;
+        f.nt4b = NT;
+    }
     f.smem3 = K3Smem<P>::bytes;
-    f.smem4b = K4bSmem<P>::bytes;
     return f;
 }
 
@@ -127,7 +146,7 @@ struct bminres_ctx {
     std::vector<cudaEvent_t> evpool;
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> ev_marks;   // (phase, index of start event)
-    int nb1 = 0, nb2 = 0, nb4 = 0;
+    int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
     long long side_blocks = 0, slow_blocks = 0;
     Kfn kf{};
 };
@@ -239,15 +258,15 @@ int cluster_grid(bminres_ctx* h, const void* fn, size_t smem, long long n, long 
 }
 
 template <typename K, typename A>
-void launch_cluster(bminres_ctx* h, K kern, int grid, size_t smem, A args, const char* what) {
+void launch_cluster(bminres_ctx* h, K kern, int grid, int nt, size_t smem, A args, const char* what) {
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.x = h->csz;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NT);
+    cfg.blockDim = dim3(nt);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = h->stream;
     cfg.attrs = at;
@@ -287,14 +306,27 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     h->n_ws = n;
     h->p_ws = p;
     h->q_ws = q;
-    // grids of the reducing panel kernels: as many whole clusters of CL CTAs as can be resident
-    long long rows_per_cta = (long long)(NT / 32) * (32 / std::max(1, (p % 2 == 0 ? p / 2 : p)));
-    h->nb1 = cluster_grid(h, (const void*)h->kf.k1, h->kf.smem1, n, rows_per_cta);
-    h->nb2 = cluster_grid(h, (const void*)h->kf.k2, h->kf.smem2, n, rows_per_cta);
-    int occ4 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, (const void*)h->kf.k4b, NT, h->kf.smem4b);
-    occ4 = std::max(1, occ4);
-    h->nb4 = grid_for(h, n, (int)std::max<long long>(1, rows_per_cta), h->n_sm * occ4);
+    // persistent one-wave grids, balanced: every SM gets the same number of CTAs; the reducing
+    // kernels use clusters of h->csz CTAs (BMINRES_CLUSTER overrides, for experiments)
+    auto occ_of = [&](const void* fn, int nt, size_t smem) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, nt, smem);
+        return std::max(1, o);
+    };
+    const char* ce = getenv("BMINRES_CLUSTER");
+    h->csz = ce ? std::max(1, std::min(8, atoi(ce))) : 2;
+    const char* oe = getenv("BMINRES_CTAS_PER_SM");
+    const int cap = oe ? std::max(1, atoi(oe)) : 8;
+    const int o1 = std::min(cap, occ_of((const void*)h->kf.k1, h->kf.nt1, h->kf.smem1));
+    const int o2 = std::min(cap, occ_of((const void*)h->kf.k2, h->kf.nt2, h->kf.smem2));
+    int o4 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, (const void*)h->kf.k4b, h->kf.nt4b, h->kf.smem4b);
+    o4 = std::min(cap, std::max(1, o4));
+    h->nb1 = std::min(NB_MAX, h->n_sm * o1) / h->csz * h->csz;
+    h->nb2 = std::min(NB_MAX, h->n_sm * o2) / h->csz * h->csz;
+    h->nb4 = h->n_sm * o4;
+    (void)cluster_grid;
+
 }
 
 // ------------------------------------------------------------------ generic column ops
@@ -381,20 +413,20 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
     TimeMark tm(h, PH_SPMM);
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
-             par, sk};
+             par, sk, h->tpw};
     cudaStream_t keep = h->stream;
     h->stream = s;
-    launch_cluster(h, h->kf.k1, h->nb1, h->kf.smem1, a, "k1_spmm");
+    launch_cluster(h, h->kf.k1, h->nb1, h->kf.nt1, h->kf.smem1, a, "k1_spmm");
     h->stream = keep;
 }
 void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k) {
     TimeMark tm(h, PH_ORTH);
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K2Args a{h->V[(sk + 1) % 3], h->V[sk], h->pool, n, h->st, h->part + (size_t)NB_MAX * (MAXP * MAXP + MAXP),
-             par, sk};
+             par, sk, h->tpw};
     cudaStream_t keep = h->stream;
     h->stream = s;
-    launch_cluster(h, h->kf.k2, h->nb2, h->kf.smem2, a, "k2_orth");
+    launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
     h->stream = keep;
 }
 // side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
@@ -406,8 +438,8 @@ void launch_k3b(bminres_ctx* h, cudaStream_t s) {
 void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k) {
     TimeMark tm(h, PH_UPDATE);
     const int sk = (int)(k % 3), par = (int)(k & 1);
-    K4bArgs a{h->V[sk], h->M[par], h->M[par ^ 1], sp.X, n, h->st, sk};
-    h->kf.k4b<<<h->nb4, NT, h->kf.smem4b, s>>>(a);
+    K4bArgs a{h->V[sk], h->M[par], h->M[par ^ 1], sp.X, n, h->st, sk, h->tpw};
+    h->kf.k4b<<<h->nb4, h->kf.nt4b, h->kf.smem4b, s>>>(a);
     check_launch(h, "k4b_update");
 }
 
@@ -737,8 +769,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // F0 = B - A X0 (C6) into the V slot of block 1 (U_1 = V_1, Tr_1 = I)
         double* F = h->V[1];
         if (o.use_x0) {
-            K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0, 0};
-            h->kf.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
+            K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0, 0, h->tpw};
+            h->kf.k1plain<<<h->nb4, NT, 0, h->stream>>>(a);
             check_launch(h, "k1_spmm(plain)");
             k_sub_from<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(B, F, (long long)panel);
             check_launch(h, "k_sub_from");
@@ -908,8 +940,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
     {
         TimeMark tm(h, PH_RESID);
-        K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->M[0], n, h->st, nullptr, 0, 0};
-        h->kf.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
+        K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->M[0], n, h->st, nullptr, 0, 0, h->tpw};
+        h->kf.k1plain<<<h->nb4, NT, 0, h->stream>>>(a);
         check_launch(h, "k1_spmm(plain)");
         launch_colsq(h, B, h->M[0], n, p, h->dsc);
     }
@@ -1075,8 +1107,14 @@ int bminres_spmm(bminres_handle h, const bminres_csr* A, const double* X, double
         if ((((uintptr_t)X) | ((uintptr_t)Y)) & 15) fail(h, BMINRES_EINVAL, "X and Y must be 16-byte aligned");
         CK(cudaSetDevice(h->device));
         const long long n = A->n_loc;
-        K1Args a{A->row_ptr, A->col_idx, A->values, X, nullptr, Y, n, nullptr, nullptr, 0, 0};
-        f.k1plain<<<grid_for(h, n, 256, 8 * h->n_sm), NT, 0, h->stream>>>(a);
+        const int vec = (p % 2 == 0) ? 2 : 1, lanes = p / vec;
+        int lp = 1;
+        while (lp < lanes) lp <<= 1;
+        const long long rpw = 32 / lp, ntiles = (n + rpw - 1) / rpw, warps = NT / 32;
+        const int tpw = (int)std::max<long long>(4, (ntiles + warps * 65536 - 1) / (warps * 65536));
+        const long long ctas = std::max<long long>(1, (ntiles + warps * tpw - 1) / (warps * tpw));
+        K1Args a{A->row_ptr, A->col_idx, A->values, X, nullptr, Y, n, nullptr, nullptr, 0, 0, tpw};
+        f.k1plain<<<(unsigned)ctas, NT, 0, h->stream>>>(a);
         check_launch(h, "k1_spmm(plain)");
         CK(cudaStreamSynchronize(h->stream));
         return BMINRES_OK;

@@ -40,6 +40,9 @@ struct PC {
     static constexpr int LANES = P / VEC;
     static constexpr int LP = LANES <= 1 ? 1 : LANES <= 2 ? 2 : LANES <= 4 ? 4 : LANES <= 8 ? 8 : LANES <= 16 ? 16 : 32;
     static constexpr int RPW = 32 / LP;
+    // shared-memory row stride: p + 2 doubles (p + 1 for odd p) so that the RPW rows a warp
+    // reads in one instruction fall on distinct banks, keeping 16-byte alignment for cp.async
+    static constexpr int RS = P + (VEC == 2 ? 2 : 1);
 };
 
 // Mapped (pinned, host-visible) flags the kernels publish; the host polls them.
@@ -132,6 +135,28 @@ __device__ __forceinline__ void stv(double* p, const double (&r)[VEC]) {
     }
 }
 
+// cp.async (LDGSTS) helpers: src-size 0 zero-fills the destination without reading src
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    const int nb = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(nb) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    const int nb = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(nb) : "memory");
+}
+template <int VEC>
+__device__ __forceinline__ void cp_async_vec(double* sdst, const double* gsrc, bool pred) {
+    if constexpr (VEC == 2)
+        cp_async16(sdst, gsrc, pred);
+    else
+        cp_async8(sdst, gsrc, pred);
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -155,13 +180,13 @@ __device__ __forceinline__ bool cluster_reduce(double* sAcc, int E, int P, doubl
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     const unsigned rank = cl.block_rank();
-    const int ncl = gridDim.x / CL, cid = blockIdx.x / CL;
+    const int csz = (int)cl.num_blocks();
+    const int ncl = gridDim.x / csz, cid = blockIdx.x / csz;
     if (rank == 0) {
         for (int e = threadIdx.x; e < E; e += blockDim.x) {
             double s = 0.0;
-#pragma unroll
-            for (int r = 0; r < CL; ++r) s += cl.map_shared_rank(sAcc, r)[e];
-            part[(size_t)e * ncl + cid] = s;
+            for (int r = 0; r < csz; ++r) s += cl.map_shared_rank(sAcc, r)[e];
+            part[(size_t)cid * E + e] = s;   // partial-major: the final sum reads coalesced rows
         }
     }
     cl.sync();  // remote shared memory must outlive the leader's reads
@@ -173,17 +198,22 @@ __device__ __forceinline__ bool cluster_reduce(double* sAcc, int E, int P, doubl
     __syncthreads();
     if (!s_last) return false;
     __threadfence();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int e = warp; e < E; e += nw) {
-        double s = 0.0;
-        for (int b = lane; b < ncl; b += 32) s += __ldcg(part + (size_t)e * ncl + b);
-        s = warp_sum(s);
-        if (lane == 0) {
-            if (e < P * P)
-                outA[(e / P) * MAXP + e % P] = s;
-            else
-                outB[((e - P * P) / P) * MAXP + (e - P * P) % P] = s;
+    // one thread per entry; 8 independent accumulators (fixed order), loads coalesced across threads
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+        int b = 0;
+        for (; b + 8 <= ncl; b += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] += __ldcg(part + (size_t)(b + u) * E + e);
         }
+        for (; b < ncl; ++b) acc[0] += __ldcg(part + (size_t)b * E + e);
+        const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        if (e < P * P)
+            outA[(e / P) * MAXP + e % P] = s;
+        else
+            outB[((e - P * P) / P) * MAXP + (e - P * P) % P] = s;
     }
     if (threadIdx.x == 0) *cnt = 0u;
     __syncthreads();

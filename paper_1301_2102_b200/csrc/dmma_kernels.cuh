@@ -1,0 +1,567 @@
+// dmma_kernels.cuh -- panel kernels whose row-local dense products run on the fp64 tensor
+// cores (mma.sync m8n8k4 f64, "DMMA"), for block sizes p that are multiples of 8.
+//
+// A warp owns a tile of TR panel rows.  Tiles are staged in shared memory by cp.async
+// (NSTAGE-deep, one commit group per tile) with row stride RS = p + 4 doubles, which makes
+// every fragment load bank-conflict free.  Fragment layouts (PTX mma.m8n8k4 .f64, as in
+// CuTe's SM80_8x8x4_F64F64F64F64_TN): A(8x4) lane l holds A[l/4][l%4]; B(4x8) B[l%4][l/4];
+// C(8x8) C[l/4][2(l%4)+v], v = 0,1.  Constant p x p factors are kept in shared memory in
+// fragment order (32 consecutive doubles per 4x8 block) so B-fragment loads are conflict free.
+#pragma once
+#include "common.cuh"
+#include "step_kernels.cuh"
+
+namespace bmr {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int P>
+struct DM {
+    static constexpr int RS = P + 4;                 // smem row stride (doubles)
+    static constexpr int TR = P <= 8 ? 16 : 8;       // rows per warp tile
+    static constexpr int KC = P / 4, NC = P / 8;     // k- and n-chunks of a p x p factor
+    static constexpr int FR = KC * NC * 32;          // doubles of one factor in fragment order
+    static constexpr int TILE = TR * RS;             // doubles of one staged panel tile
+    static constexpr int CPR = P / 2;                // 16-byte chunks per row
+};
+
+// store p x p factor M (leading dimension ld, optional sign) into fragment order
+template <int P>
+__device__ __forceinline__ void to_frag(const double* M, int ld, double sign, double* F) {
+    using D = DM<P>;
+    for (int t = threadIdx.x; t < D::FR; t += blockDim.x) {
+        const int blk = t / 32, l = t % 32, kc = blk / D::NC, nc = blk % D::NC;
+        F[t] = sign * M[(kc * 4 + l % 4) * ld + nc * 8 + l / 4];
+    }
+}
+
+// cp.async one TR x P tile of a row-major panel (rows base.., zero-fill past n) into smem
+template <int P>
+__device__ __forceinline__ void stage_tile(double* dst, const double* src, long long base, long long n, int lane) {
+    using D = DM<P>;
+    for (int c = lane; c < D::TR * D::CPR; c += 32) {
+        const int r = c / D::CPR, q = c % D::CPR;
+        const long long i = base + r;
+        const bool ok = i < n;
+        cp_async16(dst + r * D::RS + 2 * q, src + (ok ? i : 0) * P + 2 * q, ok);
+    }
+}
+
+// ------------------------------------------------------------------ K4b on DMMA
+
+template <int P>
+struct K4bDSmem {
+    static constexpr int WARPS = 4;
+    static constexpr size_t bytes = sizeof(double) * (4 * DM<P>::FR + WARPS * NSTAGE * 4 * DM<P>::TILE);
+};
+
+template <int P>
+__global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
+    using D = DM<P>;
+    constexpr int WARPS = K4bDSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
+    DevState* st = a.st;
+    if (!st->side_go) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    extern __shared__ __align__(16) double dynd4[];
+    double* fA = dynd4;        // Tr_k R_kk^{-1}
+    double* fB2 = fA + FR;     // -R_{k-2,k} R_kk^{-1}
+    double* fB1 = fB2 + FR;    // -R_{k-1,k} R_kk^{-1}
+    double* fZ = fB1 + FR;     // Z_k
+    double* pipe = fZ + FR;
+    {
+        // scratch for Tr_k and R_kk^{-1} (P x P each) in the pipeline area, then fragments
+        double* sT = pipe;
+        double* sR = pipe + P * P;
+        double* sP = pipe + 2 * P * P;
+        const double* Tk = st->Tr[a.sk];
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            const int g = (t / P) * MAXP + t % P;
+            sT[t] = Tk[g];
+            sR[t] = st->Ainv[g];
+        }
+        __syncthreads();
+        cta_matmul_nn<P>(sT, P, sR, P, sP, P);
+        __syncthreads();
+        to_frag<P>(sP, P, 1.0, fA);
+        to_frag<P>(st->B2, MAXP, -1.0, fB2);
+        to_frag<P>(st->B1, MAXP, -1.0, fB1);
+        to_frag<P>(st->Z, MAXP, 1.0, fZ);
+        __syncthreads();
+    }
+    double* wb = pipe + warp * NSTAGE * 4 * D::TILE;
+    const long long ntiles = (a.n + TR - 1) / TR;
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    auto issue = [&](long long it, int slot) {
+        const long long t = t0 + it * ts;
+        if (t < ntiles) {
+            double* sl = wb + slot * 4 * D::TILE;
+            const long long base = t * TR;
+            stage_tile<P>(sl, a.U, base, a.n, lane);
+            stage_tile<P>(sl + D::TILE, a.M2, base, a.n, lane);
+            stage_tile<P>(sl + 2 * D::TILE, a.M1, base, a.n, lane);
+            stage_tile<P>(sl + 3 * D::TILE, a.X, base, a.n, lane);
+        }
+        cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    const int fr = lane >> 2, fc = lane & 3;   // A-fragment row / col within an 8x4 block
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
+        cp_wait<NSTAGE - 1>();
+        __syncwarp();
+        double* sl = wb + (int)(it % NSTAGE) * 4 * D::TILE;
+        const double* tV = sl;
+        double* tM2 = sl + D::TILE;
+        const double* tM1 = sl + 2 * D::TILE;
+        const double* tX = sl + 3 * D::TILE;
+        const long long base = (t0 + it * ts) * TR;
+#pragma unroll
+        for (int mc = 0; mc < TR / 8; ++mc) {
+            const int r0 = mc * 8;
+            // M_k = V (Tr_k R_kk^{-1}) - M_{k-2} B2 - M_{k-1} B1  (eqn.search-dir-comp)
+            double mk[NC][2];
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                mk[nc][0] = mk[nc][1] = 0.0;
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc) {
+                    const int ai = (r0 + fr) * RS + kc * 4 + fc;
+                    const int bi = (kc * NC + nc) * 32 + lane;
+                    dmma(mk[nc][0], mk[nc][1], tV[ai], fA[bi]);
+                    dmma(mk[nc][0], mk[nc][1], tM2[ai], fB2[bi]);
+                    dmma(mk[nc][0], mk[nc][1], tM1[ai], fB1[bi]);
+                }
+            }
+            __syncwarp();
+            // M_k overwrites this chunk's M_{k-2} rows (in smem and in HBM)
+            const long long row = base + r0 + fr;
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const int col = nc * 8 + 2 * fc;
+                tM2[(r0 + fr) * RS + col] = mk[nc][0];
+                tM2[(r0 + fr) * RS + col + 1] = mk[nc][1];
+                if (row < a.n)
+                    *reinterpret_cast<double2*>(a.M2 + row * P + col) = make_double2(mk[nc][0], mk[nc][1]);
+            }
+            __syncwarp();
+            // X += M_k Z_k  (eqn.approx-update)
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const int col = nc * 8 + 2 * fc;
+                double x0 = tX[(r0 + fr) * RS + col], x1 = tX[(r0 + fr) * RS + col + 1];
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                    dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], fZ[(kc * NC + nc) * 32 + lane]);
+                if (row < a.n) *reinterpret_cast<double2*>(a.X + row * P + col) = make_double2(x0, x1);
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+}
+
+
+// Sum one warp-fragment accumulator of an 8x8 block (C layout) into sAcc[base + row*ld + col]
+// in fixed warp order (called by every warp in turn between __syncthreads).
+__device__ __forceinline__ void frag_acc(double* sAcc, int base, int ld, int m0, int n0, const double (&c)[2],
+                                         bool first, int lane) {
+    const int r = m0 + (lane >> 2), col = n0 + 2 * (lane & 3);
+    double* d = sAcc + base + r * ld + col;
+    d[0] = (first ? 0.0 : d[0]) + c[0];
+    d[1] = (first ? 0.0 : d[1]) + c[1];
+}
+
+// ------------------------------------------------------------------ K2 on DMMA
+
+template <int P>
+struct K2DSmem {
+    static constexpr int WARPS = 4;
+    static constexpr int RSQ = 12;                        // pool tile row stride (8 columns + pad)
+    static constexpr int TQ = DM<P>::TR * RSQ;
+    static constexpr int pipe = WARPS * NSTAGE * (2 * DM<P>::TILE + TQ);
+    static constexpr int LD = P + 1;
+    static constexpr int tail = (3 * P * LD + 2 * P) > (3 * P * P) ? (3 * P * LD + 2 * P) : (3 * P * P);
+    static constexpr size_t bytes = sizeof(double) * (DM<P>::FR + DM<P>::KC * 32 + pipe + P * P + MAXQ * P + tail);
+};
+
+template <int P>
+__global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
+    using D = DM<P>;
+    using S = K2DSmem<P>;
+    constexpr int WARPS = S::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR, RSQ = S::RSQ;
+    DevState* st = a.st;
+    if (!st->run_main) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
+    const int E = P * P + Q * P;
+    extern __shared__ __align__(16) double dynd2[];
+    double* fE = dynd2;              // -(Tr_k G_s) in fragment order
+    double* fF = fE + FR;            // -(Tr_k coef_{k-1}) (P x 8) in fragment order (KC blocks)
+    double* pipe = fF + KC * 32;
+    double* sAcc = pipe + S::pipe;
+    double* sTail = sAcc + P * P + MAXQ * P;
+    {
+        // G_s: lower triangle of G mirrored (the paper computes h_{i,j} for i >= j)
+        double* sGs = sTail;
+        double* sTk = sTail + P * P;
+        double* sX = sTail + 2 * P * P;
+        const double* Gp = st->G[a.par];
+        const double* Tk = st->Tr[a.sk];
+        const double* Co = st->coef[a.par ^ 1];
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            const int r = t / P, c = t % P;
+            sGs[t] = r >= c ? Gp[r * MAXP + c] : Gp[c * MAXP + r];
+            sTk[t] = Tk[r * MAXP + c];
+        }
+        __syncthreads();
+        cta_matmul_nn<P>(sTk, P, sGs, P, sX, P);
+        __syncthreads();
+        to_frag<P>(sX, P, -1.0, fE);
+        // F = Tr_k coef_{k-1}: P x 8 (pool columns q < Q, the rest 0), fragment order over KC blocks
+        for (int t = threadIdx.x; t < KC * 32; t += blockDim.x) {
+            const int kc = t / 32, l = t % 32, r = kc * 4 + l % 4, q = l / 4;
+            double s = 0.0;
+            if (q < Q)
+                for (int i = 0; i < P; ++i) s = fma(sTk[r * P + i], Co[i * MAXQ + q], s);
+            fF[t] = -s;
+        }
+        __syncthreads();
+    }
+    double g[NC][NC][2], pq[NC][2];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+        pq[i][0] = pq[i][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    }
+    double* wb = pipe + warp * NSTAGE * (2 * D::TILE + S::TQ);
+    const long long ntiles = (a.n + TR - 1) / TR;
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    auto issue = [&](long long it, int slot) {
+        const long long t = t0 + it * ts;
+        if (t < ntiles) {
+            double* sl = wb + slot * (2 * D::TILE + S::TQ);
+            const long long base = t * TR;
+            stage_tile<P>(sl, a.W, base, a.n, lane);
+            stage_tile<P>(sl + D::TILE, a.V, base, a.n, lane);
+            for (int c = lane; c < TR * MAXQ; c += 32) {
+                const int r = c / MAXQ, q = c % MAXQ;
+                const long long i = base + r;
+                const bool ok = i < a.n && q < Q;
+                if (q < Q || true)
+                    cp_async8(sl + 2 * D::TILE + r * RSQ + q, a.pool + (ok ? i * qc + qf + q : 0), ok);
+            }
+        }
+        cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
+        cp_wait<NSTAGE - 1>();
+        __syncwarp();
+        double* sl = wb + (int)(it % NSTAGE) * (2 * D::TILE + S::TQ);
+        double* tW = sl;
+        const double* tV = sl + D::TILE;
+        double* tR = sl + 2 * D::TILE;
+        const long long base = (t0 + it * ts) * TR;
+#pragma unroll
+        for (int mc = 0; mc < TR / 8; ++mc) {
+            const int r0 = mc * 8;
+            const long long row = base + r0 + fr;
+            const bool rok = row < a.n;
+            if (Q > 0) {
+                // pool r_q -= U_k coef_{k-1}(:,q) = V_k F(:,q)
+                double c0 = tR[(r0 + fr) * RSQ + 2 * fc], c1 = tR[(r0 + fr) * RSQ + 2 * fc + 1];
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc) dmma(c0, c1, tV[(r0 + fr) * RS + kc * 4 + fc], fF[kc * 32 + lane]);
+                tR[(r0 + fr) * RSQ + 2 * fc] = c0;
+                tR[(r0 + fr) * RSQ + 2 * fc + 1] = c1;
+                if (rok) {
+                    if (2 * fc < Q) a.pool[row * qc + qf + 2 * fc] = c0;
+                    if (2 * fc + 1 < Q) a.pool[row * qc + qf + 2 * fc + 1] = c1;
+                }
+            }
+            // W' = W - U_k G_s = W - V_k (Tr_k G_s)
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const int col = nc * 8 + 2 * fc;
+                double c0 = tW[(r0 + fr) * RS + col], c1 = tW[(r0 + fr) * RS + col + 1];
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                    dmma(c0, c1, tV[(r0 + fr) * RS + kc * 4 + fc], fE[(kc * NC + nc) * 32 + lane]);
+                tW[(r0 + fr) * RS + col] = c0;
+                tW[(r0 + fr) * RS + col + 1] = c1;
+                if (rok) *reinterpret_cast<double2*>(a.W + row * P + col) = make_double2(c0, c1);
+            }
+        }
+        __syncwarp();
+        // W'^T W' and R^T W' over the tile's rows, 4 rows per MMA
+#pragma unroll
+        for (int k0 = 0; k0 < TR; k0 += 4) {
+            const double* rw = tW + (k0 + fc) * RS;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const double av = rw[i * 8 + fr];
+#pragma unroll
+                for (int j = 0; j < NC; ++j) dmma(g[i][j][0], g[i][j][1], av, rw[j * 8 + fr]);
+            }
+            if (Q > 0) {
+                const double ar = tR[(k0 + fc) * RSQ + fr];
+#pragma unroll
+                for (int j = 0; j < NC; ++j) dmma(pq[j][0], pq[j][1], ar, rw[j * 8 + fr]);
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+    // rows past n were zero-filled, so they contribute nothing; reduce across warps (fixed order)
+    for (int w = 0; w < WARPS; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j < NC; ++j) frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
+            if (Q > 0) {
+                // pdot(q, m) = (R^T W')(q, m) at P*P + q*P + m, q < Q
+                const int q = fr;
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    const int col = j * 8 + 2 * fc;
+                    if (q < Q) {
+                        double* d = sAcc + P * P + q * P + col;
+                        d[0] = (w == 0 ? 0.0 : d[0]) + pq[j][0];
+                        d[1] = (w == 0 ? 0.0 : d[1]) + pq[j][1];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->pdot, &st->cnt2)) k3a_factor<P>(st, a.par, a.sk, sTail);
+}
+
+
+// ------------------------------------------------------------------ K1 on DMMA (epilogue)
+
+constexpr int K1STAGE = 2;   // V tiles are needed only after the gathers: a short pipeline
+
+template <int P>
+struct K1DSmem {
+    static constexpr int WARPS = 8;
+    static constexpr int pipe = WARPS * (K1STAGE * 2 + 1) * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile
+    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + pipe + P * P + P + 3 * P * P);
+};
+
+// W = (A V_k) Tr_k - V_{k-1} (Tr_{k-1} C_{k-1}^T); ||A u_j||^2; V_k^T W.  The gathers of the SpMM
+// are per lane (LP lanes x 16 B per row, each row summed in CSR order with fma); the three
+// row-local products run as DMMA on the staged tiles.
+template <int P>
+__global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
+    using D = DM<P>;
+    using C = PC<P>;
+    constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
+    constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
+    constexpr int E = P * P + P;
+    constexpr int CH = 4;
+    DevState* st = a.st;
+    if (!st->run_main) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int sub = lane % LP, rsub = lane / LP;
+    const bool act = sub < LANES;
+    const int c0 = sub * VEC;
+    extern __shared__ __align__(16) double dynd1[];
+    double* fT = dynd1;            // Tr_k
+    double* fD = fT + FR;          // -(Tr_{k-1} C_{k-1}^T)
+    double* pipe = fD + FR;
+    double* sAcc = pipe + K1DSmem<P>::pipe;
+    double* sScr = sAcc + P * P + P;
+    const bool has_prev = st->k_main > 1;
+    {
+        double* sTp = sScr;
+        double* sCp = sScr + P * P;
+        double* sX = sScr + 2 * P * P;
+        const double* Tk = st->Tr[a.sk];
+        const double* Tp = st->Tr[(a.sk + 2) % 3];
+        const double* Cp = st->Ck[a.par ^ 1];   // C_{k-1}
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            const int g = (t / P) * MAXP + t % P;
+            sTp[t] = Tp[g];
+            sCp[t] = Cp[g];
+        }
+        to_frag<P>(Tk, MAXP, 1.0, fT);
+        __syncthreads();
+        cta_matmul_nn<P>(sTp, P, sCp, P, sX, P, true);   // D = Tr_{k-1} C_{k-1}^T
+        __syncthreads();
+        to_frag<P>(sX, P, -1.0, fD);
+        __syncthreads();
+    }
+    double g[NC][NC][2], om[NC][2];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+        om[i][0] = om[i][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    }
+    double* wb = pipe + warp * (K1STAGE * 2 + 1) * D::TILE;
+    double* tA = wb + K1STAGE * 2 * D::TILE;   // A V_k rows, then W rows
+    const long long ntiles = (a.n + TR - 1) / TR;
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    auto issue = [&](long long it, int slot) {
+        const long long t = t0 + it * ts;
+        if (t < ntiles) {
+            double* sl = wb + slot * 2 * D::TILE;
+            stage_tile<P>(sl, a.X, t * TR, a.n, lane);
+            if (has_prev) stage_tile<P>(sl + D::TILE, a.Vprev, t * TR, a.n, lane);
+        }
+        cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < K1STAGE - 1; ++s) issue(s, s);
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + K1STAGE - 1, (int)((it + K1STAGE - 1) % K1STAGE));
+        const long long base = (t0 + it * ts) * TR;
+        // ---- SpMM rows of the tile: acc = sum_j a_ij V_k(j,:)  (CSR order, fma)
+#pragma unroll
+        for (int gp = 0; gp < TR / RPW; ++gp) {
+            const int rl = gp * RPW + rsub;
+            const long long i = base + rl;
+            const bool valid = act && i < a.n;
+            double acc[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+            int k0 = 0, k1 = 0;
+            if (valid) {
+                k0 = __ldg(a.rowptr + i);
+                k1 = __ldg(a.rowptr + i + 1);
+            }
+            for (int kb = k0; kb < k1; kb += CH) {
+                int cc[CH];
+                double av[CH];
+                double xv[CH][VEC];
+#pragma unroll
+                for (int t = 0; t < CH; ++t) {
+                    const bool pr = kb + t < k1;
+                    cc[t] = pr ? __ldg(a.col + kb + t) : -1;
+                    av[t] = pr ? __ldg(a.val + kb + t) : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < CH; ++t) {
+                    if (cc[t] >= 0) {
+                        ldv<VEC>(a.X + (long long)cc[t] * P + c0, xv[t]);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < CH; ++t)
+                    if (cc[t] >= 0) {
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
+                    }
+            }
+            if (act) {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) tA[rl * RS + c0 + v] = acc[v];
+            }
+        }
+        cp_wait<K1STAGE - 1>();
+        __syncwarp();
+        const double* sl = wb + (int)(it % K1STAGE) * 2 * D::TILE;
+        const double* tV = sl;
+        const double* tP = sl + D::TILE;
+#pragma unroll
+        for (int mc = 0; mc < TR / 8; ++mc) {
+            const int r0 = mc * 8;
+            const long long row = base + r0 + fr;
+            const bool rok = row < a.n;
+            double w[NC][2];
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                w[nc][0] = w[nc][1] = 0.0;
+                // W = (A V_k) Tr_k = A U_k, the raw candidates; ||A u_j||^2 (C14)
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                    dmma(w[nc][0], w[nc][1], tA[(r0 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
+                om[nc][0] = fma(w[nc][0], w[nc][0], om[nc][0]);
+                om[nc][1] = fma(w[nc][1], w[nc][1], om[nc][1]);
+                // W -= U_{k-1} C_{k-1}^T = V_{k-1} D  (h_{i,j} = h_{j,i})
+                if (has_prev) {
+#pragma unroll
+                    for (int kc = 0; kc < KC; ++kc)
+                        dmma(w[nc][0], w[nc][1], tP[(r0 + fr) * RS + kc * 4 + fc], fD[(kc * NC + nc) * 32 + lane]);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const int col = nc * 8 + 2 * fc;
+                tA[(r0 + fr) * RS + col] = w[nc][0];
+                tA[(r0 + fr) * RS + col + 1] = w[nc][1];
+                if (rok) *reinterpret_cast<double2*>(a.Y + row * P + col) = make_double2(w[nc][0], w[nc][1]);
+            }
+        }
+        __syncwarp();
+        // V_k^T W over the tile (rows past n are zero in both tiles)
+#pragma unroll
+        for (int k0 = 0; k0 < TR; k0 += 4) {
+            const double* rv = tV + (k0 + fc) * RS;
+            const double* rw = tA + (k0 + fc) * RS;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const double av = rv[i * 8 + fr];
+#pragma unroll
+                for (int j = 0; j < NC; ++j) dmma(g[i][j][0], g[i][j][1], av, rw[j * 8 + fr]);
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+    // om: sum over the 8 row-lanes that share a column pair
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+        for (int nc = 0; nc < NC; ++nc) {
+            om[nc][0] += __shfl_xor_sync(FULL, om[nc][0], o);
+            om[nc][1] += __shfl_xor_sync(FULL, om[nc][1], o);
+        }
+    for (int w = 0; w < WARPS; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j < NC; ++j) frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
+            if (fr == 0) {
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    double* d = sAcc + P * P + nc * 8 + 2 * fc;
+                    d[0] = (w == 0 ? 0.0 : d[0]) + om[nc][0];
+                    d[1] = (w == 0 ? 0.0 : d[1]) + om[nc][1];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // totals of V_k^T W land in Gram2 (free until K2 of this block), then G = Tr_k^T (V_k^T W)
+    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->om2[a.par], &st->cnt1)) {
+        double* sGv = sScr;
+        double* sTk = sScr + P * P;
+        const double* Tk = st->Tr[a.sk];
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            sGv[t] = st->Gram2[(t / P) * MAXP + t % P];
+            sTk[t] = Tk[(t / P) * MAXP + t % P];
+        }
+        __syncthreads();
+        cta_matmul_tn<P>(sTk, P, sGv, P, st->G[a.par], MAXP);
+    }
+}
+
+}  // namespace bmr

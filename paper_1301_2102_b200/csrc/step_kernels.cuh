@@ -40,6 +40,7 @@ struct K1Args {
     double* part;
     int par;              // k mod 2
     int sk;               // k mod 3
+    int tpw;              // row groups (tiles of RPW rows) per warp, contiguous
 };
 
 template <int P>
@@ -48,7 +49,7 @@ constexpr int k1_min_blocks() { return P <= 8 ? 3 : 1; }
 template <int P>
 struct K1Smem {   // dynamic shared memory of the epilogue variant
     static constexpr size_t bytes =
-        sizeof(double) * (4 * P * P + (NT / 32) * 3 * PC<P>::RPW * P + P * P + P);
+        sizeof(double) * (4 * P * P + (NT / 32) * 3 * PC<P>::RPW * PC<P>::RS + P * P + P);
 };
 
 // C = A^T B for P x P row-major (leading dimensions lda/ldb/ldc), all threads of the CTA.
@@ -91,7 +92,8 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
     const int c0 = sub * VEC;
-    constexpr int SR = EPI ? RPW * P : 2;
+    constexpr int RS = C::RS;
+    constexpr int SR = EPI ? RPW * RS : 2;
     extern __shared__ __align__(16) double dyn1[];
     double* sTk = dyn1;                  // Tr_k
     double* sD = sTk + P * P;            // Tr_{k-1} C_{k-1}^T
@@ -166,9 +168,9 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
                 }
         }
         if constexpr (EPI) {
-            double* rA = sRow[warp][0] + rsub * P;
-            double* rU = sRow[warp][1] + rsub * P;
-            double* rP = sRow[warp][2] + rsub * P;
+            double* rA = sRow[warp][0] + rsub * RS;
+            double* rU = sRow[warp][1] + rsub * RS;
+            double* rP = sRow[warp][2] + rsub * RS;
             if (act) {
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) {
@@ -260,12 +262,18 @@ struct K2Args {
     double* part;
     int par;              // k mod 2
     int sk;               // k mod 3
+    int tpw;              // row groups per warp, contiguous
 };
+
+constexpr int NSTAGE = 4;   // cp.async pipeline depth of the streaming panel kernels
 
 template <int P>
 struct K2Smem {
     static constexpr int LD = P + 1;
-    static constexpr int loop = 2 * P * P + P * MAXQ + 2 * (NT / 32) * PC<P>::RPW * P + P * P + MAXQ * P;
+    static constexpr int TILE = PC<P>::RPW * PC<P>::RS;  // one row group of one panel (padded rows)
+    static constexpr int RQ = PC<P>::RPW * MAXQ;         // pool values of one row group
+    static constexpr int pipe = (NT / 32) * NSTAGE * (2 * TILE + RQ);
+    static constexpr int loop = 2 * P * P + P * MAXQ + pipe + P * P + MAXQ * P;
     static constexpr int tail = (3 * P * LD + 2 * P) > (P * P + P * MAXQ) ? (3 * P * LD + 2 * P) : (P * P + P * MAXQ);
     static constexpr size_t bytes = sizeof(double) * (loop + tail);
 };
@@ -283,12 +291,12 @@ __device__ bool k3a_factor(DevState* st, int par, int sk, double* scratch) {
     double* sOm = sD + P;
     __shared__ int s_bad;
     const int tid = threadIdx.x, lane = tid & 31;
-    for (int t = tid; t < P * P; t += NT) {
+    for (int t = tid; t < P * P; t += blockDim.x) {
         const int r = t / P, c = t % P;
         sA[r * LD + c] = st->Gram2[r * MAXP + c];
         sC[r * LD + c] = 0.0;
     }
-    for (int t = tid; t < P; t += NT) {
+    for (int t = tid; t < P; t += blockDim.x) {
         sD[t] = st->Gram2[t * MAXP + t];
         sOm[t] = st->om2[par][t];
     }
@@ -352,7 +360,7 @@ __device__ bool k3a_factor(DevState* st, int par, int sk, double* scratch) {
         return false;
     }
     double* Tn = st->Tr[(sk + 1) % 3];
-    for (int t = tid; t < P * P; t += NT) {
+    for (int t = tid; t < P * P; t += blockDim.x) {
         const int r = t / P, c = t % P;
         st->Ck[par][r * MAXP + c] = sC[r * LD + c];
         Tn[r * MAXP + c] = sCi[r * LD + c];
@@ -376,13 +384,14 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
     const int c0 = sub * VEC;
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
     const int E = P * P + Q * P;
+    using SM = K2Smem<P>;
+    constexpr int TILE = SM::TILE, RQ = SM::RQ;
     extern __shared__ __align__(16) double dyn2[];
     double* sE = dyn2;                 // Tr_k G_s
-    double* sTk = sE + P * P;          // Tr_k, then scratch
+    double* sTk = sE + P * P;          // Tr_k
     double* sF = sTk + P * P;          // Tr_k coef_{k-1} (P x MAXQ)
-    double(*sV)[RPW * P] = reinterpret_cast<double(*)[RPW * P]>(sF + P * MAXQ);
-    double(*sW)[RPW * P] = reinterpret_cast<double(*)[RPW * P]>(sF + P * MAXQ + WARPS * RPW * P);
-    double* sAcc = sF + P * MAXQ + 2 * WARPS * RPW * P;
+    double* sPipe = sF + P * MAXQ;     // per warp: NSTAGE x {W tile, V tile, pool values}
+    double* sAcc = sPipe + SM::pipe;
     double* sTail = sAcc + P * P + MAXQ * P;
     {
         // G_s: lower triangle of G mirrored (the paper computes h_{i,j} for i >= j)
@@ -415,33 +424,48 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
 #pragma unroll
         for (int q = 0; q < MAXQ; ++q) pq[q][v] = 0.0;
     }
-    const long long stride = (long long)gridDim.x * WARPS * RPW;
-    for (long long base = ((long long)blockIdx.x * WARPS + warp) * RPW; base < a.n; base += stride) {
-        const long long i = base + rsub;
-        const bool valid = act && i < a.n;
-        double w[VEC], u[VEC], r[MAXQ];
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) w[v] = u[v] = 0.0;
-#pragma unroll
-        for (int q = 0; q < MAXQ; ++q) r[q] = 0.0;
-        if (valid) {
-            ldc<VEC>(a.W + i * P + c0, w);
-            ldv<VEC>(a.V + i * P + c0, u);
-#pragma unroll
-            for (int q = 0; q < MAXQ; ++q)
-                if (q < Q) r[q] = a.pool[i * qc + qf + q];
+    // NSTAGE-deep cp.async pipeline over this warp's row groups (grid-strided)
+    constexpr int RS = C::RS;
+    double* wb = sPipe + warp * NSTAGE * (2 * TILE + RQ);
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    const long long ntiles = (a.n + RPW - 1) / RPW;
+    auto issue = [&](long long it, int slot) {
+        const long long t = t0 + it * ts;
+        const long long i = t * RPW + rsub;
+        const bool ok = act && t < ntiles && i < a.n;
+        const long long ic = ok ? i : 0;
+        double* sl = wb + slot * (2 * TILE + RQ);
+        if (act) {   // idle lanes (p/VEC not a power of two) must not touch the next row's slots
+            cp_async_vec<VEC>(sl + rsub * RS + c0, a.W + ic * P + c0, ok);
+            cp_async_vec<VEC>(sl + TILE + rsub * RS + c0, a.V + ic * P + c0, ok);
+            if (sub == 0)
+                for (int q = 0; q < Q; ++q) cp_async8(sl + 2 * TILE + rsub * MAXQ + q, a.pool + ic * qc + qf + q, ok);
         }
-        if (act) {
+        cp_commit();
+    };
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) sV[warp][rsub * P + c0 + v] = u[v];
-        }
+    for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
+        cp_wait<NSTAGE - 1>();
         __syncwarp();
+        double* sl = wb + (int)(it % NSTAGE) * (2 * TILE + RQ);
+        double* tw = sl + rsub * RS;
+        const double* tv = sl + TILE + rsub * RS;
+        const double* tr = sl + 2 * TILE + rsub * MAXQ;
+        const long long i = (t0 + it * ts) * RPW + rsub;
+        const bool valid = act && i < a.n;
+        double w[VEC], r[MAXQ];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) w[v] = tw[c0 + v];
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) r[q] = (q < Q) ? tr[q] : 0.0;
         if (valid) {
             // pool r_q -= U_k coef_{k-1}(:,q) = V_k F(:,q)   (orthogonal to the newest block)
             if (Q > 0) {
 #pragma unroll
                 for (int b = 0; b < P; ++b) {
-                    const double x = sV[warp][rsub * P + b];
+                    const double x = tv[b];
 #pragma unroll
                     for (int q = 0; q < MAXQ; ++q)
                         if (q < Q) r[q] = fma(-x, sF[b * MAXQ + q], r[q]);
@@ -455,21 +479,22 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
             // W' = W - U_k G_s = W - V_k (Tr_k G_s)
 #pragma unroll
             for (int b = 0; b < P; ++b) {
-                const double x = sV[warp][rsub * P + b];
+                const double x = tv[b];
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) w[v] = fma(-x, sE[b * P + c0 + v], w[v]);
             }
             stv<VEC>(a.W + i * P + c0, w);
         }
+        __syncwarp();
         if (act) {
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) sW[warp][rsub * P + c0 + v] = valid ? w[v] : 0.0;
+            for (int v = 0; v < VEC; ++v) tw[c0 + v] = valid ? w[v] : 0.0;
         }
         __syncwarp();
         if (valid) {
 #pragma unroll
             for (int b = 0; b < P; ++b) {
-                const double x = sW[warp][rsub * P + b];
+                const double x = tw[b];
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) g[b][v] = fma(x, w[v], g[b][v]);
             }
@@ -483,6 +508,7 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
         }
         __syncwarp();
     }
+    cp_wait<0>();
 #pragma unroll
     for (int o = LP; o < 32; o <<= 1) {
 #pragma unroll
@@ -785,18 +811,21 @@ struct K4bArgs {
     long long n;
     DevState* st;
     int sk;               // k mod 3
+    int tpw;              // row groups per warp, contiguous
 };
 
 template <int P>
 struct K4bSmem {
-    static constexpr size_t bytes = sizeof(double) * (4 * P * P + (NT / 32) * 2 * 3 * PC<P>::RPW * P);
+    static constexpr int TILE = PC<P>::RPW * PC<P>::RS;
+    static constexpr int pipe = (NT / 32) * NSTAGE * 4 * TILE;   // V, M_{k-2}, M_{k-1}, X tiles
+    static constexpr size_t bytes = sizeof(double) * (4 * P * P + pipe);
 };
 
 template <int P>
 __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
     using C = PC<P>;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW, WARPS = NT / 32;
-    constexpr int RG = 2;
+    constexpr int TILE = K4bSmem<P>::TILE;
     DevState* st = a.st;
     if (!st->side_go) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -808,7 +837,7 @@ __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
     double* sB1 = sAi + P * P;
     double* sB2 = sB1 + P * P;
     double* sZ = sB2 + P * P;
-    double(*sRow)[RG][3][RPW * P] = reinterpret_cast<double(*)[RG][3][RPW * P]>(sZ + P * P);
+    double* sPipe = sZ + P * P;
     {
         // sAi = Tr_k R_kk^{-1} (built in sZ's space first)
         double* sT = sAi;
@@ -832,80 +861,75 @@ __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
         for (int t = threadIdx.x; t < P * P; t += NT) sZ[t] = st->Z[(t / P) * MAXP + t % P];
         __syncthreads();
     }
-    const long long stride = (long long)gridDim.x * WARPS * RPW * RG;
-    for (long long base = ((long long)blockIdx.x * WARPS + warp) * RPW * RG; base < a.n; base += stride) {
-        double u[RG][VEC], m2[RG][VEC], m1[RG][VEC], x[RG][VEC];
-        bool valid[RG];
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            const long long i = base + g * RPW + rsub;
-            valid[g] = act && i < a.n;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) u[g][v] = m2[g][v] = m1[g][v] = x[g][v] = 0.0;
-            if (valid[g]) {
-                ldv<VEC>(a.U + i * P + c0, u[g]);
-                ldc<VEC>(a.M2 + i * P + c0, m2[g]);
-                ldc<VEC>(a.M1 + i * P + c0, m1[g]);
-                ldc<VEC>(a.X + i * P + c0, x[g]);
-            }
+    constexpr int RS = C::RS;
+    double* wb = sPipe + warp * NSTAGE * 4 * TILE;
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    const long long ntiles = (a.n + RPW - 1) / RPW;
+    auto issue = [&](long long it, int slot) {
+        const long long t = t0 + it * ts;
+        const long long i = t * RPW + rsub;
+        const bool ok = act && t < ntiles && i < a.n;
+        const long long ic = (ok ? i : 0) * P + c0;
+        double* sl = wb + slot * 4 * TILE + rsub * RS + c0;
+        if (act) {   // idle lanes must not touch the next row's slots
+            cp_async_vec<VEC>(sl, a.U + ic, ok);
+            cp_async_vec<VEC>(sl + TILE, a.M2 + ic, ok);
+            cp_async_vec<VEC>(sl + 2 * TILE, a.M1 + ic, ok);
+            cp_async_vec<VEC>(sl + 3 * TILE, a.X + ic, ok);
         }
+        cp_commit();
+    };
 #pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            if (act) {
+    for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
+        cp_wait<NSTAGE - 1>();
+        __syncwarp();
+        double* sl = wb + (int)(it % NSTAGE) * 4 * TILE + rsub * RS;
+        const double* tv = sl;
+        double* tm2 = sl + TILE;
+        const double* tm1 = sl + 2 * TILE;
+        const double* tx = sl + 3 * TILE;
+        const long long i = (t0 + it * ts) * RPW + rsub;
+        const bool valid = act && i < a.n;
+        // M_k = U_k R_kk^{-1} - M_{k-2} B2 - M_{k-1} B1   (eqn.search-dir-comp)
+        double mk[VEC];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) {
-                    sRow[warp][g][0][rsub * P + c0 + v] = u[g][v];
-                    sRow[warp][g][1][rsub * P + c0 + v] = m2[g][v];
-                    sRow[warp][g][2][rsub * P + c0 + v] = m1[g][v];
-                }
+        for (int v = 0; v < VEC; ++v) mk[v] = 0.0;
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+            const double xu = tv[b], x2 = tm2[b], x1 = tm1[b];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                const int m = c0 + v;
+                mk[v] = fma(xu, sAi[b * P + m], mk[v]);
+                mk[v] = fma(-x2, sB2[b * P + m], mk[v]);
+                mk[v] = fma(-x1, sB1[b * P + m], mk[v]);
             }
         }
         __syncwarp();
-        double mk[RG][VEC];
+        if (act) {
 #pragma unroll
-        for (int g = 0; g < RG; ++g) {
+            for (int v = 0; v < VEC; ++v) tm2[c0 + v] = mk[v];
+        }
+        if (valid) stv<VEC>(a.M2 + i * P + c0, mk);
+        __syncwarp();
+        if (valid) {
+            // X += M_k Z_k   (eqn.approx-update)
+            double x[VEC];
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) mk[g][v] = 0.0;
+            for (int v = 0; v < VEC; ++v) x[v] = tx[c0 + v];
 #pragma unroll
             for (int b = 0; b < P; ++b) {
-                const double xu = sRow[warp][g][0][rsub * P + b];
-                const double x2 = sRow[warp][g][1][rsub * P + b];
-                const double x1 = sRow[warp][g][2][rsub * P + b];
+                const double xm = tm2[b];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) {
-                    const int m = c0 + v;
-                    mk[g][v] = fma(xu, sAi[b * P + m], mk[g][v]);
-                    mk[g][v] = fma(-x2, sB2[b * P + m], mk[g][v]);
-                    mk[g][v] = fma(-x1, sB1[b * P + m], mk[g][v]);
-                }
+                for (int v = 0; v < VEC; ++v) x[v] = fma(xm, sZ[b * P + c0 + v], x[v]);
             }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            const long long i = base + g * RPW + rsub;
-            if (valid[g]) stv<VEC>(a.M2 + i * P + c0, mk[g]);
-            if (act) {
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) sRow[warp][g][0][rsub * P + c0 + v] = mk[g][v];
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-            const long long i = base + g * RPW + rsub;
-            if (valid[g]) {
-#pragma unroll
-                for (int b = 0; b < P; ++b) {
-                    const double xm = sRow[warp][g][0][rsub * P + b];
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) x[g][v] = fma(xm, sZ[b * P + c0 + v], x[g][v]);
-                }
-                stv<VEC>(a.X + i * P + c0, x[g]);
-            }
+            stv<VEC>(a.X + i * P + c0, x);
         }
         __syncwarp();
     }
+    cp_wait<0>();
 }
 
 }  // namespace bmr
