@@ -118,6 +118,8 @@ struct bminres_ctx {
     double* pool = nullptr;
     double* part = nullptr;
     size_t part_elems = 0;
+    double* part1 = nullptr;
+    double* part2[2] = {nullptr, nullptr};
     double* dsc = nullptr;        // scratch for dot results (MAXREF+8)
     unsigned* dcnt = nullptr;     // tickets of the generic kernels
     DevState* st = nullptr;
@@ -291,8 +293,13 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         h->scr[s] = nullptr;
     }
     dalloc(h, &h->pool, (size_t)n * std::max(q, 1));
+    // generic-kernel partials, then K1 partials (ncl1 x (p*p+p)) and K2 partials x 2 parities
     h->part_elems = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8);
-    if (!h->part) CK(cudaMalloc((void**)&h->part, h->part_elems * sizeof(double)));
+    const size_t e1 = (size_t)NB_MAX * (MAXP * MAXP + MAXP), e2 = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP);
+    if (!h->part) CK(cudaMalloc((void**)&h->part, (h->part_elems + e1 + 2 * e2) * sizeof(double)));
+    h->part1 = h->part + h->part_elems;
+    h->part2[0] = h->part1 + e1;
+    h->part2[1] = h->part2[0] + e2;
     if (!h->dsc) CK(cudaMalloc((void**)&h->dsc, (MAXREF + 64) * sizeof(double)));
     if (!h->dcnt) {
         CK(cudaMalloc((void**)&h->dcnt, 16 * sizeof(unsigned)));
@@ -409,6 +416,12 @@ struct StepPtrs {
 
 // main branch of block k: gathers V_k (slot k%3), reads V_{k-1} (slot (k-1)%3), writes W and
 // then W' into slot (k+1)%3 (= V_{k+1}); parity k%2 selects the double-buffered small state
+void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
+    const int P = h->p_ws;
+    const int Emax = P * P + (which == 1 ? P : MAXQ * P);
+    k_reduce<<<(Emax + 7) / 8, 256, 0, s>>>(h->st, which, (int)(k & 1), P);
+    check_launch(h, "k_reduce");
+}
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k) {
     TimeMark tm(h, PH_SPMM);
     const int sk = (int)(k % 3), par = (int)(k & 1);
@@ -418,6 +431,7 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
     h->stream = s;
     launch_cluster(h, h->kf.k1, h->nb1, h->kf.nt1, h->kf.smem1, a, "k1_spmm");
     h->stream = keep;
+    launch_reduce(h, s, 1, k);
 }
 void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k) {
     TimeMark tm(h, PH_ORTH);
@@ -428,6 +442,7 @@ void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k) {
     h->stream = s;
     launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
     h->stream = keep;
+    launch_reduce(h, s, 2, k);
 }
 // side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
 void launch_k3b(bminres_ctx* h, cudaStream_t s) {
@@ -614,6 +629,7 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
     SET_STATE(h, q_live, q_live);
     SET_STATE(h, stop_after, stop_after);
     SET_STATE(h, need_slow, 0);
+    SET_STATE(h, given_blk, b);
     SET_STATE(h, bd_at, KINF);
     SET_STATE(h, run_main, 1);
     SET_STATE(h, k_main, b + 1);
@@ -752,6 +768,12 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     init.tau = tau;
     init.hist = hist_cap ? h->hist : nullptr;
     init.hflags = h->hf_dev;
+    init.part1 = h->part1;
+    init.part2[0] = h->part2[0];
+    init.part2[1] = h->part2[1];
+    init.ncl1 = h->nb1 / h->csz;
+    init.ncl2 = h->nb2 / h->csz;
+    init.given_blk = -1;
     for (int t = 0; t < 3; ++t)
         for (int c = 0; c < MAXP; ++c) init.Tr[t][c * MAXP + c] = 1.0;
     std::vector<double> S(MAXP * MAXP, 0.0), beta(p, 0.0), f0n(p, 0.0);
@@ -883,34 +905,38 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     long long b = 1;          // next block of the side branch
     bool main_ahead = false;  // K1, K2 of block b already done (V_{b+1} ready)
     while (!h->hf->side_done) {
-        const bool expl = !graphs || retained_live(h, (b - 1) * p + 1);
-        if (expl || !main_ahead) {
-            if (!main_ahead) {
-                launch_k1(h, h->stream, sp, n, b);
-                launch_k2(h, h->stream, n, b);
-                CK(cudaStreamSynchronize(h->stream));
-            }
-            if (h->hf->need_slow || retained_live(h, (b - 1) * p + 1)) {
+        const bool ret = retained_live(h, (b - 1) * p + 1);
+        const bool expl = !graphs || ret;
+        if (!main_ahead) {
+            launch_k1(h, h->stream, sp, n, b);
+            launch_k2(h, h->stream, n, b);
+            main_ahead = true;
+        }
+        if (ret) {   // candidates of block b meet a live retained vector: column path
+            CK(cudaStreamSynchronize(h->stream));
+            slow_block(h, n, p, b, tau, maxit);
+            finish_given_block(h, sp, n, b);
+            b++;
+            main_ahead = false;
+            continue;
+        }
+        if (expl) {
+            launch_k3b(h, h->stream);
+            launch_k4b(h, h->stream, sp, n, b);
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->hf->need_slow) {   // K3b found a breakdown in block b
                 slow_block(h, n, p, b, tau, maxit);
                 finish_given_block(h, sp, n, b);
-                b++;
-                main_ahead = false;
-                continue;
             }
-            if (expl) {
-                launch_k3b(h, h->stream);
-                launch_k4b(h, h->stream, sp, n, b);
-                b++;
-                main_ahead = false;
-                continue;
-            }
-            main_ahead = true;
+            b++;
+            main_ahead = false;
+            continue;
         }
         // pipelined graphs: side block s with main block s+1
         long long launched = 0;
         for (long long s = b; s <= nblocks; ++s) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
-            h->launches += 4;
+            h->launches += 6;
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -922,7 +948,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         if (h->hf->side_done) break;
         b = GET_STATE(h, k_side);
         if (h->hf->need_slow) {
-            // main stopped at block bd_at == b after K2; the side finished block b-1
+            // breakdown of block bd_at == b (found by K1(b+1) and K3b(b)); the side finished b-1
             slow_block(h, n, p, b, tau, maxit);
             finish_given_block(h, sp, n, b);
             b++;

@@ -61,8 +61,9 @@ struct HostFlags {
 struct DevState {
     // ---- main branch (K1, K2, K4a)
     int run_main;       // main-branch kernels run
-    int need_slow;      // K2: breakdown or Cholesky cancellation at block bd_at
-    int pad_m;
+    int need_slow;      // breakdown or Cholesky cancellation at block bd_at (K1 or K3b)
+    int ncl1, ncl2;     // cluster partials written by K1 / K2
+    long long given_blk;   // block whose C_k, Tr_{k+1}, coef_k the host supplied (column path)
     int q_first;        // first live pool vector
     int q_live;         // number of live pool vectors
     int pool_cap;       // pool panel row stride
@@ -101,6 +102,10 @@ struct DevState {
     double res[MAXP];              // latest computed relative residuals
     double* hist;                  // (hist_cap) x p computed relative residuals, or null
     HostFlags* hflags;             // device alias of the mapped host flags
+    double* part1;                 // K1 cluster partials: ncl1 x (p*p + p)
+    double* part2[2];              // K2 cluster partials by block parity: ncl2 x (p*p + q*p)
+    double red1[MAXP * MAXP + MAXP];            // totals of part1: V_k^T W (p*p), ||A u_j||^2 (p)
+    double red2[2][MAXP * MAXP + MAXQ * MAXP];  // totals of part2 by parity: W'^T W' (p*p), r_q^T W'
 };
 
 // ------------------------------------------------------------------ small helpers
@@ -168,37 +173,48 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
-// Cluster reduction.  Every CTA of a reducing panel kernel ends with its sums in shared
-// memory sAcc[E].  The CTAs of a thread-block cluster are combined through distributed
-// shared memory by the cluster's rank-0 CTA (fixed rank order), which writes one partial
-// per cluster; the last cluster leader to arrive sums the per-cluster partials in fixed
-// order into outA (entries e < P*P, at [(e/P)*MAXP + e%P]) and outB (the rest, at
-// [((e-P*P)/P)*MAXP + (e-P*P)%P]).  Returns true in the CTA that produced the totals.
-// Deterministic: no floating-point atomics.
-__device__ __forceinline__ bool cluster_reduce(double* sAcc, int E, int P, double* part, double* outA,
-                                               double* outB, unsigned* cnt) {
+// Cluster partials.  Every CTA of a reducing panel kernel ends with its sums in shared memory
+// sAcc[E].  The CTAs of a thread-block cluster are combined through distributed shared memory
+// by the cluster's rank-0 CTA (fixed rank order), which writes one partial row
+// part[cluster_id*E .. +E).  There is no last-CTA step: every CTA of the consuming kernel
+// sums the rows itself (reduce_partials), so no serial tail sits on the critical path.
+__device__ __forceinline__ void cluster_partials(const double* sAcc, int E, double* part) {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
-    const unsigned rank = cl.block_rank();
     const int csz = (int)cl.num_blocks();
-    const int ncl = gridDim.x / csz, cid = blockIdx.x / csz;
-    if (rank == 0) {
+    if (cl.block_rank() == 0) {
+        const int cid = blockIdx.x / csz;
         for (int e = threadIdx.x; e < E; e += blockDim.x) {
             double s = 0.0;
             for (int r = 0; r < csz; ++r) s += cl.map_shared_rank(sAcc, r)[e];
-            part[(size_t)cid * E + e] = s;   // partial-major: the final sum reads coalesced rows
+            part[(size_t)cid * E + e] = s;
         }
     }
     cl.sync();  // remote shared memory must outlive the leader's reads
-    if (rank != 0) return false;
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1u) == (unsigned)ncl - 1);
-    __syncthreads();
-    if (!s_last) return false;
-    __threadfence();
-    // one thread per entry; 8 independent accumulators (fixed order), loads coalesced across threads
+}
+
+// The totals of one set of cluster partials: one warp per entry, lanes stride over the partial
+// rows, a fixed shuffle tree -> deterministic.  which = 1: part1 -> red1; which = 2: part2[par]
+// -> red2[par].  Entry counts come from the state (q_live may change between launches).
+__global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par, int P) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int e = blockIdx.x * 8 + warp;
+    const bool main_stopped = !st->run_main;
+    if (main_stopped) return;
+    const int E = which == 1 ? P * P + P : P * P + st->q_live * P;
+    const int ncl = which == 1 ? st->ncl1 : st->ncl2;
+    const double* part = which == 1 ? st->part1 : st->part2[par];
+    double* out = which == 1 ? st->red1 : st->red2[par];
+    if (e >= E) return;
+    double s = 0.0;
+    for (int b = lane; b < ncl; b += 32) s += __ldcg(part + (size_t)b * E + e);
+    s = warp_sum(s);
+    if (lane == 0) out[e] = s;
+}
+
+// out[e] = sum over the ncl partial rows (fixed order, 8 interleaved accumulators; loads are
+// coalesced across threads).  Identical in every CTA that calls it (deterministic).
+__device__ __forceinline__ void reduce_partials(const double* part, int ncl, int E, double* out) {
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
         double acc[8];
 #pragma unroll
@@ -209,15 +225,179 @@ __device__ __forceinline__ bool cluster_reduce(double* sAcc, int E, int P, doubl
             for (int u = 0; u < 8; ++u) acc[u] += __ldcg(part + (size_t)(b + u) * E + e);
         }
         for (; b < ncl; ++b) acc[0] += __ldcg(part + (size_t)b * E + e);
-        const double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-        if (e < P * P)
-            outA[(e / P) * MAXP + e % P] = s;
-        else
-            outB[((e - P * P) / P) * MAXP + (e - P * P) % P] = s;
+        out[e] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
-    if (threadIdx.x == 0) *cnt = 0u;
+}
+
+// Cholesky W'^T W' = C^T C of the new block (right-looking, warp 0), the breakdown /
+// cancellation test (h_{j+p,j}^2 = pivot <= tau^2 ||A u_j||^2; pivot < 1e-4 of
+// ||w'_m||^2 -> column path, R2), C^{-1} and the pool coefficients
+// coef(:,q) = C^{-T} (W'^T r_q) = U_{k+1}^T r_q.  Inputs in shared memory: sG (Gram, ld P,
+// destroyed), sOm (p), sPd (q x p).  Outputs: sC (ld P), sCi (ld P), sCo (P x MAXQ).
+// Returns true on breakdown.  Identical in every CTA that calls it.  All threads call it.
+template <int P>
+__device__ bool factor_block(double* sG, const double* sOm, const double* sPd, int Q, double tau, double* sC,
+                             double* sCi, double* sCo) {
+    __shared__ int s_bad;
+    __shared__ double sD[P];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int t = tid; t < P * P; t += blockDim.x) {
+        sC[t] = 0.0;
+        sCi[t] = 0.0;
+    }
+    for (int t = tid; t < P; t += blockDim.x) sD[t] = sG[t * P + t];
+    for (int t = tid; t < P * MAXQ; t += blockDim.x) sCo[t] = 0.0;
+    __syncthreads();
+    if (tid < 32) {
+        bool bad = false;
+        for (int m = 0; m < P; ++m) {
+            const double d = sG[m * P + m];
+            if (!(d > tau * tau * sOm[m]) || !(d >= 1e-4 * sD[m])) {
+                bad = true;
+                break;
+            }
+            const double cmm = sqrt(d);
+            const double rc = 1.0 / cmm;
+            for (int c = m + lane; c < P; c += 32) sC[m * P + c] = (c == m) ? cmm : sG[m * P + c] * rc;
+            __syncwarp();
+            for (int t = lane; t < P * P; t += 32) {
+                const int r = t / P, c = t % P;
+                if (r > m && c >= r) sG[r * P + c] = fma(-sC[m * P + r], sC[m * P + c], sG[r * P + c]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_bad = bad;
+        if (!bad && lane < P) {
+            const int l = lane;
+            for (int r = P - 1; r >= 0; --r) {
+                double s = (r == l) ? 1.0 : 0.0;
+                for (int c = r + 1; c <= l; ++c) s = fma(-sC[r * P + c], sCi[c * P + l], s);
+                sCi[r * P + l] = (r <= l) ? s / sC[r * P + r] : 0.0;
+            }
+        }
+        if (!bad && lane < Q) {
+            double y[P];
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                double s = sPd[lane * P + m];
+#pragma unroll
+                for (int i = 0; i < m; ++i) s = fma(-sC[i * P + m], y[i], s);
+                y[m] = s / sC[m * P + m];
+                sCo[m * MAXQ + lane] = y[m];
+            }
+        }
+    }
+    __syncthreads();
+    return s_bad != 0;
+}
+
+// Publish a breakdown of block b (main branch stops; the host runs the column path).
+__device__ __forceinline__ void publish_breakdown(DevState* st, long long b) {
+    st->need_slow = 1;
+    st->run_main = 0;
+    st->bd_at = b;
+    st->hflags->bd_at = b;
+    st->hflags->need_slow = 1;
+    __threadfence_system();
+}
+
+// C = A B (transB: C = A B^T) for P x P row-major in shared memory, all threads of the CTA.
+template <int P>
+__device__ __forceinline__ void smm_nn(const double* Am, const double* Bm, double* Cm, bool transB = false) {
+    for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+        const int r = t / P, c = t % P;
+        double s = 0.0;
+        for (int i = 0; i < P; ++i) s = fma(Am[r * P + i], transB ? Bm[c * P + i] : Bm[i * P + c], s);
+        Cm[r * P + c] = s;
+    }
+}
+// C = A^T B
+template <int P>
+__device__ __forceinline__ void smm_tn(const double* Am, const double* Bm, double* Cm) {
+    for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+        const int r = t / P, c = t % P;
+        double s = 0.0;
+        for (int i = 0; i < P; ++i) s = fma(Am[i * P + r], Bm[i * P + c], s);
+        Cm[r * P + c] = s;
+    }
+}
+// shared <- global P x P block with leading dimension MAXP
+template <int P>
+__device__ __forceinline__ void load_pp(double* dst, const double* src) {
+    for (int t = threadIdx.x; t < P * P; t += blockDim.x) dst[t] = src[(t / P) * MAXP + t % P];
+}
+template <int P>
+__device__ __forceinline__ void store_pp(double* dst, const double* src) {
+    for (int t = threadIdx.x; t < P * P; t += blockDim.x) dst[(t / P) * MAXP + t % P] = src[t];
+}
+
+// Scratch (doubles) the K1 / K2 prologues need.
+template <int P>
+constexpr int prologue_scratch() { return (P * P + MAXQ * P) + 6 * P * P + P * MAXQ + P; }
+
+// K1 prologue, block k: C_{k-1}, Tr_k = C_{k-1}^{-1}, coef_{k-1} from K2(k-1)'s partials (or the
+// host's values after the column path), and D = Tr_{k-1} C_{k-1}^T.  Writes sTk and sD (P x P,
+// ld P).  Returns false when the CTA must exit (breakdown of block k-1, published by CTA 0).
+template <int P>
+__device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* sD, double* scr) {
+    const long long k = st->k_main;
+    if (k <= 1) {
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            sTk[t] = (t / P == t % P) ? 1.0 : 0.0;
+            sD[t] = 0.0;
+        }
+        __syncthreads();
+        return true;
+    }
+    double* sRed = scr;                          // Gram (P*P) + pool dots (MAXQ*P)
+    double* sC = sRed + P * P + MAXQ * P;
+    double* sCi = sC + P * P;
+    double* sTp = sCi + P * P;
+    double* sCo = sTp + P * P;
+    double* sOm = sCo + P * MAXQ;
+    const int pp = par ^ 1;                      // parity of block k-1
+    if (st->given_blk == k - 1) {
+        load_pp<P>(sC, st->Ck[pp]);
+        load_pp<P>(sTk, st->Tr[sk]);
+    } else {
+        const int Q = st->q_live;
+        for (int t = threadIdx.x; t < P * P + Q * P; t += blockDim.x) sRed[t] = st->red2[pp][t];
+        for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[pp][t];
+        __syncthreads();
+        if (factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) publish_breakdown(st, k - 1);
+            return false;
+        }
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) sTk[t] = sCi[t];
+        if (blockIdx.x == 0) {
+            store_pp<P>(st->Ck[pp], sC);
+            store_pp<P>(st->Tr[sk], sCi);
+            for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[pp][t] = sCo[t];
+        }
+    }
+    load_pp<P>(sTp, st->Tr[(sk + 2) % 3]);       // Tr_{k-1}
+    __syncthreads();
+    smm_nn<P>(sTp, sC, sD, true);                // D = Tr_{k-1} C_{k-1}^T
     __syncthreads();
     return true;
 }
+
+// K2 prologue, block k: G = Tr_k^T (V_k^T W) from K1's partials, om2; CTA 0 publishes G, om2 for
+// the side branch and the column path.  Writes sG (P x P, ld P, G itself) and sTk (Tr_k).
+template <int P>
+__device__ void k2_prologue(DevState* st, int par, int sk, double* sG, double* sTk, double* scr) {
+    double* sRed = scr;   // P*P + P
+    for (int t = threadIdx.x; t < P * P + P; t += blockDim.x) sRed[t] = st->red1[t];
+    load_pp<P>(sTk, st->Tr[sk]);
+    __syncthreads();
+    smm_tn<P>(sTk, sRed, sG);
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        store_pp<P>(st->G[par], sG);
+        for (int t = threadIdx.x; t < P; t += blockDim.x) st->om2[par][t] = sRed[P * P + t];
+        if (threadIdx.x == 0) st->k_main = st->k_main + 1;
+    }
+}
+
 
 }  // namespace bmr

@@ -185,7 +185,7 @@ struct K2DSmem {
     static constexpr int TQ = DM<P>::TR * RSQ;
     static constexpr int pipe = WARPS * NSTAGE * (2 * DM<P>::TILE + TQ);
     static constexpr int LD = P + 1;
-    static constexpr int tail = (3 * P * LD + 2 * P) > (3 * P * P) ? (3 * P * LD + 2 * P) : (3 * P * P);
+    static constexpr int tail = 4 * P * P + prologue_scratch<P>();
     static constexpr size_t bytes = sizeof(double) * (DM<P>::FR + DM<P>::KC * 32 + pipe + P * P + MAXQ * P + tail);
 };
 
@@ -207,17 +207,17 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
     double* sAcc = pipe + S::pipe;
     double* sTail = sAcc + P * P + MAXQ * P;
     {
-        // G_s: lower triangle of G mirrored (the paper computes h_{i,j} for i >= j)
+        // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
+        // computes h_{i,j} for i >= j)
         double* sGs = sTail;
         double* sTk = sTail + P * P;
         double* sX = sTail + 2 * P * P;
-        const double* Gp = st->G[a.par];
-        const double* Tk = st->Tr[a.sk];
+        double* sG = sTail + 3 * P * P;
+        k2_prologue<P>(st, a.par, a.sk, sG, sTk, sTail + 4 * P * P);
         const double* Co = st->coef[a.par ^ 1];
         for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
             const int r = t / P, c = t % P;
-            sGs[t] = r >= c ? Gp[r * MAXP + c] : Gp[c * MAXP + r];
-            sTk[t] = Tk[r * MAXP + c];
+            sGs[t] = r >= c ? sG[r * P + c] : sG[c * P + r];
         }
         __syncthreads();
         cta_matmul_nn<P>(sTk, P, sGs, P, sX, P);
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
         }
         __syncthreads();
     }
-    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->pdot, &st->cnt2)) k3a_factor<P>(st, a.par, a.sk, sTail);
+    cluster_partials(sAcc, E, st->part2[a.par]);   // K1(k+1) and K3b(k) factor W' from these
 }
 
 
@@ -356,7 +356,8 @@ template <int P>
 struct K1DSmem {
     static constexpr int WARPS = 8;
     static constexpr int pipe = WARPS * (K1STAGE * 2 + 1) * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile
-    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + pipe + P * P + P + 3 * P * P);
+    static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
+    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + (pipe > scr ? pipe : scr) + P * P + P);
 };
 
 // W = (A V_k) Tr_k - V_{k-1} (Tr_{k-1} C_{k-1}^T); ||A u_j||^2; V_k^T W.  The gathers of the SpMM
@@ -381,26 +382,16 @@ __global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
     double* fT = dynd1;            // Tr_k
     double* fD = fT + FR;          // -(Tr_{k-1} C_{k-1}^T)
     double* pipe = fD + FR;
-    double* sAcc = pipe + K1DSmem<P>::pipe;
-    double* sScr = sAcc + P * P + P;
+    constexpr int PIPE = K1DSmem<P>::pipe > K1DSmem<P>::scr ? K1DSmem<P>::pipe : K1DSmem<P>::scr;
+    double* sAcc = pipe + PIPE;
     const bool has_prev = st->k_main > 1;
     {
-        double* sTp = sScr;
-        double* sCp = sScr + P * P;
-        double* sX = sScr + 2 * P * P;
-        const double* Tk = st->Tr[a.sk];
-        const double* Tp = st->Tr[(a.sk + 2) % 3];
-        const double* Cp = st->Ck[a.par ^ 1];   // C_{k-1}
-        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
-            const int g = (t / P) * MAXP + t % P;
-            sTp[t] = Tp[g];
-            sCp[t] = Cp[g];
-        }
-        to_frag<P>(Tk, MAXP, 1.0, fT);
-        __syncthreads();
-        cta_matmul_nn<P>(sTp, P, sCp, P, sX, P, true);   // D = Tr_{k-1} C_{k-1}^T
-        __syncthreads();
-        to_frag<P>(sX, P, -1.0, fD);
+        // C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D (pipeline area as scratch)
+        double* sTk = pipe;
+        double* sD = pipe + P * P;
+        if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, pipe + 2 * P * P)) return;
+        to_frag<P>(sTk, P, 1.0, fT);
+        to_frag<P>(sD, P, -1.0, fD);
         __syncthreads();
     }
     double g[NC][NC][2], om[NC][2];
@@ -550,18 +541,7 @@ __global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
         }
         __syncthreads();
     }
-    // totals of V_k^T W land in Gram2 (free until K2 of this block), then G = Tr_k^T (V_k^T W)
-    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->om2[a.par], &st->cnt1)) {
-        double* sGv = sScr;
-        double* sTk = sScr + P * P;
-        const double* Tk = st->Tr[a.sk];
-        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
-            sGv[t] = st->Gram2[(t / P) * MAXP + t % P];
-            sTk[t] = Tk[(t / P) * MAXP + t % P];
-        }
-        __syncthreads();
-        cta_matmul_tn<P>(sTk, P, sGv, P, st->G[a.par], MAXP);
-    }
+    cluster_partials(sAcc, E, st->part1);   // K2 forms G = Tr_k^T (V_k^T W) from these
 }
 
 }  // namespace bmr

@@ -49,7 +49,7 @@ constexpr int k1_min_blocks() { return P <= 8 ? 3 : 1; }
 template <int P>
 struct K1Smem {   // dynamic shared memory of the epilogue variant
     static constexpr size_t bytes =
-        sizeof(double) * (4 * P * P + (NT / 32) * 3 * PC<P>::RPW * PC<P>::RS + P * P + P);
+        sizeof(double) * (2 * P * P + (NT / 32) * 3 * PC<P>::RPW * PC<P>::RS + P * P + P + prologue_scratch<P>());
 };
 
 // C = A^T B for P x P row-major (leading dimensions lda/ldb/ldc), all threads of the CTA.
@@ -97,25 +97,13 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
     extern __shared__ __align__(16) double dyn1[];
     double* sTk = dyn1;                  // Tr_k
     double* sD = sTk + P * P;            // Tr_{k-1} C_{k-1}^T
-    double* sTp = sD + P * P;            // scratch: Tr_{k-1}, later the V_k^T W totals
-    double* sCp = sTp + P * P;           // scratch: C_{k-1}
-    double(*sRow)[3][SR] = reinterpret_cast<double(*)[3][SR]>(sCp + P * P);   // A V_k, V_k, V_{k-1} rows
-    double* sAcc = sCp + P * P + WARPS * 3 * SR;
+    double(*sRow)[3][SR] = reinterpret_cast<double(*)[3][SR]>(sD + P * P);   // A V_k, V_k, V_{k-1} rows
+    double* sAcc = sD + P * P + WARPS * 3 * SR;
+    double* sScr = sAcc + (EPI ? E : 1);
     bool has_prev = false;
     if constexpr (EPI) {
         has_prev = st->k_main > 1;
-        const double* Tk = st->Tr[a.sk];
-        const double* Tp = st->Tr[(a.sk + 2) % 3];
-        const double* Cp = st->Ck[a.par ^ 1];   // C_{k-1}
-        for (int t = threadIdx.x; t < P * P; t += NT) {
-            const int g = (t / P) * MAXP + t % P;
-            sTk[t] = Tk[g];
-            sTp[t] = Tp[g];
-            sCp[t] = Cp[g];
-        }
-        __syncthreads();
-        cta_matmul_nn<P>(sTp, P, sCp, P, sD, P, true);   // D = Tr_{k-1} C_{k-1}^T
-        __syncthreads();
+        if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, sScr)) return;
     }
     double g[EPI ? P : 1][VEC];
     double om[VEC];
@@ -241,13 +229,7 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
             }
             __syncthreads();
         }
-        // totals of V_k^T W land in Gram2 (free until K2 of this block), then G = Tr_k^T (V_k^T W)
-        if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->om2[a.par], &st->cnt1)) {
-            double* sGv = sTp;
-            for (int t = threadIdx.x; t < P * P; t += NT) sGv[t] = st->Gram2[(t / P) * MAXP + t % P];
-            __syncthreads();
-            cta_matmul_tn<P>(sTk, P, sGv, P, st->G[a.par], MAXP);
-        }
+        cluster_partials(sAcc, E, st->part1);   // K2 forms G = Tr_k^T (V_k^T W) from these
     }
 }
 
@@ -274,103 +256,9 @@ struct K2Smem {
     static constexpr int RQ = PC<P>::RPW * MAXQ;         // pool values of one row group
     static constexpr int pipe = (NT / 32) * NSTAGE * (2 * TILE + RQ);
     static constexpr int loop = 2 * P * P + P * MAXQ + pipe + P * P + MAXQ * P;
-    static constexpr int tail = (3 * P * LD + 2 * P) > (P * P + P * MAXQ) ? (3 * P * LD + 2 * P) : (P * P + P * MAXQ);
+    static constexpr int tail = 3 * P * P + P * MAXQ + prologue_scratch<P>();
     static constexpr size_t bytes = sizeof(double) * (loop + tail);
 };
-
-// Cholesky W'^T W' = C_k^T C_k (right-looking, warp 0 of the CTA holding the totals), the
-// breakdown / cancellation test, C_k^{-1} (= Tr_{k+1}) and the pool coefficients.  Returns
-// false on a breakdown (the main branch stops at this block; the host runs the column path).
-template <int P>
-__device__ bool k3a_factor(DevState* st, int par, int sk, double* scratch) {
-    constexpr int LD = P + 1;
-    double* sA = scratch;
-    double* sC = sA + P * LD;
-    double* sCi = sC + P * LD;
-    double* sD = sCi + P * LD;
-    double* sOm = sD + P;
-    __shared__ int s_bad;
-    const int tid = threadIdx.x, lane = tid & 31;
-    for (int t = tid; t < P * P; t += blockDim.x) {
-        const int r = t / P, c = t % P;
-        sA[r * LD + c] = st->Gram2[r * MAXP + c];
-        sC[r * LD + c] = 0.0;
-    }
-    for (int t = tid; t < P; t += blockDim.x) {
-        sD[t] = st->Gram2[t * MAXP + t];
-        sOm[t] = st->om2[par][t];
-    }
-    __syncthreads();
-    if (tid < 32) {
-        const double tau = st->tau;
-        bool bad = false;
-        for (int m = 0; m < P; ++m) {
-            const double d = sA[m * LD + m];
-            // breakdown: h_{j+p,j}^2 = d <= tau^2 ||A u_j||^2; cancellation guard: the pivot kept
-            // < 1e-4 of ||w'_m||^2 (more than 4 digits lost) -> column path (R2)
-            if (!(d > tau * tau * sOm[m]) || !(d >= 1e-4 * sD[m])) {
-                bad = true;
-                break;
-            }
-            const double cmm = sqrt(d);
-            const double rc = 1.0 / cmm;
-            for (int c = m + lane; c < P; c += 32) sC[m * LD + c] = (c == m) ? cmm : sA[m * LD + c] * rc;
-            __syncwarp();
-            // trailing update A(r,c) -= C(m,r) C(m,c), m < r <= c
-            for (int t = lane; t < P * P; t += 32) {
-                const int r = t / P, c = t % P;
-                if (r > m && c >= r) sA[r * LD + c] = fma(-sC[m * LD + r], sC[m * LD + c], sA[r * LD + c]);
-            }
-            __syncwarp();
-        }
-        if (lane == 0) s_bad = bad;
-        if (!bad && lane < P) {
-            // column `lane` of C_k^{-1} (back substitution)
-            const int l = lane;
-            for (int r = P - 1; r >= 0; --r) {
-                double s = (r == l) ? 1.0 : 0.0;
-                for (int c = r + 1; c <= l; ++c) s = fma(-sC[r * LD + c], sCi[c * LD + l], s);
-                sCi[r * LD + l] = (r <= l) ? s / sC[r * LD + r] : 0.0;
-            }
-        }
-        const int Q = st->q_live;
-        if (!bad && lane < Q) {
-            // coef(:,q) = C_k^{-T} (W'^T r_q) = U_{k+1}^T r_q
-            double y[P];
-#pragma unroll
-            for (int m = 0; m < P; ++m) {
-                double s = st->pdot[lane * MAXP + m];
-#pragma unroll
-                for (int i = 0; i < m; ++i) s = fma(-sC[i * LD + m], y[i], s);
-                y[m] = s / sC[m * LD + m];
-                st->coef[par][m * MAXQ + lane] = y[m];
-            }
-        }
-    }
-    __syncthreads();
-    if (s_bad) {
-        if (tid == 0) {
-            st->need_slow = 1;
-            st->run_main = 0;
-            st->bd_at = st->k_main;
-            st->hflags->bd_at = st->k_main;
-            st->hflags->need_slow = 1;
-            __threadfence_system();
-        }
-        return false;
-    }
-    double* Tn = st->Tr[(sk + 1) % 3];
-    for (int t = tid; t < P * P; t += blockDim.x) {
-        const int r = t / P, c = t % P;
-        st->Ck[par][r * MAXP + c] = sC[r * LD + c];
-        Tn[r * MAXP + c] = sCi[r * LD + c];
-    }
-    if (tid == 0) {
-        st->k_main = st->k_main + 1;
-        st->hflags->k_main = st->k_main;
-    }
-    return true;
-}
 
 template <int P>
 __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
@@ -394,16 +282,16 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
     double* sAcc = sPipe + SM::pipe;
     double* sTail = sAcc + P * P + MAXQ * P;
     {
-        // G_s: lower triangle of G mirrored (the paper computes h_{i,j} for i >= j)
+        // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
+        // computes h_{i,j} for i >= j)
         double* sGs = sTail;
         double* sCo = sTail + P * P;
-        const double* Gp = st->G[a.par];
-        const double* Tk = st->Tr[a.sk];
+        double* sG = sCo + P * MAXQ;
+        k2_prologue<P>(st, a.par, a.sk, sG, sTk, sG + P * P);
         const double* Co = st->coef[a.par ^ 1];
         for (int t = threadIdx.x; t < P * P; t += NT) {
             const int r = t / P, c = t % P;
-            sGs[t] = r >= c ? Gp[r * MAXP + c] : Gp[c * MAXP + r];
-            sTk[t] = Tk[r * MAXP + c];
+            sGs[t] = r >= c ? sG[r * P + c] : sG[c * P + r];
         }
         for (int t = threadIdx.x; t < P * MAXQ; t += NT) sCo[t] = Co[t];
         __syncthreads();
@@ -540,7 +428,7 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
         }
         __syncthreads();
     }
-    if (cluster_reduce(sAcc, E, P, a.part, st->Gram2, st->pdot, &st->cnt2)) k3a_factor<P>(st, a.par, a.sk, sTail);
+    cluster_partials(sAcc, E, st->part2[a.par]);   // K1(k+1) and K3b(k) factor W' from these
 }
 
 // ------------------------------------------------------------------ K3b: small banded QR (side)
@@ -556,7 +444,9 @@ struct K3Smem {
     static constexpr int nA = P * LD;
     static constexpr int nH = 4 * P * LD;
     static constexpr int nV = W2 * (P + 2);
-    static constexpr int doubles = 6 * nA + nH + nV + 3 * P + P * P;
+    static constexpr int rest = nH + nV + 3 * P + P * P;
+    static constexpr int scr = 8 * P * P + 2 * MAXQ * P + P + 8;   // prologue scratch (reuses sH..)
+    static constexpr int doubles = 6 * nA + (rest > scr ? rest : scr);
     static constexpr size_t bytes = sizeof(double) * doubles;
 };
 
@@ -567,10 +457,11 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ long long s_k, s_jd, s_maxit, s_hcap;
     __shared__ double s_tol;
-    __shared__ int s_valid, s_stop_after, s_mlast, s_stop;
+    __shared__ int s_valid, s_stop_after, s_mlast, s_stop, s_given;
     if (tid == 0) {
         const long long k = st->k_side;
         s_valid = (k < st->stop_side_at) && (k < st->bd_at);
+        s_given = st->given_blk == k;
         s_k = k;
         s_jd = st->j_done;
         s_maxit = st->maxit;
@@ -596,9 +487,33 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     double* sHist = sRes + P;     // residual rows of this block (P x P)
     const long long k = s_k, j0 = s_jd + 1, maxit = s_maxit;
     const int par = (int)(k & 1);
+    {
+        // C_k: factor W'^T W' from K2(k)'s partials (as K1(k+1) does), or the host's C_k
+        double* scr = sH;   // scratch (the Hessenberg frame is filled later)
+        double* sCc = scr + prologue_scratch<P>();
+        bool bad = false;
+        if (s_given) {
+            load_pp<P>(sCc, st->Ck[par]);
+        } else {
+            const int Q = st->q_live;
+            double* sRed = scr;
+            double* sOm = scr + P * P + MAXQ * P;
+            for (int t = tid; t < P * P + Q * P; t += K3T) sRed[t] = st->red2[par][t];
+            for (int t = tid; t < P; t += K3T) sOm[t] = st->om2[par][t];
+            __syncthreads();
+            bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sCc, sOm + P, sOm + P + P * P);
+        }
+        if (bad) {   // breakdown of block k: the host runs the column path, then re-runs this block
+            if (tid == 0) {
+                st->side_go = 0;
+                publish_breakdown(st, k);
+            }
+            return;
+        }
+        for (int t = tid; t < P * P; t += K3T) sC[(t / P) * LD + t % P] = sCc[t];
+    }
     for (int t = tid; t < P * P; t += K3T) {
         const int r = t / P, c = t % P, g = r * MAXP + c, s = r * LD + c;
-        sC[s] = st->Ck[par][g];
         sT[s] = st->T[g];
         sG[s] = st->G[par][g];
         sCp[s] = st->CprevS[g];
