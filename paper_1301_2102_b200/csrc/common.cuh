@@ -333,7 +333,7 @@ __device__ __forceinline__ void store_pp(double* dst, const double* src) {
 
 // Scratch (doubles) the K1 / K2 prologues need.
 template <int P>
-constexpr int prologue_scratch() { return (P * P + MAXQ * P) + 6 * P * P + P * MAXQ + P; }
+__host__ __device__ constexpr int prologue_scratch() { return (P * P + MAXQ * P) + 6 * P * P + P * MAXQ + P; }
 
 // K1 prologue, block k: C_{k-1}, Tr_k = C_{k-1}^{-1}, coef_{k-1} from K2(k-1)'s partials (or the
 // host's values after the column path), and D = Tr_{k-1} C_{k-1}^T.  Writes sTk and sD (P x P,

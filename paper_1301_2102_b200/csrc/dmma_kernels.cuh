@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
 
 // ------------------------------------------------------------------ K1 on DMMA (epilogue)
 
-constexpr int K1STAGE = 2;   // V tiles are needed only after the gathers: a short pipeline
+constexpr int K1STAGE = 1;   // V tiles are issued at tile start and land during the gathers
 
 template <int P>
 struct K1DSmem {
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int E = P * P + P;
-    constexpr int CH = 4;
+    constexpr int CH = P <= 8 ? 8 : 4;
     DevState* st = a.st;
     if (!st->run_main) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
