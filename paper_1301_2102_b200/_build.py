@@ -9,7 +9,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbminres.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("bminres.cu",)]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "step_kernels.cuh", "aux_kernels.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "step_kernels.cuh", "aux_kernels.cuh", "dmma_kernels.cuh")] + [
     os.path.join(ROOT, "include", "bminres.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "step_kernels.cuh"
 #include "dmma_kernels.cuh"
+#include "row_kernels.cuh"
 
 using namespace bmr;
 
@@ -47,7 +48,7 @@ struct Kfn {  // per-p kernel table
 };
 
 template <int P>
-Kfn make_kfn() {
+Kfn make_kfn(int q) {
     Kfn f;
     f.k1 = k1_spmm<P, true>;
     f.nt1 = NT;
@@ -60,6 +61,11 @@ Kfn make_kfn() {
     if constexpr (P % 8 == 0) {
         if (!getenv("BMINRES_NO_DMMA")) {
             f.k1 = k1_dmma<P>;
+            if constexpr (P == 8) {   // occupancy / register trade-off of the SpMM pipeline (experiments)
+                const char* mb = getenv("BMINRES_K1_MINB");
+                if (mb && atoi(mb) == 3) f.k1 = k1_dmma<P, 3>;
+                if (mb && atoi(mb) == 4) f.k1 = k1_dmma<P, 4>;
+            }
             f.smem1 = K1DSmem<P>::bytes;
             f.nt1 = 256;
             f.k2 = k2_dmma<P>;
@@ -74,22 +80,29 @@ Kfn make_kfn() {
         f.smem4b = K4bSmem<P>::bytes;
         f.nt4b = NT;
     }
+    if constexpr (P <= 8) {   // thread-per-row TMA kernels (row_kernels.cuh)
+        if (q <= K2R_QMAX && !getenv("BMINRES_NO_ROWK")) {
+            f.k2 = k2_row<P>;
+            f.smem2 = K2RSmem<P>::bytes;
+            f.nt2 = RT;
+        }
+    }
     f.smem3 = K3Smem<P>::bytes;
     return f;
 }
 
-bool kfn_for(int p, Kfn* out) {
+bool kfn_for(int p, Kfn* out, int q = 0) {
     switch (p) {
-        case 1: *out = make_kfn<1>(); return true;
-        case 2: *out = make_kfn<2>(); return true;
-        case 3: *out = make_kfn<3>(); return true;
-        case 4: *out = make_kfn<4>(); return true;
-        case 5: *out = make_kfn<5>(); return true;
-        case 6: *out = make_kfn<6>(); return true;
-        case 7: *out = make_kfn<7>(); return true;
-        case 8: *out = make_kfn<8>(); return true;
-        case 16: *out = make_kfn<16>(); return true;
-        case 32: *out = make_kfn<32>(); return true;
+        case 1: *out = make_kfn<1>(q); return true;
+        case 2: *out = make_kfn<2>(q); return true;
+        case 3: *out = make_kfn<3>(q); return true;
+        case 4: *out = make_kfn<4>(q); return true;
+        case 5: *out = make_kfn<5>(q); return true;
+        case 6: *out = make_kfn<6>(q); return true;
+        case 7: *out = make_kfn<7>(q); return true;
+        case 8: *out = make_kfn<8>(q); return true;
+        case 16: *out = make_kfn<16>(q); return true;
+        case 32: *out = make_kfn<32>(q); return true;
         default: return false;
     }
 }
@@ -284,7 +297,8 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
         h->gexec[s] = nullptr;
     }
-    size_t panel = (size_t)n * p;
+    // panels carry 32 doubles of slack past row n-1 (the 16-byte round-up of TMA bulk copies)
+    size_t panel = (size_t)n * p + 32;
     for (int s = 0; s < 3; ++s) dalloc(h, &h->V[s], panel);
     dalloc(h, &h->M[0], panel);
     dalloc(h, &h->M[1], panel);
@@ -292,7 +306,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         if (h->scr[s]) cudaFree(h->scr[s]);
         h->scr[s] = nullptr;
     }
-    dalloc(h, &h->pool, (size_t)n * std::max(q, 1));
+    dalloc(h, &h->pool, (size_t)n * std::max(q, 1) + 32);
     // generic-kernel partials, then K1 partials (ncl1 x (p*p+p)) and K2 partials x 2 parities
     h->part_elems = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8);
     const size_t e1 = (size_t)NB_MAX * (MAXP * MAXP + MAXP), e2 = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP);
@@ -666,7 +680,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     if (o.world != 1) fail(h, BMINRES_EINVAL, "world > 1 is not implemented in this version");
     const long long n = A->n_loc;
     if (A->n != A->n_loc || A->row_begin != 0) fail(h, BMINRES_EINVAL, "world = 1 needs n_loc = n, row_begin = 0");
-    if (p < 1 || p > BMINRES_MAX_P || !kfn_for(p, &h->kf)) fail(h, BMINRES_EINVAL, "unsupported block size p");
+    if (p < 1 || p > BMINRES_MAX_P || !kfn_for(p, &h->kf, o.pool_size)) fail(h, BMINRES_EINVAL, "unsupported block size p");
     if (n < p) fail(h, BMINRES_EINVAL, "n < p");
     if (!std::isfinite(tol) || tol < 0 || maxit < 0 || !std::isfinite(tau) || tau < 0)
         fail(h, BMINRES_EINVAL, "tol / maxit / deflation_tol out of range");

@@ -162,6 +162,46 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) and mbarriers (1-D: contiguous panel rows)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared, completion counted on bar (bytes: multiple of 16, both addresses 16-aligned)
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// shared -> global (bulk group)
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;\n" ::"n"(N) : "memory"); }
+// generic-proxy shared-memory writes -> visible to the async proxy (before a bulk store reads them)
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -235,57 +275,59 @@ __device__ __forceinline__ void reduce_partials(const double* part, int ncl, int
 // coef(:,q) = C^{-T} (W'^T r_q) = U_{k+1}^T r_q.  Inputs in shared memory: sG (Gram, ld P,
 // destroyed), sOm (p), sPd (q x p).  Outputs: sC (ld P), sCi (ld P), sCo (P x MAXQ).
 // Returns true on breakdown.  Identical in every CTA that calls it.  All threads call it.
+//
+// Latency: this sits on the critical path of every block step (K1's prologue, K3b), so the
+// serial chain has no divisions and no square roots: one rsqrt per pivot (r_m = 1/C(m,m),
+// C(m,m) = d r_m), and the inverse is built row by row inside the same loop -- with L = C^T,
+// row m of L^{-1} = (e_m - sum_{i<m} L(m,i) L^{-1}(i,:)) r_m needs only rows < m of C.
 template <int P>
 __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, int Q, double tau, double* sC,
                              double* sCi, double* sCo) {
     __shared__ int s_bad;
-    __shared__ double sD[P];
     const int tid = threadIdx.x, lane = tid & 31;
-    for (int t = tid; t < P * P; t += blockDim.x) {
-        sC[t] = 0.0;
-        sCi[t] = 0.0;
-    }
-    for (int t = tid; t < P; t += blockDim.x) sD[t] = sG[t * P + t];
-    for (int t = tid; t < P * MAXQ; t += blockDim.x) sCo[t] = 0.0;
-    __syncthreads();
     if (tid < 32) {
+        for (int t = lane; t < P * P; t += 32) {
+            sC[t] = 0.0;
+            sCi[t] = 0.0;
+        }
+        for (int t = lane; t < P * MAXQ; t += 32) sCo[t] = 0.0;
+        const double tau2 = tau * tau;
+        double d0[(P + 31) / 32];   // the pivots before elimination (cancellation guard)
+#pragma unroll
+        for (int u = 0; u < (P + 31) / 32; ++u) d0[u] = (lane + 32 * u < P) ? sG[(lane + 32 * u) * (P + 1)] : 0.0;
+        __syncwarp();
         bool bad = false;
         for (int m = 0; m < P; ++m) {
             const double d = sG[m * P + m];
-            if (!(d > tau * tau * sOm[m]) || !(d >= 1e-4 * sD[m])) {
+            const double dm0 = __shfl_sync(FULL, d0[m / 32], m % 32);
+            if (!(d > tau2 * sOm[m]) || !(d >= 1e-4 * dm0)) {
                 bad = true;
                 break;
             }
-            const double cmm = sqrt(d);
-            const double rc = 1.0 / cmm;
-            for (int c = m + lane; c < P; c += 32) sC[m * P + c] = (c == m) ? cmm : sG[m * P + c] * rc;
+            const double r = rsqrt(d);   // 1 / C(m,m)
+            for (int c = m + lane; c < P; c += 32) sC[m * P + c] = (c == m) ? d * r : sG[m * P + c] * r;
+            // C^{-1}(c, m) = L^{-1}(m, c), c <= m
+            for (int c = lane; c <= m; c += 32) {
+                double s = (c == m) ? 1.0 : 0.0;
+                for (int i = c; i < m; ++i) s = fma(-sC[i * P + m], sCi[c * P + i], s);
+                sCi[c * P + m] = s * r;
+            }
             __syncwarp();
             for (int t = lane; t < P * P; t += 32) {
-                const int r = t / P, c = t % P;
-                if (r > m && c >= r) sG[r * P + c] = fma(-sC[m * P + r], sC[m * P + c], sG[r * P + c]);
+                const int i = t / P, j = t % P;
+                if (i > m && j >= i) sG[i * P + j] = fma(-sC[m * P + i], sC[m * P + j], sG[i * P + j]);
             }
             __syncwarp();
         }
         if (lane == 0) s_bad = bad;
-        if (!bad && lane < P) {
-            const int l = lane;
-            for (int r = P - 1; r >= 0; --r) {
-                double s = (r == l) ? 1.0 : 0.0;
-                for (int c = r + 1; c <= l; ++c) s = fma(-sC[r * P + c], sCi[c * P + l], s);
-                sCi[r * P + l] = (r <= l) ? s / sC[r * P + r] : 0.0;
+        // coef(:, q) = C^{-T} pd(q, :): coef(m, q) = sum_{c <= m} C^{-1}(c, m) pd(q, c)
+        if (!bad)
+            for (int t = lane; t < P * Q; t += 32) {
+                const int m = t % P, q = t / P;
+                double s = 0.0;
+                for (int c = 0; c <= m; ++c) s = fma(sCi[c * P + m], sPd[q * P + c], s);
+                sCo[m * MAXQ + q] = s;
             }
-        }
-        if (!bad && lane < Q) {
-            double y[P];
-#pragma unroll
-            for (int m = 0; m < P; ++m) {
-                double s = sPd[lane * P + m];
-#pragma unroll
-                for (int i = 0; i < m; ++i) s = fma(-sC[i * P + m], y[i], s);
-                y[m] = s / sC[m * P + m];
-                sCo[m * MAXQ + lane] = y[m];
-            }
-        }
     }
     __syncthreads();
     return s_bad != 0;

@@ -56,7 +56,7 @@ __device__ __forceinline__ void stage_tile(double* dst, const double* src, long 
 template <int P>
 struct K4bDSmem {
     static constexpr int WARPS = 4;
-    static constexpr size_t bytes = sizeof(double) * (4 * DM<P>::FR + WARPS * NSTAGE * 4 * DM<P>::TILE);
+    static constexpr size_t bytes = sizeof(double) * (4 * DM<P>::FR + WARPS * NSTAGE * 4 * DM<P>::TILE + 3 * P * P);
 };
 
 template <int P>
@@ -72,26 +72,7 @@ __global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
     double* fB1 = fB2 + FR;    // -R_{k-1,k} R_kk^{-1}
     double* fZ = fB1 + FR;     // Z_k
     double* pipe = fZ + FR;
-    {
-        // scratch for Tr_k and R_kk^{-1} (P x P each) in the pipeline area, then fragments
-        double* sT = pipe;
-        double* sR = pipe + P * P;
-        double* sP = pipe + 2 * P * P;
-        const double* Tk = st->Tr[a.sk];
-        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
-            const int g = (t / P) * MAXP + t % P;
-            sT[t] = Tk[g];
-            sR[t] = st->Ainv[g];
-        }
-        __syncthreads();
-        cta_matmul_nn<P>(sT, P, sR, P, sP, P);
-        __syncthreads();
-        to_frag<P>(sP, P, 1.0, fA);
-        to_frag<P>(st->B2, MAXP, -1.0, fB2);
-        to_frag<P>(st->B1, MAXP, -1.0, fB1);
-        to_frag<P>(st->Z, MAXP, 1.0, fZ);
-        __syncthreads();
-    }
+    double* scr = pipe + WARPS * NSTAGE * 4 * D::TILE;
     double* wb = pipe + warp * NSTAGE * 4 * D::TILE;
     const long long ntiles = (a.n + TR - 1) / TR;
     const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
@@ -107,8 +88,28 @@ __global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
         }
         cp_commit();
     };
+    // the first stages stream in while the prologue forms the p x p factors
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    {
+        double* sT = scr;
+        double* sR = scr + P * P;
+        double* sP = scr + 2 * P * P;
+        const double* Tk = st->Tr[a.sk];
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            const int g = (t / P) * MAXP + t % P;
+            sT[t] = Tk[g];
+            sR[t] = st->Ainv[g];
+        }
+        __syncthreads();
+        cta_matmul_nn<P>(sT, P, sR, P, sP, P);
+        __syncthreads();
+        to_frag<P>(sP, P, 1.0, fA);
+        to_frag<P>(st->B2, MAXP, -1.0, fB2);
+        to_frag<P>(st->B1, MAXP, -1.0, fB1);
+        to_frag<P>(st->Z, MAXP, 1.0, fZ);
+        __syncthreads();
+    }
     const int fr = lane >> 2, fc = lane & 3;   // A-fragment row / col within an 8x4 block
     for (long long it = 0; t0 + it * ts < ntiles; ++it) {
         issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
@@ -206,40 +207,6 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
     double* pipe = fF + KC * 32;
     double* sAcc = pipe + S::pipe;
     double* sTail = sAcc + P * P + MAXQ * P;
-    {
-        // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
-        // computes h_{i,j} for i >= j, P:270-272)
-        double* sGs = sTail;
-        double* sTk = sTail + P * P;
-        double* sX = sTail + 2 * P * P;
-        double* sG = sTail + 3 * P * P;
-        k2_prologue<P>(st, a.par, a.sk, sG, sTk, sTail + 4 * P * P);
-        const double* Co = st->coef[a.par ^ 1];
-        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
-            const int r = t / P, c = t % P;
-            sGs[t] = r >= c ? sG[r * P + c] : sG[c * P + r];
-        }
-        __syncthreads();
-        cta_matmul_nn<P>(sTk, P, sGs, P, sX, P);
-        __syncthreads();
-        to_frag<P>(sX, P, -1.0, fE);
-        // F = Tr_k coef_{k-1}: P x 8 (pool columns q < Q, the rest 0), fragment order over KC blocks
-        for (int t = threadIdx.x; t < KC * 32; t += blockDim.x) {
-            const int kc = t / 32, l = t % 32, r = kc * 4 + l % 4, q = l / 4;
-            double s = 0.0;
-            if (q < Q)
-                for (int i = 0; i < P; ++i) s = fma(sTk[r * P + i], Co[i * MAXQ + q], s);
-            fF[t] = -s;
-        }
-        __syncthreads();
-    }
-    double g[NC][NC][2], pq[NC][2];
-#pragma unroll
-    for (int i = 0; i < NC; ++i) {
-        pq[i][0] = pq[i][1] = 0.0;
-#pragma unroll
-        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
-    }
     double* wb = pipe + warp * NSTAGE * (2 * D::TILE + S::TQ);
     const long long ntiles = (a.n + TR - 1) / TR;
     const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
@@ -260,8 +227,46 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
         }
         cp_commit();
     };
+    // the first stages stream in while the prologue runs (it only needs the small state)
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    {
+        // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
+        // computes h_{i,j} for i >= j, P:270-272)
+        double* sGs = sTail;
+        double* sTk = sTail + P * P;
+        double* sX = sTail + 2 * P * P;
+        double* sG = sTail + 3 * P * P;
+        double* sCo = sTail + 4 * P * P;                // P x MAXQ
+        double* sScr = sCo + P * MAXQ;
+        const double* Co = st->coef[a.par ^ 1];
+        for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) sCo[t] = Co[t];
+        k2_prologue<P>(st, a.par, a.sk, sG, sTk, sScr);   // (syncs after its loads)
+        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
+            const int r = t / P, c = t % P;
+            sGs[t] = r >= c ? sG[r * P + c] : sG[c * P + r];
+        }
+        __syncthreads();
+        cta_matmul_nn<P>(sTk, P, sGs, P, sX, P);
+        // F = Tr_k coef_{k-1}: P x 8 (pool columns q < Q, the rest 0), fragment order over KC blocks
+        for (int t = threadIdx.x; t < KC * 32; t += blockDim.x) {
+            const int kc = t / 32, l = t % 32, r = kc * 4 + l % 4, q = l / 4;
+            double s = 0.0;
+            if (q < Q)
+                for (int i = 0; i < P; ++i) s = fma(sTk[r * P + i], sCo[i * MAXQ + q], s);
+            fF[t] = -s;
+        }
+        __syncthreads();
+        to_frag<P>(sX, P, -1.0, fE);
+        __syncthreads();
+    }
+    double g[NC][NC][2], pq[NC][2];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+        pq[i][0] = pq[i][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    }
     for (long long it = 0; t0 + it * ts < ntiles; ++it) {
         issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
         cp_wait<NSTAGE - 1>();
@@ -350,27 +355,32 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
 
 // ------------------------------------------------------------------ K1 on DMMA (epilogue)
 
-constexpr int K1STAGE = 1;   // V tiles are issued at tile start and land during the gathers
-
 template <int P>
 struct K1DSmem {
     static constexpr int WARPS = 8;
-    static constexpr int pipe = WARPS * (K1STAGE * 2 + 1) * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile
+    static constexpr int pipe = WARPS * 3 * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile per warp
     static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
-    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + (pipe > scr ? pipe : scr) + P * P + P);
+    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + pipe + scr + P * P + P);
 };
 
 // W = (A V_k) Tr_k - V_{k-1} (Tr_{k-1} C_{k-1}^T); ||A u_j||^2; V_k^T W.  The gathers of the SpMM
 // are per lane (LP lanes x 16 B per row, each row summed in CSR order with fma); the three
 // row-local products run as DMMA on the staged tiles.
-template <int P>
-__global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
+//
+// Latency structure: a warp walks its rows as a stream of row groups (RPW rows per warp
+// instruction, TR/RPW groups per tile) with a software pipeline -- while the gathers of group
+// q are in flight, the column indices and values of group q+1 and the row pointers of group
+// q+2 are loaded.  The SpMM of the warp's first tile runs before the prologue (the Cholesky of
+// the previous block's Gram), which only the epilogue needs.
+template <int P, int MINB = (P <= 8 ? 2 : 1)>
+__global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
     using D = DM<P>;
     using C = PC<P>;
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int E = P * P + P;
     constexpr int CH = P <= 8 ? 8 : 4;
+    constexpr int G = TR / RPW;   // row groups per tile
     DevState* st = a.st;
     if (!st->run_main) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -382,18 +392,9 @@ __global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
     double* fT = dynd1;            // Tr_k
     double* fD = fT + FR;          // -(Tr_{k-1} C_{k-1}^T)
     double* pipe = fD + FR;
-    constexpr int PIPE = K1DSmem<P>::pipe > K1DSmem<P>::scr ? K1DSmem<P>::pipe : K1DSmem<P>::scr;
-    double* sAcc = pipe + PIPE;
+    double* scr = pipe + K1DSmem<P>::pipe;
+    double* sAcc = scr + K1DSmem<P>::scr;
     const bool has_prev = st->k_main > 1;
-    {
-        // C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D (pipeline area as scratch)
-        double* sTk = pipe;
-        double* sD = pipe + P * P;
-        if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, pipe + 2 * P * P)) return;
-        to_frag<P>(sTk, P, 1.0, fT);
-        to_frag<P>(sD, P, -1.0, fD);
-        __syncthreads();
-    }
     double g[NC][NC][2], om[NC][2];
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -401,74 +402,126 @@ __global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
 #pragma unroll
         for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
     }
-    double* wb = pipe + warp * (K1STAGE * 2 + 1) * D::TILE;
-    double* tA = wb + K1STAGE * 2 * D::TILE;   // A V_k rows, then W rows
+    double* wb = pipe + warp * 3 * D::TILE;
+    double* tA = wb + 2 * D::TILE;   // A V_k rows, then W rows
+    // each CTA owns a contiguous slab of tiles (its warps interleave inside it), so the
+    // gathers of neighbouring rows (stencil offsets +-1, +-nx) hit this SM's L1
     const long long ntiles = (a.n + TR - 1) / TR;
-    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
-    auto issue = [&](long long it, int slot) {
-        const long long t = t0 + it * ts;
-        if (t < ntiles) {
-            double* sl = wb + slot * 2 * D::TILE;
-            stage_tile<P>(sl, a.X, t * TR, a.n, lane);
-            if (has_prev) stage_tile<P>(sl + D::TILE, a.Vprev, t * TR, a.n, lane);
-        }
-        cp_commit();
+    const long long tpc = (ntiles + gridDim.x - 1) / gridDim.x;
+    const long long cbeg = (long long)blockIdx.x * tpc, cend = cbeg + tpc < ntiles ? cbeg + tpc : ntiles;
+    const long long t0 = cbeg + warp, ts = WARPS;
+    const long long my_tiles = t0 < cend ? (cend - 1 - t0) / ts + 1 : 0;
+    const long long nq = my_tiles * G;   // row groups of this warp
+    auto row_of = [&](long long q) -> long long {
+        return (t0 + (q / G) * ts) * TR + (int)(q % G) * RPW + rsub;
     };
-#pragma unroll
-    for (int s = 0; s < K1STAGE - 1; ++s) issue(s, s);
-    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
-        issue(it + K1STAGE - 1, (int)((it + K1STAGE - 1) % K1STAGE));
-        const long long base = (t0 + it * ts) * TR;
-        // ---- SpMM rows of the tile: acc = sum_j a_ij V_k(j,:)  (CSR order, fma)
-#pragma unroll
-        for (int gp = 0; gp < TR / RPW; ++gp) {
-            const int rl = gp * RPW + rsub;
-            const long long i = base + rl;
-            const bool valid = act && i < a.n;
-            double acc[VEC];
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-            int k0 = 0, k1 = 0;
-            if (valid) {
-                k0 = __ldg(a.rowptr + i);
-                k1 = __ldg(a.rowptr + i + 1);
-            }
-            for (int kb = k0; kb < k1; kb += CH) {
-                int cc[CH];
-                double av[CH];
-                double xv[CH][VEC];
-#pragma unroll
-                for (int t = 0; t < CH; ++t) {
-                    const bool pr = kb + t < k1;
-                    cc[t] = pr ? __ldg(a.col + kb + t) : -1;
-                    av[t] = pr ? __ldg(a.val + kb + t) : 0.0;
-                }
-#pragma unroll
-                for (int t = 0; t < CH; ++t) {
-                    if (cc[t] >= 0) {
-                        ldv<VEC>(a.X + (long long)cc[t] * P + c0, xv[t]);
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < CH; ++t)
-                    if (cc[t] >= 0) {
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
-                    }
-            }
-            if (act) {
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) tA[rl * RS + c0 + v] = acc[v];
+    // pipeline registers: row pointers of group q+1 (rn0, rn1); cols / values of group q
+    int k0 = 0, k1 = 0, rn0 = 0, rn1 = 0;
+    int cc[CH];
+    double av[CH];
+    auto load_rp = [&](long long q, int& r0, int& r1) {
+        r0 = r1 = 0;
+        if (q < nq) {
+            const long long i = row_of(q);
+            if (act && i < a.n) {
+                r0 = __ldg(a.rowptr + i);
+                r1 = __ldg(a.rowptr + i + 1);
             }
         }
-        cp_wait<K1STAGE - 1>();
+    };
+    auto load_cv = [&](int r0, int r1, int (&c)[CH], double (&v)[CH]) {
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const bool pr = r0 + t < r1;
+            c[t] = pr ? __ldg(a.col + r0 + t) : -1;
+            v[t] = pr ? __ldg(a.val + r0 + t) : 0.0;
+        }
+    };
+    // group q: gathers (first CH entries) || loads of group q+1 || row pointers of q+2
+    auto process_group = [&](long long q) {
+        if (q % G == 0) {   // first group of a tile: stage the tile's V_k, V_{k-1} rows
+            const long long base = (t0 + (q / G) * ts) * TR;
+            stage_tile<P>(wb, a.X, base, a.n, lane);
+            if (has_prev) stage_tile<P>(wb + D::TILE, a.Vprev, base, a.n, lane);
+            cp_commit();
+        }
+        double xv[CH][VEC];
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            if (cc[t] >= 0) {
+                ldv<VEC>(a.X + (long long)cc[t] * P + c0, xv[t]);
+            } else {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
+            }
+        }
+        const int gk0 = k0, gk1 = k1;
+        k0 = rn0;
+        k1 = rn1;
+        int cn[CH];
+        double an[CH];
+        load_cv(k0, k1, cn, an);
+        load_rp(q + 2, rn0, rn1);
+        double acc[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+#pragma unroll
+        for (int t = 0; t < CH; ++t)
+            if (cc[t] >= 0) {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
+            }
+        // rows longer than CH entries: the remaining chunks, in CSR order
+        for (int kb = gk0 + CH; kb < gk1; kb += CH) {
+            int c2[CH];
+            double a2[CH];
+            load_cv(kb, gk1, c2, a2);
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                if (c2[t] >= 0) {
+                    ldv<VEC>(a.X + (long long)c2[t] * P + c0, xv[t]);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fma(a2[t], xv[t][v], acc[v]);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            cc[t] = cn[t];
+            av[t] = an[t];
+        }
+        if (act) {
+            const int rl = (int)(q % G) * RPW + rsub;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) tA[rl * RS + c0 + v] = acc[v];
+        }
+    };
+    // pipeline fill, then the SpMM of the first tile (no dependence on the prologue)
+    load_rp(0, k0, k1);
+    load_rp(1, rn0, rn1);
+    load_cv(k0, k1, cc, av);
+    long long q = 0;
+    for (; q < G && q < nq; ++q) process_group(q);
+    {
+        // C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D
+        double* sTk = scr;
+        double* sD = scr + P * P;
+        if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, scr + 2 * P * P)) {
+            cp_wait<0>();
+            return;
+        }
+        to_frag<P>(sTk, P, 1.0, fT);
+        to_frag<P>(sD, P, -1.0, fD);
+        __syncthreads();
+    }
+    for (long long it = 0; it < my_tiles; ++it) {
+        if (it > 0)
+            for (int gq = 0; gq < G; ++gq, ++q) process_group(q);
+        const long long base = (t0 + it * ts) * TR;
+        cp_wait<0>();
         __syncwarp();
-        const double* sl = wb + (int)(it % K1STAGE) * 2 * D::TILE;
-        const double* tV = sl;
-        const double* tP = sl + D::TILE;
+        const double* tV = wb;
+        const double* tP = wb + D::TILE;
 #pragma unroll
         for (int mc = 0; mc < TR / 8; ++mc) {
             const int r0 = mc * 8;
@@ -524,22 +577,45 @@ __global__ void __launch_bounds__(256) k1_dmma(K1Args a) {
             om[nc][0] += __shfl_xor_sync(FULL, om[nc][0], o);
             om[nc][1] += __shfl_xor_sync(FULL, om[nc][1], o);
         }
-    for (int w = 0; w < WARPS; ++w) {
-        if (warp == w) {
+    if constexpr (WARPS * E <= K1DSmem<P>::pipe) {
+        // one slot per warp in the (now idle) pipeline area, then a fixed-order sum over warps
+        __syncthreads();
+        double* slot = pipe + warp * E;
 #pragma unroll
-            for (int i = 0; i < NC; ++i)
+        for (int i = 0; i < NC; ++i)
 #pragma unroll
-                for (int j = 0; j < NC; ++j) frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
-            if (fr == 0) {
+            for (int j = 0; j < NC; ++j) frag_acc(slot, 0, P, i * 8, j * 8, g[i][j], true, lane);
+        if (fr == 0) {
 #pragma unroll
-                for (int nc = 0; nc < NC; ++nc) {
-                    double* d = sAcc + P * P + nc * 8 + 2 * fc;
-                    d[0] = (w == 0 ? 0.0 : d[0]) + om[nc][0];
-                    d[1] = (w == 0 ? 0.0 : d[1]) + om[nc][1];
-                }
+            for (int nc = 0; nc < NC; ++nc) {
+                slot[P * P + nc * 8 + 2 * fc] = om[nc][0];
+                slot[P * P + nc * 8 + 2 * fc + 1] = om[nc][1];
             }
         }
         __syncthreads();
+        for (int e = threadIdx.x; e < E; e += blockDim.x) {
+            double t = pipe[e];
+            for (int w = 1; w < WARPS; ++w) t += pipe[w * E + e];
+            sAcc[e] = t;
+        }
+    } else {
+        for (int w = 0; w < WARPS; ++w) {
+            if (warp == w) {
+#pragma unroll
+                for (int i = 0; i < NC; ++i)
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
+                if (fr == 0) {
+#pragma unroll
+                    for (int nc = 0; nc < NC; ++nc) {
+                        double* d = sAcc + P * P + nc * 8 + 2 * fc;
+                        d[0] = (w == 0 ? 0.0 : d[0]) + om[nc][0];
+                        d[1] = (w == 0 ? 0.0 : d[1]) + om[nc][1];
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
     cluster_partials(sAcc, E, st->part1);   // K2 forms G = Tr_k^T (V_k^T W) from these
 }

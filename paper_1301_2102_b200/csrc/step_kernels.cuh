@@ -444,7 +444,7 @@ struct K3Smem {
     static constexpr int nA = P * LD;
     static constexpr int nH = 4 * P * LD;
     static constexpr int nV = W2 * (P + 2);
-    static constexpr int rest = nH + nV + 3 * P + P * P;
+    static constexpr int rest = nH + nV + 4 * P + P * P;
     static constexpr int scr = 8 * P * P + 2 * MAXQ * P + P + 8;   // prologue scratch (reuses sH..)
     static constexpr int doubles = 6 * nA + (rest > scr ? rest : scr);
     static constexpr size_t bytes = sizeof(double) * doubles;
@@ -482,9 +482,10 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     double* sH = sCp + S::nA;     // the block's p Hessenberg columns, global-row frame (4p rows)
     double* sV = sH + S::nH;      // reflector ring: v (p+1) + tau per slot
     double* sHn = sV + S::nV;     // ||h_j||
-    double* sBeta = sHn + P;      // ||b_i||
+    double* sBeta = sHn + P;      // 1 / ||b_i||
     double* sRes = sBeta + P;     // residuals of the last completed iteration
     double* sHist = sRes + P;     // residual rows of this block (P x P)
+    double* sRd = sHist + P * P;  // 1 / r_jj of this block's columns
     const long long k = s_k, j0 = s_jd + 1, maxit = s_maxit;
     const int par = (int)(k & 1);
     {
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     }
     for (int s = tid; s < W2; s += K3T) sV[s * (P + 2) + P + 1] = st->rtau[s];
     for (int t = tid; t < P; t += K3T) {
-        sBeta[t] = st->beta[t];
+        sBeta[t] = st->beta[t] > 0.0 ? 1.0 / st->beta[t] : 0.0;   // 1 / ||b_i|| (0: converged at j = 0)
         sRes[t] = st->res[t];
     }
     __syncthreads();
@@ -583,20 +584,25 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             for (int q = 1 + lane; q <= P; q += 32) x2 = fma(sH[(o + q) * LD + m], sH[(o + q) * LD + m], x2);
             x2 = warp_sum(x2);
             const double xnorm = sqrt(x2);
+            // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
+            // v = x/(alpha - beta); one reciprocal 1/(beta (alpha - beta)) serves both quotients
             double tj, beta, scl;
             if (xnorm == 0.0) {
                 tj = 0.0;
                 beta = alpha;
                 scl = 0.0;
             } else {
-                beta = -copysign(hypot(alpha, xnorm), alpha);
-                tj = (beta - alpha) / beta;
-                scl = 1.0 / (alpha - beta);
+                beta = -copysign(sqrt(fma(alpha, alpha, x2)), alpha);
+                const double s = alpha - beta;
+                const double inv = 1.0 / (beta * s);
+                tj = -s * s * inv;
+                scl = beta * inv;
             }
             if (fabs(beta) <= DBL_EPSILON * sHn[m]) {
                 stop = 3;
                 break;
             }
+            if (lane == 0) sRd[m] = 1.0 / beta;   // 1 / r_jj for R_kk^{-1}
             double* vj = sV + slot * (P + 2);
             for (int q = lane; q <= P; q += 32) vj[q] = (q == 0) ? 1.0 : sH[(o + q) * LD + m] * scl;
             if (lane == 0) vj[P + 1] = tj;
@@ -630,8 +636,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 const double tl = -s * vj[P];
                 sT[(P - 1) * LD + c] = tl;
                 r2 = fma(tl, tl, r2);
-                const double b = sBeta[c];
-                rel = b > 0.0 ? sqrt(r2) / b : 0.0;
+                rel = sqrt(r2) * sBeta[c];
                 sRes[c] = rel;
                 sHist[m * P + c] = rel;
             }
@@ -655,7 +660,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 double s = (r == l) ? 1.0 : 0.0;
                 if (l <= m_last && r <= l) {
                     for (int c = r + 1; c <= l; ++c) s = fma(-sH[(2 * P + r) * LD + c], sI[c * LD + l], s);
-                    sI[r * LD + l] = s / sH[(2 * P + r) * LD + r];
+                    sI[r * LD + l] = s * sRd[r];
                 } else {
                     sI[r * LD + l] = s;
                 }

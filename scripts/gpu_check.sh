@@ -1,0 +1,19 @@
+#!/bin/bash
+# One GPU round trip: parity tests, bench, ncu launch list, ncu --set full of the step kernels.
+# usage (via gpurun): bash scripts/gpu_check.sh TAG [tests|notests] [full|nofull]
+set -u
+TAG=${1:-run}; TESTS=${2:-tests}; FULL=${3:-full}
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo BUILD FAIL; tail -30 $OUT/build.log; exit 1; }
+if [ "$TESTS" = tests ]; then
+  timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $OUT/pytest.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $OUT/smoke.log
+fi
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches.csv \
+  python bench.py --steps 1 --warmup 1 --iters 400 --no-kernel-timing --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "ncu-launch rc=$?"
+if [ "$FULL" = full ]; then
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k1_|k2_|k3b_|k4b_|dmma" -s 400 -c 10 \
+    -o $OUT/full python bench.py --steps 1 --warmup 1 --iters 800 --no-kernel-timing --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1; echo "ncu-full rc=$?"
+fi
