@@ -45,11 +45,13 @@ struct Kfn {  // per-p kernel table
     void (*k4b)(K4bArgs);
     size_t smem1, smem2, smem3, smem4b;
     int nt1, nt2, nt4b;
+    bool fused;   // K1 applies the M/X update of block k-2 in graph mode (DMMA K1)
 };
 
 template <int P>
 Kfn make_kfn(int q) {
     Kfn f;
+    f.fused = false;
     f.k1 = k1_spmm<P, true>;
     f.nt1 = NT;
     f.smem1 = K1Smem<P>::bytes;
@@ -61,11 +63,7 @@ Kfn make_kfn(int q) {
     if constexpr (P % 8 == 0) {
         if (!getenv("BMINRES_NO_DMMA")) {
             f.k1 = k1_dmma<P>;
-            if constexpr (P == 8) {   // occupancy / register trade-off of the SpMM pipeline (experiments)
-                const char* mb = getenv("BMINRES_K1_MINB");
-                if (mb && atoi(mb) == 3) f.k1 = k1_dmma<P, 3>;
-                if (mb && atoi(mb) == 4) f.k1 = k1_dmma<P, 4>;
-            }
+            f.fused = getenv("BMINRES_NO_FUSE") == nullptr;
             f.smem1 = K1DSmem<P>::bytes;
             f.nt1 = 256;
             f.k2 = k2_dmma<P>;
@@ -162,8 +160,12 @@ struct bminres_ctx {
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> ev_marks;   // (phase, index of start event)
     int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
+    bool pdl = true;   // programmatic dependent launch of the block-step kernels
+    int prio_hi = 0;   // greatest stream priority (side branch)
     long long side_blocks = 0, slow_blocks = 0;
     Kfn kf{};
+    unsigned long long* trace = nullptr;   // timeline tracing buffers (tooling)
+    unsigned* trace_tick = nullptr;
 };
 
 namespace {
@@ -272,20 +274,25 @@ int cluster_grid(bminres_ctx* h, const void* fn, size_t smem, long long n, long 
     return ncl * CL;
 }
 
+// Block-step kernels are launched with programmatic stream serialization (PDL): a kernel may
+// start while its predecessor drains and runs its pre-wait work (prefetch of panels written two
+// launches back) before griddepcontrol.wait (common.cuh pdl_wait).
 template <typename K, typename A>
 void launch_cluster(bminres_ctx* h, K kern, int grid, int nt, size_t smem, A args, const char* what) {
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = h->csz;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(nt);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = h->stream;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args);
     if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
     h->launches++;
@@ -334,6 +341,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, nt, smem);
         return std::max(1, o);
     };
+    h->pdl = getenv("BMINRES_NO_PDL") == nullptr;
     const char* ce = getenv("BMINRES_CLUSTER");
     h->csz = ce ? std::max(1, std::min(8, atoi(ce))) : 2;
     const char* oe = getenv("BMINRES_CTAS_PER_SM");
@@ -343,8 +351,10 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     int o4 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o4, (const void*)h->kf.k4b, h->kf.nt4b, h->kf.smem4b);
     o4 = std::min(cap, std::max(1, o4));
-    h->nb1 = std::min(NB_MAX, h->n_sm * o1) / h->csz * h->csz;
-    h->nb2 = std::min(NB_MAX, h->n_sm * o2) / h->csz * h->csz;
+    // the main-branch grids leave one CTA slot free on csz SMs, so the side branch (K3b, one
+    // CTA) is never starved of a register file while K1 / K2 run
+    h->nb1 = (std::min(NB_MAX, h->n_sm * o1) - (o1 > 1 ? h->csz : 0)) / h->csz * h->csz;
+    h->nb2 = (std::min(NB_MAX, h->n_sm * o2) - (o2 > 1 ? h->csz : 0)) / h->csz * h->csz;
     h->nb4 = h->n_sm * o4;
     (void)cluster_grid;
 
@@ -433,21 +443,31 @@ struct StepPtrs {
 void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     const int P = h->p_ws;
     const int Emax = P * P + (which == 1 ? P : MAXQ * P);
-    k_reduce<<<(Emax + 7) / 8, 256, 0, s>>>(h->st, which, (int)(k & 1), P);
-    check_launch(h, "k_reduce");
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+    cfg.gridDim = dim3((Emax + 7) / 8);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P);
+    if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_reduce: ") + cudaGetErrorString(e));
+    h->launches++;
 }
-void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k) {
+void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
     TimeMark tm(h, PH_SPMM);
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
-             par, sk, h->tpw};
+             par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X};
     cudaStream_t keep = h->stream;
     h->stream = s;
     launch_cluster(h, h->kf.k1, h->nb1, h->kf.nt1, h->kf.smem1, a, "k1_spmm");
     h->stream = keep;
     launch_reduce(h, s, 1, k);
 }
-void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k) {
+void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k, bool with_reduce = true) {
     TimeMark tm(h, PH_ORTH);
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K2Args a{h->V[(sk + 1) % 3], h->V[sk], h->pool, n, h->st, h->part + (size_t)NB_MAX * (MAXP * MAXP + MAXP),
@@ -456,23 +476,39 @@ void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k) {
     h->stream = s;
     launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
     h->stream = keep;
-    launch_reduce(h, s, 2, k);
+    if (with_reduce) launch_reduce(h, s, 2, k);
 }
 // side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
 void launch_k3b(bminres_ctx* h, cudaStream_t s) {
     TimeMark tm(h, PH_SMALLQR);
-    h->kf.k3b<<<1, K3T, h->kf.smem3, s>>>(h->st);
-    check_launch(h, "k3b_smallqr");
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;   // (also recorded into graph kernel nodes)
+    at[0].val.priority = h->prio_hi;
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(K3T);
+    cfg.dynamicSmemBytes = h->kf.smem3;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k3b, h->st);
+    if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k3b_smallqr: ") + cudaGetErrorString(e));
+    h->launches++;
 }
-void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k) {
+// (blk = 0: the block is not recorded in upd_last -- graph captures, whose k is a residue)
+void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int force = 0,
+                bool record = true) {
     TimeMark tm(h, PH_UPDATE);
     const int sk = (int)(k % 3), par = (int)(k & 1);
-    K4bArgs a{h->V[sk], h->M[par], h->M[par ^ 1], sp.X, n, h->st, sk, h->tpw};
+    K4bArgs a{h->V[sk], h->M[par], h->M[par ^ 1], sp.X, n, h->st, sk, h->tpw, par, force, record ? k : 0};
     h->kf.k4b<<<h->nb4, h->kf.nt4b, h->kf.smem4b, s>>>(a);
     check_launch(h, "k4b_update");
 }
 
-// Graph for side block s (s mod 6): {K1, K2 of block s+1} || {K3b, K4b of block s}.
+// Graph for side block s (s mod 6): main {reduce2 of block s, K1 + reduce1 + K2 of block s+1}
+// || side {K3b (, K4b) of block s}, forked after reduce2(s), whose totals K3b factors.  Inside a
+// graph every main-branch edge is programmatic (PDL).  Fused mode: K1(s+1) applies the M/X
+// update of block s-1 and the side branch is K3b alone.
 void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
     const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->V[0], h->M[0], (const void*)(intptr_t)n,
                           (const void*)(intptr_t)h->p_ws};
@@ -485,12 +521,13 @@ void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
         long long saved = h->launches;
         const long long sblk = 6 + q;   // any block with this residue mod 6
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        launch_reduce(h, h->stream, 2, sblk);
         CK(cudaEventRecord(h->ev_fork, h->stream));
         CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-        launch_k1(h, h->stream, sp, n, sblk + 1);
-        launch_k2(h, h->stream, n, sblk + 1);
+        launch_k1(h, h->stream, sp, n, sblk + 1, h->kf.fused ? 1 : 0);
+        launch_k2(h, h->stream, n, sblk + 1, false);
         launch_k3b(h, h->side);
-        launch_k4b(h, h->side, sp, n, sblk);
+        if (!h->kf.fused) launch_k4b(h, h->side, sp, n, sblk, 0, false);
         CK(cudaEventRecord(h->ev_join, h->side));
         CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         CK(cudaStreamEndCapture(h->stream, &g));
@@ -665,6 +702,15 @@ void finish_given_block(bminres_ctx* h, const StepPtrs& sp, long long n, long lo
     CK(cudaStreamSynchronize(h->stream));
 }
 
+// Fused mode: apply the M/X updates of blocks whose K3b has run but whose K1 (two blocks
+// later, which applies them) did not (end of a graph run).  Drains the stream.
+void flush_updates(bminres_ctx* h, const StepPtrs& sp, long long n) {
+    if (!h->kf.fused) return;
+    const long long last = GET_STATE(h, upd_last), ks = GET_STATE(h, k_side);
+    for (long long b = last + 1; b < ks; ++b) launch_k4b(h, h->stream, sp, n, b, 1);
+    CK(cudaStreamSynchronize(h->stream));
+}
+
 bool retained_live(bminres_ctx* h, long long jfirst) {
     for (auto& r : h->retained)
         if (r.expiry >= jfirst) return true;
@@ -788,6 +834,23 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     init.ncl1 = h->nb1 / h->csz;
     init.ncl2 = h->nb2 / h->csz;
     init.given_blk = -1;
+    init.k_upd_min = KINF;
+    init.upd_last = 0;
+    // timeline tracing (tooling): BMINRES_TRACE=<launch number> records that launch of every
+    // block-step kernel (globaltimer per CTA and phase point), dumped to BMINRES_TRACE_FILE
+    const char* trace_env = getenv("BMINRES_TRACE");
+    const size_t trace_elems = (size_t)TR_NKIND * TRACE_CTAS * TRACE_PTS;
+    if (trace_env) {
+        if (!h->trace) {
+            CK(cudaMalloc((void**)&h->trace, trace_elems * sizeof(unsigned long long)));
+            CK(cudaMalloc((void**)&h->trace_tick, TR_NKIND * sizeof(unsigned)));
+        }
+        CK(cudaMemsetAsync(h->trace, 0, trace_elems * sizeof(unsigned long long), h->stream));
+        CK(cudaMemsetAsync(h->trace_tick, 0, TR_NKIND * sizeof(unsigned), h->stream));
+        init.trace = h->trace;
+        init.trace_tick = h->trace_tick;
+        init.trace_launch = atoll(trace_env);
+    }
     for (int t = 0; t < 3; ++t)
         for (int c = 0; c < MAXP; ++c) init.Tr[t][c * MAXP + c] = 1.0;
     std::vector<double> S(MAXP * MAXP, 0.0), beta(p, 0.0), f0n(p, 0.0);
@@ -921,9 +984,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     while (!h->hf->side_done) {
         const bool ret = retained_live(h, (b - 1) * p + 1);
         const bool expl = !graphs || ret;
-        if (!main_ahead) {
+        if (!main_ahead) {   // (reduce2 of block b is left pending: the graph / explicit path runs it)
             launch_k1(h, h->stream, sp, n, b);
-            launch_k2(h, h->stream, n, b);
+            launch_k2(h, h->stream, n, b, false);
             main_ahead = true;
         }
         if (ret) {   // candidates of block b meet a live retained vector: column path
@@ -935,6 +998,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             continue;
         }
         if (expl) {
+            launch_reduce(h, h->stream, 2, b);
             launch_k3b(h, h->stream);
             launch_k4b(h, h->stream, sp, n, b);
             CK(cudaStreamSynchronize(h->stream));
@@ -946,11 +1010,13 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             main_ahead = false;
             continue;
         }
-        // pipelined graphs: side block s with main block s+1
+        // pipelined graphs: side block s with main block s+1 (fused: K1(s+1) applies the
+        // update of block s-1; updates of blocks < b were applied explicitly)
+        if (h->kf.fused) SET_STATE(h, k_upd_min, b);
         long long launched = 0;
         for (long long s = b; s <= nblocks; ++s) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
-            h->launches += 6;
+            h->launches += h->kf.fused ? 5 : 6;
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -959,6 +1025,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             }
         }
         CK(cudaStreamSynchronize(h->stream));
+        flush_updates(h, sp, n);
+        if (h->kf.fused) SET_STATE(h, k_upd_min, KINF);
         if (h->hf->side_done) break;
         b = GET_STATE(h, k_side);
         if (h->hf->need_slow) {
@@ -1018,6 +1086,14 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         s.phase_launches[mk.first] += 1;
     }
     s.gpu_launches = h->launches;
+    if (trace_env && getenv("BMINRES_TRACE_FILE")) {
+        std::vector<unsigned long long> tb(trace_elems);
+        CK(cudaMemcpy(tb.data(), h->trace, trace_elems * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(getenv("BMINRES_TRACE_FILE"), "wb")) {
+            fwrite(tb.data(), sizeof(unsigned long long), tb.size(), f);
+            fclose(f);
+        }
+    }
     const double abytes = 12.0 * A->nnz + 4.0 * (n + 1);
     s.bytes_per_block_step = abytes + 10.0 * 8.0 * (double)panel;   // SURVEY §8(d) algorithmic model
     s.spmm_bytes_per_launch = abytes + 3.0 * 8.0 * (double)panel;
@@ -1082,13 +1158,19 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
             CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
             h->own_stream = true;
         }
-        CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        // the side branch (K3b: one CTA, serial) gets the highest stream priority so its CTA is
+        // dispatched ahead of the main-branch grids
+        int prio_lo = 0, prio_hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        h->prio_hi = prio_hi;
+        CK(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, prio_hi));
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
         // large dynamic shared memory for the p = 32 kernels
-        for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 16, 32}) {
+        for (int p : {1, 2, 3, 4, 5, 6, 7, 8, 16, 32})
+            for (int qv : {0, MAXQ}) {   // (the K2 variant depends on the pool size)
             Kfn f;
-            kfn_for(p, &f);
+            kfn_for(p, &f, qv);
             CK(cudaFuncSetAttribute((const void*)f.k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem1));
             CK(cudaFuncSetAttribute((const void*)f.k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem2));
             CK(cudaFuncSetAttribute((const void*)f.k3b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));

@@ -92,10 +92,14 @@ struct DevState {
     // ---- side-branch state
     double CprevS[MAXP * MAXP];    // C_{k-1} for the Hessenberg assembly
     double T[MAXP * MAXP];         // tail of \bar Z (rows j..j+p-1), T(r,c)
-    double Z[MAXP * MAXP];         // Z_k: row m = z_{(k-1)p+m+1}^T (rows past the stop are 0)
-    double Ainv[MAXP * MAXP];      // R_kk^{-1}
-    double B1[MAXP * MAXP];        // R_{k-1,k} R_kk^{-1}
-    double B2[MAXP * MAXP];        // R_{k-2,k} R_kk^{-1}
+    // K3b(k) outputs for the M/X update of block k, double-buffered by block parity (the update
+    // of block k runs in K1(k+2), beside K3b(k+1))
+    double Z[2][MAXP * MAXP];      // Z_k: row m = z_{(k-1)p+m+1}^T (rows past the stop are 0)
+    double Ainv[2][MAXP * MAXP];   // R_kk^{-1}
+    double B1[2][MAXP * MAXP];     // R_{k-1,k} R_kk^{-1}
+    double B2[2][MAXP * MAXP];     // R_{k-2,k} R_kk^{-1}
+    long long k_upd_min;           // fused updates (K1(k) applies block k-2's) only for blocks >= this
+    long long upd_last;            // last block whose M/X update was applied
     double rv[(2 * MAXP + 1) * (MAXP + 1)];   // Householder ring, slot = i mod (2p+1)
     double rtau[2 * MAXP + 1];
     double beta[MAXP];             // ||b_i||
@@ -106,7 +110,35 @@ struct DevState {
     double* part2[2];              // K2 cluster partials by block parity: ncl2 x (p*p + q*p)
     double red1[MAXP * MAXP + MAXP];            // totals of part1: V_k^T W (p*p), ||A u_j||^2 (p)
     double red2[2][MAXP * MAXP + MAXQ * MAXP];  // totals of part2 by parity: W'^T W' (p*p), r_q^T W'
+    // ---- timeline tracing (tooling; null when off): %globaltimer stamps of launch number
+    // trace_launch of each kernel type, per CTA, TRACE_PTS points (see trace_begin)
+    unsigned long long* trace;
+    unsigned* trace_tick;
+    long long trace_launch;
 };
+
+// kernel types of the trace buffer
+enum TraceKind { TR_K1 = 0, TR_RED1, TR_K2, TR_RED2, TR_K3B, TR_K4B, TR_NKIND };
+constexpr int TRACE_PTS = 8;
+constexpr int TRACE_CTAS = 1024;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// thread 0 of each CTA: the stamp row of this CTA if this launch is the traced one, else null
+__device__ __forceinline__ unsigned long long* trace_begin(const DevState* st, int kind) {
+    if (st->trace == nullptr || threadIdx.x != 0) return nullptr;
+    const unsigned t = atomicAdd(st->trace_tick + kind, 1u);
+    if ((long long)(t / gridDim.x) != st->trace_launch || blockIdx.x >= TRACE_CTAS) return nullptr;
+    unsigned long long* r = st->trace + ((size_t)kind * TRACE_CTAS + blockIdx.x) * TRACE_PTS;
+    r[0] = gtimer();
+    return r;
+}
+__device__ __forceinline__ void trace_pt(unsigned long long* r, int pt) {
+    if (r) r[pt] = gtimer();
+}
 
 // ------------------------------------------------------------------ small helpers
 
@@ -202,11 +234,35 @@ __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_g
 // generic-proxy shared-memory writes -> visible to the async proxy (before a bulk store reads them)
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
+// ---- Programmatic dependent launch (PDL).  A kernel launched with programmatic stream
+// serialization may start while its predecessor drains; pdl_wait() blocks until the predecessor
+// has completed and its memory is visible.  Work before pdl_wait() may only read data of kernels
+// that completed before the predecessor started.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     return v;
 }
+// Deterministic butterfly reduce-scatter of 64 per-lane values over a warp (62 shuffles instead
+// of 64 x 5): on return, v[0] and v[1] of lane l hold the warp totals of entries 2l and 2l+1.
+__device__ __forceinline__ void warp_reduce_scatter64(double (&v)[64]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int lvl = 0; lvl < 5; ++lvl) {
+        const int o = 16 >> lvl, half = 32 >> lvl;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+            const double keep = up ? v[half + i] : v[i];
+            const double send = up ? v[i] : v[half + i];
+            v[i] = keep + __shfl_xor_sync(FULL, send, o);
+        }
+    }
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
@@ -217,7 +273,7 @@ __device__ __forceinline__ double warp_max(double v) {
 // sAcc[E].  The CTAs of a thread-block cluster are combined through distributed shared memory
 // by the cluster's rank-0 CTA (fixed rank order), which writes one partial row
 // part[cluster_id*E .. +E).  There is no last-CTA step: every CTA of the consuming kernel
-// sums the rows itself (reduce_partials), so no serial tail sits on the critical path.
+// reduces the rows with k_reduce (many CTAs in parallel; a single last-CTA tail measured slower).
 __device__ __forceinline__ void cluster_partials(const double* sAcc, int E, double* part) {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
@@ -235,12 +291,17 @@ __device__ __forceinline__ void cluster_partials(const double* sAcc, int E, doub
 
 // The totals of one set of cluster partials: one warp per entry, lanes stride over the partial
 // rows, a fixed shuffle tree -> deterministic.  which = 1: part1 -> red1; which = 2: part2[par]
-// -> red2[par].  Entry counts come from the state (q_live may change between launches).
+// -> red2[par].  Entry counts come from the state (q_live may change between launches).  Launched
+// with PDL after K1 / K2; it triggers no dependents early (the dependent launches at exit, so
+// waiting CTAs never hold SM slots the side branch needs, and its pre-wait prefetch may read the
+// panels of the kernel before this one).
 __global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par, int P) {
+    unsigned long long* tr = trace_begin(st, which == 1 ? TR_RED1 : TR_RED2);
+    pdl_wait();
+    trace_pt(tr, 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int e = blockIdx.x * 8 + warp;
-    const bool main_stopped = !st->run_main;
-    if (main_stopped) return;
+    if (!st->run_main) return;
     const int E = which == 1 ? P * P + P : P * P + st->q_live * P;
     const int ncl = which == 1 ? st->ncl1 : st->ncl2;
     const double* part = which == 1 ? st->part1 : st->part2[par];
@@ -250,23 +311,7 @@ __global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par
     for (int b = lane; b < ncl; b += 32) s += __ldcg(part + (size_t)b * E + e);
     s = warp_sum(s);
     if (lane == 0) out[e] = s;
-}
-
-// out[e] = sum over the ncl partial rows (fixed order, 8 interleaved accumulators; loads are
-// coalesced across threads).  Identical in every CTA that calls it (deterministic).
-__device__ __forceinline__ void reduce_partials(const double* part, int ncl, int E, double* out) {
-    for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        double acc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-        int b = 0;
-        for (; b + 8 <= ncl; b += 8) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] += __ldcg(part + (size_t)(b + u) * E + e);
-        }
-        for (; b < ncl; ++b) acc[0] += __ldcg(part + (size_t)b * E + e);
-        out[e] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    }
+    trace_pt(tr, 5);
 }
 
 // Cholesky W'^T W' = C^T C of the new block (right-looking, warp 0), the breakdown /
@@ -285,6 +330,64 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
                              double* sCi, double* sCo) {
     __shared__ int s_bad;
     const int tid = threadIdx.x, lane = tid & 31;
+    if constexpr (P <= 8) {
+        // register version: lane j < P holds column j of the Gram (fully unrolled, the
+        // trailing update takes C(m, i) from lane i by shuffle)
+        if (tid < 32) {
+            const double tau2 = tau * tau;
+            const bool own = lane < P;
+            double g[P];
+#pragma unroll
+            for (int i = 0; i < P; ++i) g[i] = own ? sG[i * P + lane] : 0.0;
+            const double d0 = own ? sG[lane * P + lane] : 0.0;
+            double cm[P], rr[P];
+            bool bad = false;
+#pragma unroll
+            for (int m = 0; m < P; ++m) {
+                const double dm = __shfl_sync(FULL, g[m], m);
+                const double d0m = __shfl_sync(FULL, d0, m);
+                if (!(dm > tau2 * sOm[m]) || !(dm >= 1e-4 * d0m)) {
+                    bad = true;
+                    break;
+                }
+                const double r = rsqrt(dm);
+                rr[m] = r;
+                const double cmj = lane > m ? g[m] * r : (lane == m ? dm * r : 0.0);
+                cm[m] = cmj;
+#pragma unroll
+                for (int i = m + 1; i < P; ++i) g[i] = fma(-__shfl_sync(FULL, cmj, i), cmj, g[i]);
+            }
+            if (lane == 0) s_bad = bad;
+            if (!bad) {
+                if (own)
+#pragma unroll
+                    for (int m = 0; m < P; ++m) sC[m * P + lane] = cm[m];
+                __syncwarp();
+                // C^{-1}(:, l) by back substitution, lane l (x(c) = 0 for c > l)
+                double x[P];
+#pragma unroll
+                for (int r = P - 1; r >= 0; --r) {
+                    double s = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+                    for (int c = r + 1; c < P; ++c) s = fma(-sC[r * P + c], x[c], s);
+                    x[r] = (r <= lane) ? s * rr[r] : 0.0;
+                }
+                if (own)
+#pragma unroll
+                    for (int r = 0; r < P; ++r) sCi[r * P + lane] = x[r];
+                for (int t = lane; t < P * MAXQ; t += 32) sCo[t] = 0.0;
+                __syncwarp();
+                for (int t = lane; t < P * Q; t += 32) {
+                    const int m = t % P, q = t / P;
+                    double s = 0.0;
+                    for (int c = 0; c <= m; ++c) s = fma(sCi[c * P + m], sPd[q * P + c], s);
+                    sCo[m * MAXQ + q] = s;
+                }
+            }
+        }
+        __syncthreads();
+        return s_bad != 0;
+    }
     if (tid < 32) {
         for (int t = lane; t < P * P; t += 32) {
             sC[t] = 0.0;

@@ -51,34 +51,34 @@ __device__ __forceinline__ void stage_tile(double* dst, const double* src, long 
     }
 }
 
-// ------------------------------------------------------------------ K4b on DMMA
-
-template <int P>
-struct K4bDSmem {
-    static constexpr int WARPS = 4;
-    static constexpr size_t bytes = sizeof(double) * (4 * DM<P>::FR + WARPS * NSTAGE * 4 * DM<P>::TILE + 3 * P * P);
+// ------------------------------------------------------------------ M/X update on DMMA (row a5)
+//
+// M_k = V_k (Tr_k R_kk^{-1}) - M_{k-2} R_{k-2,k}R_kk^{-1} - M_{k-1} R_{k-1,k}R_kk^{-1}
+// (eqn.search-dir-comp); X += M_k Z_k (eqn.approx-update).
+// Warp w of the CTA streams tiles t0 + w + i*ts (< tend) through an NS-deep cp.async ring.
+// Used by the standalone K4b (grid-strided) and, fused, by K1 two blocks later (CTA slab).
+template <int P, int WARPS, int NS>
+struct UpdSmem {
+    static constexpr int doubles = 4 * DM<P>::FR + WARPS * NS * 4 * DM<P>::TILE + 3 * P * P;
 };
 
-template <int P>
-__global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
+template <int P, int WARPS, int NS>
+__device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long long tend, double* smem) {
     using D = DM<P>;
-    constexpr int WARPS = K4bDSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
+    constexpr int TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     DevState* st = a.st;
-    if (!st->side_go) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    extern __shared__ __align__(16) double dynd4[];
-    double* fA = dynd4;        // Tr_k R_kk^{-1}
+    double* fA = smem;         // Tr_k R_kk^{-1}
     double* fB2 = fA + FR;     // -R_{k-2,k} R_kk^{-1}
     double* fB1 = fB2 + FR;    // -R_{k-1,k} R_kk^{-1}
     double* fZ = fB1 + FR;     // Z_k
     double* pipe = fZ + FR;
-    double* scr = pipe + WARPS * NSTAGE * 4 * D::TILE;
-    double* wb = pipe + warp * NSTAGE * 4 * D::TILE;
-    const long long ntiles = (a.n + TR - 1) / TR;
-    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    double* scr = pipe + WARPS * NS * 4 * D::TILE;
+    double* wb = pipe + warp * NS * 4 * D::TILE;
+    const long long tw = t0 + warp;
     auto issue = [&](long long it, int slot) {
-        const long long t = t0 + it * ts;
-        if (t < ntiles) {
+        const long long t = tw + it * ts;
+        if (t < tend) {
             double* sl = wb + slot * 4 * D::TILE;
             const long long base = t * TR;
             stage_tile<P>(sl, a.U, base, a.n, lane);
@@ -88,9 +88,9 @@ __global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
         }
         cp_commit();
     };
-    // the first stages stream in while the prologue forms the p x p factors
+    // the first stages stream in while the p x p factors are formed
 #pragma unroll
-    for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    for (int s = 0; s < NS - 1; ++s) issue(s, s);
     {
         double* sT = scr;
         double* sR = scr + P * P;
@@ -99,32 +99,31 @@ __global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
         for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
             const int g = (t / P) * MAXP + t % P;
             sT[t] = Tk[g];
-            sR[t] = st->Ainv[g];
+            sR[t] = st->Ainv[a.par][g];
         }
         __syncthreads();
         cta_matmul_nn<P>(sT, P, sR, P, sP, P);
         __syncthreads();
         to_frag<P>(sP, P, 1.0, fA);
-        to_frag<P>(st->B2, MAXP, -1.0, fB2);
-        to_frag<P>(st->B1, MAXP, -1.0, fB1);
-        to_frag<P>(st->Z, MAXP, 1.0, fZ);
+        to_frag<P>(st->B2[a.par], MAXP, -1.0, fB2);
+        to_frag<P>(st->B1[a.par], MAXP, -1.0, fB1);
+        to_frag<P>(st->Z[a.par], MAXP, 1.0, fZ);
         __syncthreads();
     }
     const int fr = lane >> 2, fc = lane & 3;   // A-fragment row / col within an 8x4 block
-    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
-        issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
-        cp_wait<NSTAGE - 1>();
+    for (long long it = 0; tw + it * ts < tend; ++it) {
+        issue(it + NS - 1, (int)((it + NS - 1) % NS));
+        cp_wait<NS - 1>();
         __syncwarp();
-        double* sl = wb + (int)(it % NSTAGE) * 4 * D::TILE;
+        double* sl = wb + (int)(it % NS) * 4 * D::TILE;
         const double* tV = sl;
         double* tM2 = sl + D::TILE;
         const double* tM1 = sl + 2 * D::TILE;
         const double* tX = sl + 3 * D::TILE;
-        const long long base = (t0 + it * ts) * TR;
+        const long long base = (tw + it * ts) * TR;
 #pragma unroll
         for (int mc = 0; mc < TR / 8; ++mc) {
             const int r0 = mc * 8;
-            // M_k = V (Tr_k R_kk^{-1}) - M_{k-2} B2 - M_{k-1} B1  (eqn.search-dir-comp)
             double mk[NC][2];
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
@@ -150,7 +149,6 @@ __global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
                     *reinterpret_cast<double2*>(a.M2 + row * P + col) = make_double2(mk[nc][0], mk[nc][1]);
             }
             __syncwarp();
-            // X += M_k Z_k  (eqn.approx-update)
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 const int col = nc * 8 + 2 * fc;
@@ -164,6 +162,27 @@ __global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
         __syncwarp();
     }
     cp_wait<0>();
+}
+
+// ------------------------------------------------------------------ K4b on DMMA (standalone)
+
+template <int P>
+struct K4bDSmem {
+    static constexpr int WARPS = 4;
+    static constexpr size_t bytes = sizeof(double) * UpdSmem<P, WARPS, NSTAGE>::doubles;
+};
+
+template <int P>
+__global__ void __launch_bounds__(128) k4b_dmma(K4bArgs a) {
+    constexpr int WARPS = K4bDSmem<P>::WARPS;
+    DevState* st = a.st;
+    if (!a.force && !st->side_go) return;
+    unsigned long long* tr = trace_begin(st, TR_K4B);
+    if (a.blk > 0 && blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = a.blk;
+    extern __shared__ __align__(16) double dynd4[];
+    const long long ntiles = (a.n + DM<P>::TR - 1) / DM<P>::TR;
+    dmma_update<P, WARPS, NSTAGE>(a, (long long)blockIdx.x * WARPS, (long long)gridDim.x * WARPS, ntiles, dynd4);
+    trace_pt(tr, 5);
 }
 
 
@@ -227,9 +246,11 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
         }
         cp_commit();
     };
-    // the first stages stream in while the prologue runs (it only needs the small state)
+    // the first stages stream in during the wait and the prologue (K1 completed before
+    // reduce1 started; only the totals come from reduce1)
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    pdl_wait();   // red1 (reduce1) is ready
     {
         // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
         // computes h_{i,j} for i >= j)
@@ -326,6 +347,7 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
         __syncwarp();
     }
     cp_wait<0>();
+    pdl_trigger();   // the dependent (reduce2) launches while this grid reduces its partials
     // rows past n were zero-filled, so they contribute nothing; reduce across warps (fixed order)
     for (int w = 0; w < WARPS; ++w) {
         if (warp == w) {
@@ -349,7 +371,7 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
         }
         __syncthreads();
     }
-    cluster_partials(sAcc, E, st->part2[a.par]);   // K1(k+1) and K3b(k) factor W' from these
+    cluster_partials(sAcc, E, st->part2[a.par]);   // reduce2, then K1(k+1) and K3b(k) factor W' from these
 }
 
 
@@ -358,9 +380,12 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
 template <int P>
 struct K1DSmem {
     static constexpr int WARPS = 8;
+    static constexpr int UNS = 2;                            // cp.async stages of the fused update
     static constexpr int pipe = WARPS * 3 * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile per warp
     static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
-    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + pipe + scr + P * P + P);
+    static constexpr int upd = UpdSmem<P, WARPS, UNS>::doubles;   // the update runs first, then the SpMM
+    static constexpr int region = (pipe + scr > upd) ? pipe + scr : upd;
+    static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + region + P * P + P);
 };
 
 // W = (A V_k) Tr_k - V_{k-1} (Tr_{k-1} C_{k-1}^T); ||A u_j||^2; V_k^T W.  The gathers of the SpMM
@@ -372,8 +397,8 @@ struct K1DSmem {
 // q are in flight, the column indices and values of group q+1 and the row pointers of group
 // q+2 are loaded.  The SpMM of the warp's first tile runs before the prologue (the Cholesky of
 // the previous block's Gram), which only the epilogue needs.
-template <int P, int MINB = (P <= 8 ? 2 : 1)>
-__global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
+template <int P>
+__global__ void __launch_bounds__(256, P <= 8 ? 2 : 1) k1_dmma(K1Args a) {
     using D = DM<P>;
     using C = PC<P>;
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
@@ -382,7 +407,7 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
     constexpr int CH = P <= 8 ? 8 : 4;
     constexpr int G = TR / RPW;   // row groups per tile
     DevState* st = a.st;
-    if (!st->run_main) return;
+    unsigned long long* tr = trace_begin(st, TR_K1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane >> 2, fc = lane & 3;
     const int sub = lane % LP, rsub = lane / LP;
@@ -393,7 +418,27 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
     double* fD = fT + FR;          // -(Tr_{k-1} C_{k-1}^T)
     double* pipe = fD + FR;
     double* scr = pipe + K1DSmem<P>::pipe;
-    double* sAcc = scr + K1DSmem<P>::scr;
+    double* sAcc = pipe + K1DSmem<P>::region;
+    // each CTA owns a contiguous slab of tiles (its warps interleave inside it), so the
+    // gathers of neighbouring rows (stencil offsets +-1, +-nx) hit this SM's L1
+    const long long ntiles = (a.n + TR - 1) / TR;
+    const long long tpc = (ntiles + gridDim.x - 1) / gridDim.x;
+    const long long cbeg = (long long)blockIdx.x * tpc, cend = cbeg + tpc < ntiles ? cbeg + tpc : ntiles;
+    if (a.fuse) {
+        // M/X update of block b = k-2 (row a5), on this CTA's slab before its W rows overwrite
+        // V_b (same slot): it needs only K3b(b) and the panels, not the red2 totals, so it runs
+        // before pdl_wait.  The condition reads state that K3b(k-1), running beside this
+        // kernel, can change only in ways that leave it unchanged (uniform over CTAs).
+        const long long k = st->k_main, b = k - 2;
+        if (b >= st->k_upd_min && b < st->k_side && b < st->stop_side_at) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = b;
+            K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b};
+            dmma_update<P, WARPS, K1DSmem<P>::UNS>(u, cbeg, WARPS, cend, pipe);
+            __syncthreads();   // the region is reused by the SpMM
+        }
+    }
+    trace_pt(tr, 1);
+    if (!st->run_main) return;
     const bool has_prev = st->k_main > 1;
     double g[NC][NC][2], om[NC][2];
 #pragma unroll
@@ -404,11 +449,6 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
     }
     double* wb = pipe + warp * 3 * D::TILE;
     double* tA = wb + 2 * D::TILE;   // A V_k rows, then W rows
-    // each CTA owns a contiguous slab of tiles (its warps interleave inside it), so the
-    // gathers of neighbouring rows (stencil offsets +-1, +-nx) hit this SM's L1
-    const long long ntiles = (a.n + TR - 1) / TR;
-    const long long tpc = (ntiles + gridDim.x - 1) / gridDim.x;
-    const long long cbeg = (long long)blockIdx.x * tpc, cend = cbeg + tpc < ntiles ? cbeg + tpc : ntiles;
     const long long t0 = cbeg + warp, ts = WARPS;
     const long long my_tiles = t0 < cend ? (cend - 1 - t0) / ts + 1 : 0;
     const long long nq = my_tiles * G;   // row groups of this warp
@@ -502,6 +542,8 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
     load_cv(k0, k1, cc, av);
     long long q = 0;
     for (; q < G && q < nq; ++q) process_group(q);
+    pdl_wait();   // red2 (reduce2 of block k-1) is ready
+    trace_pt(tr, 2);
     {
         // C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D
         double* sTk = scr;
@@ -514,6 +556,7 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
         to_frag<P>(sD, P, -1.0, fD);
         __syncthreads();
     }
+    trace_pt(tr, 3);
     for (long long it = 0; it < my_tiles; ++it) {
         if (it > 0)
             for (int gq = 0; gq < G; ++gq, ++q) process_group(q);
@@ -569,6 +612,8 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
         __syncwarp();
     }
     cp_wait<0>();
+    trace_pt(tr, 4);
+    pdl_trigger();   // the dependent (reduce1) launches while this grid reduces its partials
     // om: sum over the 8 row-lanes that share a column pair
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1)
@@ -617,7 +662,8 @@ __global__ void __launch_bounds__(256, MINB) k1_dmma(K1Args a) {
             __syncthreads();
         }
     }
-    cluster_partials(sAcc, E, st->part1);   // K2 forms G = Tr_k^T (V_k^T W) from these
+    cluster_partials(sAcc, E, st->part1);   // reduce1, then K2 forms G = Tr_k^T (V_k^T W)
+    trace_pt(tr, 5);
 }
 
 }  // namespace bmr

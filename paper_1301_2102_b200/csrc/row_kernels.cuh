@@ -58,7 +58,7 @@ struct K2RSmem {
     static constexpr int TQ = RT * K2R_QMAX + 2;        // pool tile (row stride pool_cap <= K2R_QMAX)
     static constexpr int STAGE = 2 * TILE + TQ;
     static constexpr int E = P * P + K2R_QMAX * P;
-    static constexpr int red = (RT / 32) * (P * (P + 1) / 2 + K2R_QMAX * P);
+    static constexpr int red = (RT / 32) * 64;
     static constexpr int tail = 4 * P * P + P * MAXQ + prologue_scratch<P>();
     static constexpr size_t bytes =
         sizeof(double) * (RNS * STAGE + P * P + P * MAXQ + (red > tail ? red : tail) + E) + 8 * RNS + 16;
@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
     constexpr int NG = P * (P + 1) / 2;
     DevState* st = a.st;
     if (!st->run_main) return;
+    unsigned long long* tr = trace_begin(st, TR_K2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
     const int E = P * P + Q * P;
@@ -101,7 +102,10 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
     }
     __syncthreads();
     if (tid == 0)
-        for (int s = 0; s < RNS - 1; ++s) issue(s);
+        for (int s = 0; s < RNS - 1; ++s) issue(s);   // W (K1 completed before reduce1) streams in
+    trace_pt(tr, 1);
+    pdl_wait();   // red1 (reduce1) is ready
+    trace_pt(tr, 2);
     {
         // G = Tr_k^T (V_k^T W) from K1's partials; E = -(Tr_k G_s), F = -(Tr_k coef_{k-1})
         double* sGs = sTail;
@@ -132,6 +136,7 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
         }
         __syncthreads();
     }
+    trace_pt(tr, 3);
     double g[NG], pd[K2R_QMAX][P];
 #pragma unroll
     for (int e = 0; e < NG; ++e) g[e] = 0.0;
@@ -200,22 +205,27 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
         }
         __syncthreads();   // stage s is free for the TMA load of tile it+RNS
     }
-    // partials: warp shuffle tree -> per-warp slot -> fixed-order sum over warps (deterministic)
-    constexpr int NE = NG + K2R_QMAX * P;
+    trace_pt(tr, 4);
+    pdl_trigger();   // the dependent (reduce2) launches while this grid reduces its partials
+    // partials: butterfly reduce-scatter per warp -> per-warp slot -> fixed-order sum over warps
+    constexpr int NE = 64;
+    static_assert(NG + K2R_QMAX * P <= NE, "partials exceed the reduce-scatter width");
     double* red = sTail;
     __syncthreads();   // the prologue scratch in sTail is dead
+    {
+        double v[NE];
 #pragma unroll
-    for (int e = 0; e < NG; ++e) {
-        const double t = warp_sum(g[e]);
-        if (lane == 0) red[warp * NE + e] = t;
+        for (int e = 0; e < NE; ++e) v[e] = 0.0;
+#pragma unroll
+        for (int e = 0; e < NG; ++e) v[e] = g[e];
+#pragma unroll
+        for (int q = 0; q < K2R_QMAX; ++q)
+#pragma unroll
+            for (int m = 0; m < P; ++m) v[NG + q * P + m] = pd[q][m];
+        warp_reduce_scatter64(v);
+        red[warp * NE + 2 * lane] = v[0];
+        red[warp * NE + 2 * lane + 1] = v[1];
     }
-#pragma unroll
-    for (int q = 0; q < K2R_QMAX; ++q)
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-            const double t = warp_sum(pd[q][m]);
-            if (lane == 0) red[warp * NE + NG + q * P + m] = t;
-        }
     __syncthreads();
     for (int t = tid; t < E; t += RT) {
         int src;
@@ -230,7 +240,8 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
         for (int w = 1; w < RT / 32; ++w) s += red[w * NE + src];
         sAcc[t] = s;
     }
-    cluster_partials(sAcc, E, st->part2[a.par]);   // K1(k+1) and K3b(k) factor W' from these
+    cluster_partials(sAcc, E, st->part2[a.par]);   // reduce2, then K1(k+1) and K3b(k) factor W'
+    trace_pt(tr, 5);
 }
 
 }  // namespace bmr

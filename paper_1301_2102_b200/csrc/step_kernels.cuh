@@ -41,6 +41,11 @@ struct K1Args {
     int par;              // k mod 2
     int sk;               // k mod 3
     int tpw;              // row groups (tiles of RPW rows) per warp, contiguous
+    // fused M/X update of block k-2 (DMMA K1 only, graph mode): Y holds V_{k-2} on entry
+    int fuse;             // 1: apply the update of block k-2 before the SpMM
+    double* Mk2;          // M slot k mod 2: M_{k-4} in, M_{k-2} out
+    const double* Mk1;    // M slot (k+1) mod 2: M_{k-3}
+    double* Xs;           // solution panel
 };
 
 template <int P>
@@ -86,6 +91,8 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
     constexpr int CH = 4;
     DevState* st = a.st;
     if constexpr (EPI) {
+        pdl_trigger();
+        pdl_wait();
         if (!st->run_main) return;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
             }
             __syncthreads();
         }
-        cluster_partials(sAcc, E, st->part1);   // K2 forms G = Tr_k^T (V_k^T W) from these
+        cluster_partials(sAcc, E, st->part1);   // reduce1, then K2 forms G = Tr_k^T (V_k^T W)
     }
 }
 
@@ -270,6 +277,8 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
     const int c0 = sub * VEC;
+    pdl_trigger();
+    pdl_wait();
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
     const int E = P * P + Q * P;
     using SM = K2Smem<P>;
@@ -428,7 +437,7 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
         }
         __syncthreads();
     }
-    cluster_partials(sAcc, E, st->part2[a.par]);   // K1(k+1) and K3b(k) factor W' from these
+    cluster_partials(sAcc, E, st->part2[a.par]);   // reduce2, then K1(k+1) and K3b(k) factor W'
 }
 
 // ------------------------------------------------------------------ K3b: small banded QR (side)
@@ -455,6 +464,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     using S = K3Smem<P>;
     constexpr int W2 = S::W2, LD = S::LD;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long* tr = trace_begin(st, TR_K3B);
     __shared__ long long s_k, s_jd, s_maxit, s_hcap;
     __shared__ double s_tol;
     __shared__ int s_valid, s_stop_after, s_mlast, s_stop, s_given;
@@ -513,6 +523,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         }
         for (int t = tid; t < P * P; t += K3T) sC[(t / P) * LD + t % P] = sCc[t];
     }
+    trace_pt(tr, 2);
     for (int t = tid; t < P * P; t += K3T) {
         const int r = t / P, c = t % P, g = r * MAXP + c, s = r * LD + c;
         sT[s] = st->T[g];
@@ -672,6 +683,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         }
     }
     __syncthreads();
+    trace_pt(tr, 3);
     const int m_last = s_mlast, stop = s_stop;
     // ---- stores (all threads): B1 = R_{k-1,k} Ainv, B2 = R_{k-2,k} Ainv, side state for block k+1
     for (int t = tid; t < P * P; t += K3T) {
@@ -681,10 +693,10 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             s1 = fma(sH[(P + a2) * LD + b], sI[b * LD + l], s1);
             if (a2 >= b) s2 = fma(sH[a2 * LD + b], sI[b * LD + l], s2);
         }
-        st->B1[g] = s1;
-        st->B2[g] = s2;
-        st->Ainv[g] = sI[a2 * LD + l];
-        st->Z[g] = sZ[a2 * LD + l];
+        st->B1[par][g] = s1;
+        st->B2[par][g] = s2;
+        st->Ainv[par][g] = sI[a2 * LD + l];
+        st->Z[par][g] = sZ[a2 * LD + l];
         st->T[g] = sT[a2 * LD + l];
         st->CprevS[g] = sC[a2 * LD + l];
     }
@@ -719,6 +731,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         if (end) st->hflags->side_done = 1;
         __threadfence_system();
     }
+    trace_pt(tr, 5);
 }
 
 // ------------------------------------------------------------------ K4b: directions and X (side)
@@ -732,6 +745,9 @@ struct K4bArgs {
     DevState* st;
     int sk;               // k mod 3
     int tpw;              // row groups per warp, contiguous
+    int par;              // k mod 2 (K3b output buffer)
+    int force;            // 1: apply regardless of side_go (host flush of a pending update)
+    long long blk;        // k (recorded in upd_last; 0: not recorded)
 };
 
 template <int P>
@@ -747,7 +763,8 @@ __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW, WARPS = NT / 32;
     constexpr int TILE = K4bSmem<P>::TILE;
     DevState* st = a.st;
-    if (!st->side_go) return;
+    if (!a.force && !st->side_go) return;
+    if (a.blk > 0 && blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = a.blk;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
@@ -766,7 +783,7 @@ __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
         for (int t = threadIdx.x; t < P * P; t += NT) {
             const int g = (t / P) * MAXP + t % P;
             sT[t] = Tk[g];
-            sR[t] = st->Ainv[g];
+            sR[t] = st->Ainv[a.par][g];
         }
         __syncthreads();
         cta_matmul_nn<P>(sT, P, sR, P, sZ, P);
@@ -774,11 +791,11 @@ __global__ void __launch_bounds__(NT) k4b_update(K4bArgs a) {
         for (int t = threadIdx.x; t < P * P; t += NT) {
             const int g = (t / P) * MAXP + t % P;
             sAi[t] = sZ[t];
-            sB1[t] = st->B1[g];
-            sB2[t] = st->B2[g];
+            sB1[t] = st->B1[a.par][g];
+            sB2[t] = st->B2[a.par][g];
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < P * P; t += NT) sZ[t] = st->Z[(t / P) * MAXP + t % P];
+        for (int t = threadIdx.x; t < P * P; t += NT) sZ[t] = st->Z[a.par][(t / P) * MAXP + t % P];
         __syncthreads();
     }
     constexpr int RS = C::RS;
