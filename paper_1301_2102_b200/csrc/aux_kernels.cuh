@@ -145,6 +145,55 @@ __global__ void __launch_bounds__(256) k_colsq(const double* X, const double* Y,
     if (threadIdx.x == 0) *cnt = 0u;
 }
 
+// out[a*P + b] = sum_i X(i,a) X(i,b): the Gram of a row-major n x P panel (start block, CholQR2).
+// Thread t owns entries e = t, t+256, ... < P*P and a fixed row order; CTA partials, then the
+// last CTA sums them in fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_gram(const double* X, long long n, int P, double* part, int nb, double* out,
+                                              unsigned* cnt) {
+    const int E = P * P;
+    const int per = (E + 255) / 256;   // entries per thread (<= 4 for P <= 32)
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const int rows_par = E >= 256 ? 1 : 256 / E;   // rows processed in parallel by this CTA
+    const int e0 = E >= 256 ? threadIdx.x : threadIdx.x % E;
+    const int r0 = E >= 256 ? 0 : threadIdx.x / E;
+    if (r0 < rows_par) {
+        for (long long i = (long long)blockIdx.x * rows_par + r0; i < n; i += (long long)gridDim.x * rows_par) {
+            const double* x = X + i * P;
+            for (int u = 0; u < per; ++u) {
+                const int e = e0 + u * 256;
+                if (e < E) s[u] = fma(x[e / P], x[e % P], s[u]);
+            }
+        }
+    }
+    __shared__ double sred[256][4];
+    for (int u = 0; u < 4; ++u) sred[threadIdx.x][u] = s[u];
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += 256) {
+        double r = 0.0;
+        if (E >= 256) {
+            r = sred[e % 256][e / 256];
+        } else {
+            for (int y = 0; y < rows_par; ++y) r += sred[y * E + e][0];
+        }
+        part[(size_t)e * nb + blockIdx.x] = r;
+    }
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int e = warp; e < E; e += 8) {
+        double t = 0.0;
+        for (int b = lane; b < nb; b += 32) t += __ldcg(part + (size_t)e * nb + b);
+        t = warp_sum(t);
+        if (lane == 0) out[e] = t;
+    }
+    if (threadIdx.x == 0) *cnt = 0u;
+}
+
 // out = V Tr (row-major n x P panels; Tr P x P with leading dimension MAXP): materialises
 // U_k = V_k Tr_k for the column-by-column path
 __global__ void k_materialize(const double* V, const double* Tr, double* out, long long n, int P) {

@@ -132,6 +132,7 @@ struct bminres_ctx {
     double* part1 = nullptr;
     double* part2[2] = {nullptr, nullptr};
     double* dsc = nullptr;        // scratch for dot results (MAXREF+8)
+    double* gdev = nullptr;       // start block: Gram columns, then a p x p inverse (2 MAXP^2)
     unsigned* dcnt = nullptr;     // tickets of the generic kernels
     DevState* st = nullptr;
     HostFlags* hf = nullptr;      // host pointer (mapped)
@@ -161,6 +162,7 @@ struct bminres_ctx {
     std::vector<std::pair<int, size_t>> ev_marks;   // (phase, index of start event)
     int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
     bool pdl = true;   // programmatic dependent launch of the block-step kernels
+    int gblocks = 2;   // block steps per captured graph (halves the graph-boundary gaps)
     int prio_hi = 0;   // greatest stream priority (side branch)
     long long side_blocks = 0, slow_blocks = 0;
     Kfn kf{};
@@ -322,6 +324,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     h->part2[0] = h->part1 + e1;
     h->part2[1] = h->part2[0] + e2;
     if (!h->dsc) CK(cudaMalloc((void**)&h->dsc, (MAXREF + 64) * sizeof(double)));
+    if (!h->gdev) CK(cudaMalloc((void**)&h->gdev, 2 * MAXP * MAXP * sizeof(double)));
     if (!h->dcnt) {
         CK(cudaMalloc((void**)&h->dcnt, 16 * sizeof(unsigned)));
         CK(cudaMemset(h->dcnt, 0, 16 * sizeof(unsigned)));
@@ -342,6 +345,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         return std::max(1, o);
     };
     h->pdl = getenv("BMINRES_NO_PDL") == nullptr;
+    if (const char* gb = getenv("BMINRES_GRAPH_BLOCKS")) h->gblocks = std::max(1, std::min(6, atoi(gb)));
     const char* ce = getenv("BMINRES_CLUSTER");
     h->csz = ce ? std::max(1, std::min(8, atoi(ce))) : 2;
     const char* oe = getenv("BMINRES_CTAS_PER_SM");
@@ -511,7 +515,7 @@ void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n,
 // update of block s-1 and the side branch is K3b alone.
 void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
     const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->V[0], h->M[0], (const void*)(intptr_t)n,
-                          (const void*)(intptr_t)h->p_ws};
+                          (const void*)(intptr_t)(h->p_ws * 16 + h->gblocks)};
     bool same = h->gexec[0] && std::equal(key, key + 8, h->gkey);
     if (same) return;
     for (int q = 0; q < 6; ++q) {
@@ -521,14 +525,20 @@ void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
         long long saved = h->launches;
         const long long sblk = 6 + q;   // any block with this residue mod 6
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        launch_reduce(h, h->stream, 2, sblk);
-        CK(cudaEventRecord(h->ev_fork, h->stream));
-        CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-        launch_k1(h, h->stream, sp, n, sblk + 1, h->kf.fused ? 1 : 0);
-        launch_k2(h, h->stream, n, sblk + 1, false);
-        launch_k3b(h, h->side);
-        if (!h->kf.fused) launch_k4b(h, h->side, sp, n, sblk, 0, false);
-        CK(cudaEventRecord(h->ev_join, h->side));
+        for (int j = 0; j < h->gblocks; ++j) {   // block steps t = s .. s+gblocks-1 of one graph
+            const long long t = sblk + j;
+            launch_reduce(h, h->stream, 2, t);
+            CK(cudaEventRecord(h->ev_fork, h->stream));
+            CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+            // K1(t+1) applies the update of block t-1 (fused) and overwrites V_{t-1}: it waits for
+            // the side work of block t-1 (inside this graph from the second step on)
+            if (j > 0) CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+            launch_k1(h, h->stream, sp, n, t + 1, h->kf.fused ? 1 : 0);
+            launch_k2(h, h->stream, n, t + 1, false);
+            launch_k3b(h, h->side);
+            if (!h->kf.fused) launch_k4b(h, h->side, sp, n, t, 0, false);
+            CK(cudaEventRecord(h->ev_join, h->side));
+        }
         CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
         CK(cudaStreamEndCapture(h->stream, &g));
         h->launches = saved;
@@ -711,6 +721,74 @@ void flush_updates(bminres_ctx* h, const StepPtrs& sp, long long n) {
     CK(cudaStreamSynchronize(h->stream));
 }
 
+// Gram G = F^T F of a row-major n x p panel (one k_gram launch), copied to the host (synchronising).
+std::vector<double> panel_gram(bminres_ctx* h, const double* F, long long n, int p) {
+    const int nb = grid_for(h, n, 64, std::min(NB_MAX, 2 * h->n_sm));
+    k_gram<<<nb, 256, 0, h->stream>>>(F, n, p, h->part, nb, h->gdev, h->dcnt + 2);
+    check_launch(h, "k_gram");
+    std::vector<double> G((size_t)p * p);
+    CK(cudaMemcpyAsync(G.data(), h->gdev, G.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return G;
+}
+
+// Upper Cholesky G = R^T R (p x p, row-major, ld p).  Fails when a pivot keeps less than
+// `keep` of its column's squared norm (cancellation) or is not positive.
+bool host_chol(const std::vector<double>& G, int p, double keep, std::vector<double>& R) {
+    R.assign((size_t)p * p, 0.0);
+    std::vector<double> A = G;
+    for (int m = 0; m < p; ++m) {
+        const double d = A[m * p + m];
+        if (!(d > 0.0) || !(d > keep * G[m * p + m])) return false;
+        const double r = std::sqrt(d);
+        for (int c = m; c < p; ++c) R[m * p + c] = (c == m) ? r : A[m * p + c] / r;
+        for (int i = m + 1; i < p; ++i)
+            for (int j = i; j < p; ++j) A[i * p + j] -= R[m * p + i] * R[m * p + j];
+    }
+    return true;
+}
+
+// Start block fast path (row a0): thin QR F0 = U_p S by CholQR2 -- two Gram passes, the p x p
+// factors on the host, U = F R^{-1} on the device.  It is taken only when no column of F0 can be
+// (near-)dependent: every first-pass pivot must keep >= 1e-4 of its column's squared norm, far
+// above the deflation threshold tau^2 (C13); otherwise the caller runs the column-by-column MGS2
+// path, which decides step-0 deflation exactly as the oracle does.  In exact arithmetic S and U
+// are those of the Gram-Schmidt QR (R with positive diagonal is unique).
+bool fast_start(bminres_ctx* h, double* F, long long n, int p, std::vector<double>& S) {
+    if (getenv("BMINRES_NO_FAST_START")) return false;
+    std::vector<double> R1, R2;
+    if (!host_chol(panel_gram(h, F, n, p), p, 1e-4, R1)) return false;
+    auto upload_inverse = [&](const std::vector<double>& R) {   // R^{-1} (upper), ld MAXP
+        std::vector<double> Ri((size_t)MAXP * MAXP, 0.0);
+        for (int l = 0; l < p; ++l)
+            for (int r = l; r >= 0; --r) {
+                double s = (r == l) ? 1.0 : 0.0;
+                for (int c = r + 1; c <= l; ++c) s -= R[r * p + c] * Ri[c * MAXP + l];
+                Ri[r * MAXP + l] = s / R[r * p + r];
+            }
+        CK(cudaMemcpyAsync(h->gdev + MAXP * MAXP, Ri.data(), Ri.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream));
+    };
+    double* U = h->V[0];   // free until block 3
+    const int g = grid_for(h, n * p, 256, 8 * h->n_sm);
+    upload_inverse(R1);
+    k_materialize<<<g, 256, 0, h->stream>>>(F, h->gdev + MAXP * MAXP, U, n, p);
+    check_launch(h, "k_materialize");
+    if (!host_chol(panel_gram(h, U, n, p), p, 0.5, R2)) return false;
+    upload_inverse(R2);
+    k_materialize<<<g, 256, 0, h->stream>>>(U, h->gdev + MAXP * MAXP, F, n, p);
+    check_launch(h, "k_materialize");
+    CK(cudaMemsetAsync(U, 0, (size_t)n * p * sizeof(double), h->stream));
+    std::fill(S.begin(), S.end(), 0.0);
+    for (int r = 0; r < p; ++r)   // S = R2 R1
+        for (int c = r; c < p; ++c) {
+            double s = 0.0;
+            for (int t = r; t <= c; ++t) s += R2[r * p + t] * R1[t * p + c];
+            S[r * MAXP + c] = s;
+        }
+    return true;
+}
+
 bool retained_live(bminres_ctx* h, long long jfirst) {
     for (auto& r : h->retained)
         if (r.expiry >= jfirst) return true;
@@ -885,9 +963,11 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             f0n[c] = std::sqrt(f2[c]);
         }
         // thin QR F0 = U_p S with one re-orthogonalisation (classical GS, two passes) and
-        // step-0 deflation (eqn.init-QR; reading C13)
+        // step-0 deflation (eqn.init-QR; reading C13); CholQR2 fast path when no
+        // column can deflate
         long long nrep0 = 0;
-        for (int i = 0; i < p; ++i) {
+        const bool fast = fast_start(h, F, n, p, S);
+        for (int i = 0; i < (fast ? 0 : p); ++i) {
             Col fi{F + i, p};
             std::vector<Col> prev;
             for (int l = 0; l < i; ++l) prev.push_back(Col{F + l, p});
@@ -976,7 +1056,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     if (graphs && !finished) build_graphs(h, sp, n);
     CK(cudaEventRecord(e_loop0, h->stream));
     const long long nblocks = (maxit + p - 1) / p;
-    const int LAG = 6;
+    const int GB = h->gblocks;               // block steps per graph
+    const int LAG = std::max(2, 6 / GB);     // graphs in flight before the host polls
     std::vector<cudaEvent_t> lag_ev(LAG);
     for (auto& e : lag_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     long long b = 1;          // next block of the side branch
@@ -1014,9 +1095,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // update of block s-1; updates of blocks < b were applied explicitly)
         if (h->kf.fused) SET_STATE(h, k_upd_min, b);
         long long launched = 0;
-        for (long long s = b; s <= nblocks; ++s) {
+        for (long long s = b; s <= nblocks; s += GB) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
-            h->launches += h->kf.fused ? 5 : 6;
+            h->launches += GB * (h->kf.fused ? 5 : 6);
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -1275,8 +1356,10 @@ void bminres_destroy(bminres_handle h) {
     for (int s = 0; s < 6; ++s)
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
     for (double* p : {h->V[0], h->V[1], h->V[2], h->M[0], h->M[1], h->scr[0], h->scr[1], h->pool, h->part, h->dsc,
-                      h->a_val, h->bx, h->xx, h->hist})
+                      h->gdev, h->a_val, h->bx, h->xx, h->hist})
         if (p) cudaFree(p);
+    if (h->trace) cudaFree(h->trace);
+    if (h->trace_tick) cudaFree(h->trace_tick);
     if (h->a_rowptr) cudaFree(h->a_rowptr);
     if (h->a_col) cudaFree(h->a_col);
     if (h->dcnt) cudaFree(h->dcnt);
