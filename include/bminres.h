@@ -90,7 +90,8 @@ typedef struct {
     double ratio;    /* h / omega */
 } bminres_event;
 
-#define BMINRES_NPHASE 10  /* spmm, orth, smallqr, update, slowpath, start, resid, other, basis, spare */
+#define BMINRES_NPHASE 10  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
+                              reduce (k_reduce), spmm_fused (K1 with the M/X update of block k-2) */
 
 typedef struct {
     int32_t status;           /* return code of the last solve */

@@ -157,13 +157,32 @@ __global__ void __launch_bounds__(256) k_gram(const double* X, long long n, int 
     const int e0 = E >= 256 ? threadIdx.x : threadIdx.x % E;
     const int r0 = E >= 256 ? 0 : threadIdx.x / E;
     if (r0 < rows_par) {
-        for (long long i = (long long)blockIdx.x * rows_par + r0; i < n; i += (long long)gridDim.x * rows_par) {
-            const double* x = X + i * P;
-            for (int u = 0; u < per; ++u) {
-                const int e = e0 + u * 256;
-                if (e < E) s[u] = fma(x[e / P], x[e % P], s[u]);
+        int ia[4], ib[4];
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * 256;
+            ia[u] = e < E ? e / P : 0;
+            ib[u] = e < E ? e % P : 0;
+        }
+        // rows in groups of 8 so that 16 loads per entry are in flight (the loop is latency-bound)
+        const long long stride = (long long)gridDim.x * rows_par;
+        long long i = (long long)blockIdx.x * rows_par + r0;
+        for (; i + 7 * stride < n; i += 8 * stride) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (u >= per || e0 + u * 256 >= E) break;
+                double xa[8], xb[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    xa[r] = X[(i + r * stride) * P + ia[u]];
+                    xb[r] = X[(i + r * stride) * P + ib[u]];
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) s[u] = fma(xa[r], xb[r], s[u]);
             }
         }
+        for (; i < n; i += stride)
+            for (int u = 0; u < per; ++u)
+                if (e0 + u * 256 < E) s[u] = fma(X[i * P + ia[u]], X[i * P + ib[u]], s[u]);
     }
     __shared__ double sred[256][4];
     for (int u = 0; u < 4; ++u) sred[threadIdx.x][u] = s[u];

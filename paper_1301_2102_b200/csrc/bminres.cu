@@ -30,7 +30,8 @@ using namespace bmr;
 
 namespace {
 
-enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER };
+enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER, PH_REDUCE,
+             PH_SPMM_FUSED };
 
 struct Retained {
     double* v;
@@ -445,6 +446,7 @@ struct StepPtrs {
 // main branch of block k: gathers V_k (slot k%3), reads V_{k-1} (slot (k-1)%3), writes W and
 // then W' into slot (k+1)%3 (= V_{k+1}); parity k%2 selects the double-buffered small state
 void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
+    TimeMark tm(h, PH_REDUCE);
     const int P = h->p_ws;
     const int Emax = P * P + (which == 1 ? P : MAXQ * P);
     cudaLaunchConfig_t cfg{};
@@ -461,25 +463,29 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     h->launches++;
 }
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
-    TimeMark tm(h, PH_SPMM);
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
              par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X};
-    cudaStream_t keep = h->stream;
-    h->stream = s;
-    launch_cluster(h, h->kf.k1, h->nb1, h->kf.nt1, h->kf.smem1, a, "k1_spmm");
-    h->stream = keep;
+    {
+        TimeMark tm(h, fuse ? PH_SPMM_FUSED : PH_SPMM);
+        cudaStream_t keep = h->stream;
+        h->stream = s;
+        launch_cluster(h, h->kf.k1, h->nb1, h->kf.nt1, h->kf.smem1, a, "k1_spmm");
+        h->stream = keep;
+    }
     launch_reduce(h, s, 1, k);
 }
 void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k, bool with_reduce = true) {
-    TimeMark tm(h, PH_ORTH);
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K2Args a{h->V[(sk + 1) % 3], h->V[sk], h->pool, n, h->st, h->part + (size_t)NB_MAX * (MAXP * MAXP + MAXP),
              par, sk, h->tpw};
-    cudaStream_t keep = h->stream;
-    h->stream = s;
-    launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
-    h->stream = keep;
+    {
+        TimeMark tm(h, PH_ORTH);
+        cudaStream_t keep = h->stream;
+        h->stream = s;
+        launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
+        h->stream = keep;
+    }
     if (with_reduce) launch_reduce(h, s, 2, k);
 }
 // side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
@@ -1053,6 +1059,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
 
     // ---- block loop
     const bool graphs = o.use_graphs && !o.timing;
+    // timing mode of a fused kernel set: the graph's launches issued explicitly, in the graph's
+    // order, with an event pair around each (the kernels the product runs, timed one by one)
+    const bool fused_expl = o.timing && h->kf.fused;
     if (graphs && !finished) build_graphs(h, sp, n);
     CK(cudaEventRecord(e_loop0, h->stream));
     const long long nblocks = (maxit + p - 1) / p;
@@ -1064,7 +1073,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     bool main_ahead = false;  // K1, K2 of block b already done (V_{b+1} ready)
     while (!h->hf->side_done) {
         const bool ret = retained_live(h, (b - 1) * p + 1);
-        const bool expl = !graphs || ret;
+        const bool expl = (!graphs && !fused_expl) || ret;
         if (!main_ahead) {   // (reduce2 of block b is left pending: the graph / explicit path runs it)
             launch_k1(h, h->stream, sp, n, b);
             launch_k2(h, h->stream, n, b, false);
@@ -1095,7 +1104,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // update of block s-1; updates of blocks < b were applied explicitly)
         if (h->kf.fused) SET_STATE(h, k_upd_min, b);
         long long launched = 0;
-        for (long long s = b; s <= nblocks; s += GB) {
+        for (long long s = b; s <= nblocks && graphs; s += GB) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
             h->launches += GB * (h->kf.fused ? 5 : 6);
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
@@ -1104,6 +1113,14 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
                 CK(cudaEventSynchronize(lag_ev[launched % LAG]));
                 if (h->hf->side_done || h->hf->need_slow) break;
             }
+        }
+        for (long long s = b; s <= nblocks && !graphs; ++s) {   // fused_expl (timing mode)
+            launch_reduce(h, h->stream, 2, s);
+            launch_k3b(h, h->stream);
+            launch_k1(h, h->stream, sp, n, s + 1, 1);
+            launch_k2(h, h->stream, n, s + 1, false);
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->hf->side_done || h->hf->need_slow) break;
         }
         CK(cudaStreamSynchronize(h->stream));
         flush_updates(h, sp, n);
