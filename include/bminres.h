@@ -41,7 +41,7 @@ extern "C" {
 #define BMINRES_MAXIT 1        /* j reached maxit first (Alg. 2); X holds X_maxit */
 #define BMINRES_EINVAL (-1)    /* bad argument: p out of range, n < p, malformed CSR, tol not finite */
 #define BMINRES_ECUDA (-2)     /* CUDA runtime error (message in bminres_last_error) */
-#define BMINRES_ENCCL (-3)     /* reserved: collective error (world > 1) */
+#define BMINRES_ENCCL (-3)     /* collective / transport error (world > 1) */
 #define BMINRES_ENOMEM (-4)    /* device allocation failed */
 #define BMINRES_EPOOL (-5)     /* breakdown with the replacement pool empty, not converged */
 #define BMINRES_ESINGULAR_R (-6) /* |r_jj| <= eps_mach*||h_j||: R_j singular, X cannot be updated */
@@ -69,7 +69,7 @@ typedef struct {
 
 typedef struct {
     int32_t device;          /* CUDA device ordinal */
-    int32_t rank, world;     /* row partition; only world = 1 is implemented in this version */
+    int32_t rank, world;     /* row partition (world > 1: see "Row-partitioned solves" below) */
     void *stream;            /* cudaStream_t to run on; NULL = a stream the library creates */
     uint64_t seed;           /* random replacement vectors (reading C17), default 0 */
     int32_t pool_size;       /* random vectors kept orthogonal to the basis, 0..8, default 1 */
@@ -155,6 +155,48 @@ int bminres_random_vector(bminres_handle h, uint64_t seed, uint64_t stream, uint
 
 /* Bytes of device workspace bminres_solve allocates for (n_loc, p, pool_size). */
 size_t bminres_workspace_bytes(int64_t n_loc, int32_t p, int32_t pool_size);
+
+/* ---- Row-partitioned solves (world > 1) ----
+ * Rank r passes the contiguous rows [row_begin, row_begin + n_loc) of A (GLOBAL column
+ * indices), B and X; ranks are in row order and cover 0..n-1.  Per block step the only
+ * exchanges are the halo of the SpMM (the V rows other ranks' CSR rows reference, sent after K2)
+ * and one fp64 sum-allreduce after each of the two grid-wide reductions; the small banded QR
+ * runs replicated.  A transport must be attached before the first solve: NCCL
+ * (bminres_get_unique_id on one rank, the id broadcast by the caller, bminres_init_nccl on every
+ * rank; graph-capturable) or host callbacks (bminres_set_comm_callbacks; data staged through
+ * host memory, plain launches -- a testing transport).  The allreduce must return bitwise
+ * identical sums on every rank (ranks then take identical decisions). */
+
+/* Host callbacks of a transport; every pointer is HOST memory; return 0 on success.
+ * allreduce: in-place sum over ranks of count doubles.
+ * alltoallv: send holds scount[q] int64 for each rank q (in rank order) -> recv gets rcount[q]
+ *            int64 from each rank q (in rank order).
+ * exchange:  same layout, doubles. */
+typedef struct {
+    void *ctx;
+    int (*allreduce)(void *ctx, double *buf, int64_t count);
+    int (*alltoallv)(void *ctx, const int64_t *send, const int64_t *scount, int64_t *recv, const int64_t *rcount);
+    int (*exchange)(void *ctx, const double *send, const int64_t *scount, double *recv, const int64_t *rcount);
+} bminres_comm_callbacks;
+
+/* NCCL unique id (128 bytes) for bminres_init_nccl; one rank creates it.  BMINRES_ENCCL if
+ * libnccl.so.2 cannot be loaded (dlopen; override the path with BMINRES_NCCL_LIB). */
+int bminres_get_unique_id(uint8_t out[128]);
+
+/* Create the handle's NCCL communicator for (opt.rank, opt.world) on its device. */
+int bminres_init_nccl(bminres_handle h, const uint8_t id[128]);
+
+/* Attach host-callback transport for (opt.rank, opt.world); cb is copied. */
+int bminres_set_comm_callbacks(bminres_handle h, const bminres_comm_callbacks *cb);
+
+/* Halo plan of a row partition (host only; no device, no communication).  offsets[0..world]:
+ * global row offsets (rank q owns [offsets[q], offsets[q+1])).  col_idx: this rank's nnz
+ * GLOBAL column indices.  Outputs: local_col[nnz] = column index into the extended panel
+ * [n_loc own rows | n_halo halo rows]; halo_rows[n_halo] = the global rows of the halo,
+ * ascending (hence grouped by owner rank); halo_count[world] = halo rows owned by each rank.
+ * Pass halo_rows = NULL to query *n_halo only.  BMINRES_EINVAL on a column outside [0, n). */
+int bminres_halo_plan(int32_t world, int32_t rank, const int64_t *offsets, int64_t nnz, const int32_t *col_idx,
+                      int32_t *local_col, int64_t *halo_rows, int64_t *n_halo, int64_t *halo_count);
 
 /* Message of the last error on this handle (or the last create error if h is NULL). */
 const char *bminres_last_error(bminres_handle h);

@@ -38,6 +38,17 @@ class CsrStruct(C.Structure):
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
 
 
+ALLRED_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                           C.POINTER(C.c_int64))
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                          C.POINTER(C.c_int64))
+
+
+class CommCallbacks(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allreduce", ALLRED_FN), ("alltoallv", ALLTOALLV_FN), ("exchange", EXCHANGE_FN)]
+
+
 class Event(C.Structure):
     _fields_ = [("j", C.c_int64), ("col", C.c_int32), ("kind", C.c_int32), ("action", C.c_int32),
                 ("pad", C.c_int32), ("ratio", C.c_double)]
@@ -78,6 +89,11 @@ def lib():
                                             C.c_int64, C.c_void_p, C.c_int64]
         L.bminres_workspace_bytes.argtypes = [C.c_int64, C.c_int32, C.c_int32]
         L.bminres_workspace_bytes.restype = C.c_size_t
+        L.bminres_get_unique_id.argtypes = [C.c_void_p]
+        L.bminres_init_nccl.argtypes = [C.c_void_p, C.c_void_p]
+        L.bminres_set_comm_callbacks.argtypes = [C.c_void_p, C.POINTER(CommCallbacks)]
+        L.bminres_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
         L.bminres_last_error.argtypes = [C.c_void_p]
         L.bminres_last_error.restype = C.c_char_p
         L.bminres_destroy.argtypes = [C.c_void_p]
@@ -88,6 +104,7 @@ def lib():
 
 EXPORTED = ["bminres_default_options", "bminres_create", "bminres_solve", "bminres_stats", "bminres_get_history",
             "bminres_get_events", "bminres_spmm", "bminres_random_vector", "bminres_workspace_bytes",
+            "bminres_get_unique_id", "bminres_init_nccl", "bminres_set_comm_callbacks", "bminres_halo_plan",
             "bminres_last_error", "bminres_destroy"]
 
 
@@ -108,11 +125,15 @@ def _ptr(x):
 
 @dataclass
 class DeviceCsr:
-    """CSR arrays resident on one CUDA device (torch tensors): int32 row_ptr/col_idx, fp64 values."""
+    """CSR arrays resident on one CUDA device (torch tensors): int32 row_ptr/col_idx, fp64 values.
+    n = rows held here; for a row partition (world > 1) rows [row_begin, row_begin + n) of an
+    n_global x n_global matrix, column indices global."""
     n: int
     row_ptr: object
     col_idx: object
     values: object
+    row_begin: int = 0
+    n_global: int | None = None
 
     @property
     def nnz(self) -> int:
@@ -125,13 +146,27 @@ class DeviceCsr:
                    torch.from_numpy(np.ascontiguousarray(A.indices, dtype=np.int32)).to(device),
                    torch.from_numpy(np.ascontiguousarray(A.data, dtype=np.float64)).to(device))
 
+    @classmethod
+    def rows_from_host(cls, A, row_begin: int, row_end: int, device="cuda"):
+        """Rows [row_begin, row_end) of the host CSR A (global column indices kept)."""
+        import torch
+        ip = np.asarray(A.indptr, dtype=np.int64)
+        k0, k1 = int(ip[row_begin]), int(ip[row_end])
+        rp = (ip[row_begin:row_end + 1] - k0).astype(np.int32)
+        return cls(row_end - row_begin, torch.from_numpy(rp).to(device),
+                   torch.from_numpy(np.ascontiguousarray(A.indices[k0:k1], dtype=np.int32)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(A.data[k0:k1], dtype=np.float64)).to(device),
+                   row_begin, int(A.n))
+
 
 def _csr_struct(A) -> CsrStruct:
     s = CsrStruct()
     if isinstance(A, DeviceCsr):
-        s.n, s.nnz = A.n, A.nnz
+        s.n, s.nnz = (A.n_global if A.n_global is not None else A.n), A.nnz
         s.row_ptr, s.col_idx, s.values = _ptr(A.row_ptr), _ptr(A.col_idx), _ptr(A.values)
-        keep = (A,)
+        s.row_begin, s.n_loc = A.row_begin, A.n
+        s._keep = (A,)
+        return s
     else:  # host CSR (numpy): the library stages it
         ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
         ix = np.ascontiguousarray(A.indices, dtype=np.int32)
@@ -142,6 +177,26 @@ def _csr_struct(A) -> CsrStruct:
     s.row_begin, s.n_loc = 0, s.n
     s._keep = keep
     return s
+
+
+def halo_plan(world: int, rank: int, offsets, col_idx):
+    """bminres_halo_plan (host only): (local_col, halo_rows, halo_count) of this rank's global
+    column indices under the row partition `offsets` (world+1 int64)."""
+    L = lib()
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    col = np.ascontiguousarray(col_idx, dtype=np.int32)
+    nh = C.c_int64()
+    rc = L.bminres_halo_plan(world, rank, off.ctypes.data, len(col), col.ctypes.data, None, None, C.byref(nh), None)
+    if rc != 0:
+        raise BminresError(f"bminres_halo_plan: {STATUS.get(rc, rc)}")
+    local = np.zeros(max(len(col), 1), dtype=np.int32)
+    rows = np.zeros(max(nh.value, 1), dtype=np.int64)
+    cnt = np.zeros(world, dtype=np.int64)
+    rc = L.bminres_halo_plan(world, rank, off.ctypes.data, len(col), col.ctypes.data, local.ctypes.data,
+                             rows.ctypes.data, C.byref(nh), cnt.ctypes.data)
+    if rc != 0:
+        raise BminresError(f"bminres_halo_plan: {STATUS.get(rc, rc)}")
+    return local[:len(col)], rows[:nh.value], cnt
 
 
 @dataclass
@@ -158,23 +213,120 @@ class SolveResult:
         return STATUS.get(self.status, str(self.status))
 
 
+class TorchComm:
+    """Host-callback transport over a torch.distributed process group (e.g. gloo): the testing
+    transport of a row-partitioned solve (bminres_set_comm_callbacks).  Marshalling only; the
+    allreduce is an all-gather summed in rank order, so every rank gets bitwise identical sums."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.cb = CommCallbacks(None, ALLRED_FN(self._allreduce), ALLTOALLV_FN(self._alltoallv),
+                                EXCHANGE_FN(self._exchange))
+
+    def _allreduce(self, ctx, buf, count):
+        try:
+            import torch
+            a = np.ctypeslib.as_array(buf, shape=(count,))
+            t = torch.from_numpy(a.copy())
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            self.dist.all_gather(parts, t, group=self.group)
+            tot = parts[0].clone()
+            for q in range(1, self.world):
+                tot += parts[q]
+            a[:] = tot.numpy()
+            return 0
+        except Exception:   # noqa: BLE001 -- reported to the library as a transport error
+            return 1
+
+    def _p2p(self, send, scount, recv, rcount, dtype):
+        import torch
+        sc = [int(scount[q]) for q in range(self.world)]
+        rc = [int(rcount[q]) for q in range(self.world)]
+        s_arr = np.ctypeslib.as_array(send, shape=(max(sum(sc), 1),))
+        r_arr = np.ctypeslib.as_array(recv, shape=(max(sum(rc), 1),))
+        so = np.concatenate([[0], np.cumsum(sc)]).astype(int)
+        ro = np.concatenate([[0], np.cumsum(rc)]).astype(int)
+        reqs, bufs = [], []
+        for q in range(self.world):
+            if q == self.rank:
+                r_arr[ro[q]:ro[q] + rc[q]] = s_arr[so[q]:so[q] + sc[q]]
+                continue
+            if sc[q]:
+                reqs.append(self.dist.isend(torch.from_numpy(s_arr[so[q]:so[q] + sc[q]].copy()), q, group=self.group))
+            if rc[q]:
+                t = torch.empty(rc[q], dtype=dtype)
+                bufs.append((q, t))
+                reqs.append(self.dist.irecv(t, q, group=self.group))
+        for r in reqs:
+            r.wait()
+        for q, t in bufs:
+            r_arr[ro[q]:ro[q] + rc[q]] = t.numpy()
+
+    def _alltoallv(self, ctx, send, scount, recv, rcount):
+        try:
+            import torch
+            self._p2p(send, scount, recv, rcount, torch.int64)
+            return 0
+        except Exception:   # noqa: BLE001
+            return 1
+
+    def _exchange(self, ctx, send, scount, recv, rcount):
+        try:
+            import torch
+            self._p2p(send, scount, recv, rcount, torch.float64)
+            return 0
+        except Exception:   # noqa: BLE001
+            return 1
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    rc = lib().bminres_get_unique_id(C.addressof(buf))
+    if rc != 0:
+        raise BminresError(f"bminres_get_unique_id: {STATUS.get(rc, rc)}: {lib().bminres_last_error(None).decode()}")
+    return bytes(buf)
+
+
 class Solver:
-    """One handle of the C ABI (bminres_create ... bminres_destroy)."""
+    """One handle of the C ABI (bminres_create ... bminres_destroy).
+
+    Row-partitioned solves (world > 1): pass rank/world and comm = "nccl" (the unique id is
+    broadcast over the default torch.distributed group) or a TorchComm (host callbacks)."""
 
     def __init__(self, device: int = 0, *, pool_size: int = 1, seed: int = 0, use_graphs: bool = True,
-                 timing: bool = False, record_history: bool = True, use_x0: bool = False, stream=None):
+                 timing: bool = False, record_history: bool = True, use_x0: bool = False, stream=None,
+                 rank: int = 0, world: int = 1, comm=None):
         L = lib()
         o = Options()
         L.bminres_default_options(C.byref(o))
         o.device, o.pool_size, o.seed = device, pool_size, seed
         o.use_graphs, o.timing, o.record_history, o.use_x0 = int(use_graphs), int(timing), int(record_history), int(use_x0)
         o.stream = stream
+        o.rank, o.world = rank, world
         h = C.c_void_p()
         rc = L.bminres_create(C.byref(o), C.byref(h))
         if rc != 0:
             raise BminresError(f"bminres_create: {STATUS.get(rc, rc)}: {L.bminres_last_error(None).decode()}")
         self._h = h
         self.options = o
+        self._comm = comm
+        if comm == "nccl":
+            uid = nccl_unique_id() if rank == 0 else None
+            if world > 1:
+                import torch.distributed as dist
+                box = [uid]
+                dist.broadcast_object_list(box, src=0)
+                uid = box[0]
+            buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            rc = L.bminres_init_nccl(self._h, C.addressof(buf))
+            if rc != 0:
+                raise BminresError(f"bminres_init_nccl: {STATUS.get(rc, rc)}: {self.last_error()}")
+        elif comm is not None:
+            rc = L.bminres_set_comm_callbacks(self._h, C.byref(comm.cb))
+            if rc != 0:
+                raise BminresError(f"bminres_set_comm_callbacks: {STATUS.get(rc, rc)}")
 
     def close(self):
         if getattr(self, "_h", None):

@@ -25,6 +25,7 @@
 #include "step_kernels.cuh"
 #include "dmma_kernels.cuh"
 #include "row_kernels.cuh"
+#include "comm.cuh"
 
 using namespace bmr;
 
@@ -169,6 +170,18 @@ struct bminres_ctx {
     Kfn kf{};
     unsigned long long* trace = nullptr;   // timeline tracing buffers (tooling)
     unsigned* trace_tick = nullptr;
+    // row partition (world > 1; comm.cuh)
+    Transport* tp = nullptr;
+    HaloPlan plan;
+    const void* plan_key[5] = {};
+    long long n_ext = -1;                  // n_loc + n_halo rows of the V slots
+    long long next_ws = -1;                // n_ext the workspace was sized for
+    int* d_lcol = nullptr;                 // CSR column indices remapped into the extended panel
+    long long* d_send_rows = nullptr;      // local rows the peers read, grouped by peer
+    double* d_sendbuf = nullptr;
+    size_t lcol_cap = 0, send_cap = 0, sendbuf_cap = 0;
+    std::vector<long long> sc_d, rc_d;     // halo counts in doubles (rows x p) per peer
+    int world() const { return opt.world; }
 };
 
 namespace {
@@ -187,6 +200,13 @@ thread_local std::string g_create_err;
 void fail(bminres_ctx* h, int code, const std::string& msg) {
     h->err = msg;
     throw Err{code};
+}
+
+// sum over ranks (world > 1) of count doubles at dev, in place, stream-ordered on s
+void allred(bminres_ctx* h, double* dev, long long count, cudaStream_t s) {
+    if (!h->tp) return;
+    std::string err;
+    if (!h->tp->allreduce(dev, count, s, err)) fail(h, BMINRES_ENCCL, err);
 }
 
 bool is_device_ptr(const void* p) {
@@ -302,14 +322,17 @@ void launch_cluster(bminres_ctx* h, K kern, int grid, int nt, size_t smem, A arg
 }
 
 void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
-    if (h->n_ws == n && h->p_ws == p && h->q_ws == q) return;
+    if (h->n_ws == n && h->p_ws == p && h->q_ws == q && h->next_ws == h->n_ext) return;
+    h->next_ws = h->n_ext;
     for (int s = 0; s < 6; ++s) {
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
         h->gexec[s] = nullptr;
     }
-    // panels carry 32 doubles of slack past row n-1 (the 16-byte round-up of TMA bulk copies)
+    // panels carry 32 doubles of slack past row n-1 (the 16-byte round-up of TMA bulk copies);
+    // the V slots also hold the halo rows of a row partition (n_ext >= n)
     size_t panel = (size_t)n * p + 32;
-    for (int s = 0; s < 3; ++s) dalloc(h, &h->V[s], panel);
+    const size_t vpanel = (size_t)std::max(n, h->n_ext) * p + 32;
+    for (int s = 0; s < 3; ++s) dalloc(h, &h->V[s], vpanel);
     dalloc(h, &h->M[0], panel);
     dalloc(h, &h->M[1], panel);
     for (int s = 0; s < 2; ++s) {
@@ -386,6 +409,7 @@ void launch_dots(bminres_ctx* h, long long n, const std::vector<Col>& v, Col t, 
     a.cnt = h->dcnt;
     k_dots<<<a.nb, 256, 0, h->stream>>>(a);
     check_launch(h, "k_dots");
+    allred(h, out, a.K, h->stream);
 }
 
 // host-visible dot products (synchronising)
@@ -432,6 +456,7 @@ void launch_colsq(bminres_ctx* h, const double* X, const double* Y, long long n,
     int nb = grid_for(h, n, R * 16, std::min(NB_MAX, 2 * h->n_sm));
     k_colsq<<<nb, 256, 0, h->stream>>>(X, Y, n, p, h->part, nb, out, h->dcnt + 1);
     check_launch(h, "k_colsq");
+    allred(h, out, p, h->stream);
 }
 
 // ------------------------------------------------------------------ block-step launches
@@ -461,6 +486,25 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P);
     if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_reduce: ") + cudaGetErrorString(e));
     h->launches++;
+    if (h->tp) {   // the totals over all ranks (K3b then runs replicated)
+        double* tot = which == 1 ? h->st->red1 : h->st->red2[k & 1];
+        allred(h, tot, which == 1 ? P * P + P : P * P + MAXQ * P, s);
+    }
+}
+
+// Halo exchange of a V slot (world > 1): pack the rows the peers read, land the peers' rows in
+// this slot's halo region [n_loc, n_loc + n_halo).  Every rank calls it at the same points.
+void halo_exchange(bminres_ctx* h, double* V, int p, cudaStream_t s) {
+    if (!h->tp) return;
+    TimeMark tm(h, PH_OTHER);
+    const long long ns = (long long)h->plan.send_rows.size();
+    if (ns > 0) {
+        k_pack_rows<<<grid_for(h, ns * p, 256, 4 * h->n_sm), 256, 0, s>>>(V, h->d_send_rows, ns, p, h->d_sendbuf);
+        check_launch(h, "k_pack_rows");
+    }
+    std::string err;
+    if (!h->tp->exchange(h->d_sendbuf, h->sc_d.data(), V + h->plan.n_loc * p, h->rc_d.data(), s, err))
+        fail(h, BMINRES_ENCCL, err);
 }
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
     const int sk = (int)(k % 3), par = (int)(k & 1);
@@ -486,6 +530,7 @@ void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k, bool wi
         launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
         h->stream = keep;
     }
+    halo_exchange(h, h->V[(sk + 1) % 3], h->p_ws, s);   // V_{k+1} rows the peers' SpMM reads
     if (with_reduce) launch_reduce(h, s, 2, k);
 }
 // side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
@@ -709,6 +754,7 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
                   MAXP * MAXQ * sizeof(double), cudaMemcpyHostToDevice));
     h->hf->need_slow = 0;
     h->slow_blocks++;
+    halo_exchange(h, Wp, p, h->stream);   // the new U_{b+1} rows the peers read
 }
 
 // Finish block b after the column path: its side branch (K3b, K4b).
@@ -732,6 +778,7 @@ std::vector<double> panel_gram(bminres_ctx* h, const double* F, long long n, int
     const int nb = grid_for(h, n, 64, std::min(NB_MAX, 2 * h->n_sm));
     k_gram<<<nb, 256, 0, h->stream>>>(F, n, p, h->part, nb, h->gdev, h->dcnt + 2);
     check_launch(h, "k_gram");
+    allred(h, h->gdev, (long long)p * p, h->stream);
     std::vector<double> G((size_t)p * p);
     CK(cudaMemcpyAsync(G.data(), h->gdev, G.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
@@ -801,15 +848,97 @@ bool retained_live(bminres_ctx* h, long long jfirst) {
     return false;
 }
 
+// ------------------------------------------------------------------ row partition setup
+
+// Build (or reuse) the halo plan of this rank's CSR rows: offsets of all ranks, remote columns by
+// owner, the lists the peers read from this rank (exchanged), the remapped column indices.
+void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, int p) {
+    const int world = h->opt.world, rank = h->opt.rank;
+    const void* key[5] = {A->col_idx, (const void*)(intptr_t)A->nnz, (const void*)(intptr_t)A->row_begin,
+                          (const void*)(intptr_t)A->n_loc, (const void*)(intptr_t)A->n};
+    std::string err;
+    if (!(h->d_lcol && std::equal(key, key + 5, h->plan_key))) {
+        // offsets of every rank: all-to-all of (row_begin, n_loc)
+        std::vector<long long> snd(2 * world), rcv(2 * world), one(world, 2);
+        for (int q = 0; q < world; ++q) {
+            snd[2 * q] = A->row_begin;
+            snd[2 * q + 1] = A->n_loc;
+        }
+        if (!h->tp->alltoallv(snd.data(), one.data(), rcv.data(), one.data(), h->stream, err))
+            fail(h, BMINRES_ENCCL, err);
+        std::vector<long long> off(world + 1, 0);
+        for (int q = 0; q < world; ++q) {
+            if (rcv[2 * q] != off[q]) fail(h, BMINRES_EINVAL, "ranks must own contiguous row blocks in rank order");
+            off[q + 1] = off[q] + rcv[2 * q + 1];
+        }
+        if (off[world] != A->n) fail(h, BMINRES_EINVAL, "the ranks' rows do not cover 0..n-1");
+        std::vector<int> col(std::max<long long>(A->nnz, 1));
+        CK(cudaMemcpy(col.data(), col_dev, A->nnz * sizeof(int), cudaMemcpyDeviceToHost));
+        HaloPlan& pl = h->plan;
+        if (!build_halo_plan(world, rank, off.data(), A->nnz, col.data(), pl))
+            fail(h, BMINRES_EINVAL, "column index outside [0, n)");
+        // tell every owner which of its rows this rank reads
+        std::vector<long long> rq(world, 1), cnt_in(world);
+        if (!h->tp->alltoallv(pl.recv_count.data(), rq.data(), cnt_in.data(), rq.data(), h->stream, err))
+            fail(h, BMINRES_ENCCL, err);
+        pl.send_count = cnt_in;
+        long long ns = 0;
+        for (long long c : cnt_in) ns += c;
+        std::vector<long long> req(std::max<long long>(ns, 1));
+        if (!h->tp->alltoallv(pl.halo_rows.data(), pl.recv_count.data(), req.data(), pl.send_count.data(), h->stream,
+                              err))
+            fail(h, BMINRES_ENCCL, err);
+        pl.send_rows.assign(req.begin(), req.begin() + ns);
+        for (auto& r : pl.send_rows) {
+            r -= A->row_begin;
+            if (r < 0 || r >= A->n_loc) fail(h, BMINRES_EINVAL, "halo request outside this rank's rows");
+        }
+        if (h->lcol_cap < (size_t)std::max<long long>(A->nnz, 1)) {
+            dalloc(h, &h->d_lcol, std::max<long long>(A->nnz, 1));
+            h->lcol_cap = std::max<long long>(A->nnz, 1);
+        }
+        CK(cudaMemcpy(h->d_lcol, pl.local_col.data(), A->nnz * sizeof(int), cudaMemcpyHostToDevice));
+        if (h->send_cap < (size_t)std::max<long long>(ns, 1)) {
+            dalloc(h, &h->d_send_rows, std::max<long long>(ns, 1));
+            h->send_cap = std::max<long long>(ns, 1);
+        }
+        CK(cudaMemcpy(h->d_send_rows, pl.send_rows.data(), ns * sizeof(long long), cudaMemcpyHostToDevice));
+        std::copy(key, key + 5, h->plan_key);
+    }
+    const long long ns = (long long)h->plan.send_rows.size();
+    if (h->sendbuf_cap < (size_t)std::max<long long>(ns * p, 1)) {
+        dalloc(h, &h->d_sendbuf, std::max<long long>(ns * p, 1));
+        h->sendbuf_cap = std::max<long long>(ns * p, 1);
+    }
+    h->sc_d.assign(world, 0);
+    h->rc_d.assign(world, 0);
+    for (int q = 0; q < world; ++q) {
+        h->sc_d[q] = h->plan.send_count[q] * p;
+        h->rc_d[q] = h->plan.recv_count[q] * p;
+    }
+    h->n_ext = A->n_loc + h->plan.n_halo;
+}
+
+// Y = A X for the local rows with X extended by its halo (world > 1): X's local rows are copied
+// into the scratch slot Vs, the halo exchanged, and the SpMM gathers from Vs.
+const double* extended_input(bminres_ctx* h, const double* X, long long n, int p, double* Vs) {
+    if (!h->tp) return X;
+    CK(cudaMemcpyAsync(Vs, X, (size_t)n * p * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    halo_exchange(h, Vs, p, h->stream);
+    return Vs;
+}
+
 // ------------------------------------------------------------------ the solve
 
 int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xin, int p, double tol, long long maxit,
              double tau) {
     const bminres_options& o = h->opt;
     if (!A || !Bin || !Xin) fail(h, BMINRES_EINVAL, "null argument");
-    if (o.world != 1) fail(h, BMINRES_EINVAL, "world > 1 is not implemented in this version");
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world) fail(h, BMINRES_EINVAL, "rank / world out of range");
+    if (o.world > 1 && !h->tp) fail(h, BMINRES_EINVAL, "world > 1 needs a transport (bminres_init_nccl / callbacks)");
     const long long n = A->n_loc;
-    if (A->n != A->n_loc || A->row_begin != 0) fail(h, BMINRES_EINVAL, "world = 1 needs n_loc = n, row_begin = 0");
+    if (o.world == 1 && (A->n != A->n_loc || A->row_begin != 0))
+        fail(h, BMINRES_EINVAL, "world = 1 needs n_loc = n, row_begin = 0");
     if (p < 1 || p > BMINRES_MAX_P || !kfn_for(p, &h->kf, o.pool_size)) fail(h, BMINRES_EINVAL, "unsupported block size p");
     if (n < p) fail(h, BMINRES_EINVAL, "n < p");
     if (!std::isfinite(tol) || tol < 0 || maxit < 0 || !std::isfinite(tau) || tau < 0)
@@ -883,6 +1012,12 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         }
         if ((((uintptr_t)Bin) | ((uintptr_t)sp.X)) & 15) fail(h, BMINRES_EINVAL, "B and X must be 16-byte aligned");
     }
+    if (h->tp) {   // (a transport at world = 1 runs the same path with an empty halo)
+        setup_partition(h, A, sp.col, p);   // halo plan; the SpMM reads the remapped columns
+        sp.col = h->d_lcol;
+    } else {
+        h->n_ext = n;
+    }
     ensure_workspace(h, n, p, q);
     const double* B = Bin;
 
@@ -952,7 +1087,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // F0 = B - A X0 (C6) into the V slot of block 1 (U_1 = V_1, Tr_1 = I)
         double* F = h->V[1];
         if (o.use_x0) {
-            K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, F, n, h->st, nullptr, 0, 0, h->tpw};
+            const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);
+            K1Args a{sp.rowptr, sp.col, sp.val, Xe, nullptr, F, n, h->st, nullptr, 0, 0, h->tpw};
             h->kf.k1plain<<<h->nb4, NT, 0, h->stream>>>(a);
             check_launch(h, "k1_spmm(plain)");
             k_sub_from<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(B, F, (long long)panel);
@@ -1047,6 +1183,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         finished = true;
     }
     CK(cudaMemcpyAsync(h->st, &init, sizeof(DevState), cudaMemcpyHostToDevice, h->stream));
+    halo_exchange(h, h->V[1], p, h->stream);   // U_1 rows the peers' first SpMM reads
     if (hist_cap) CK(cudaMemcpyAsync(h->hist, h0.data(), p * sizeof(double), cudaMemcpyHostToDevice, h->stream));
     h->hf->side_done = finished ? 1 : 0;
     h->hf->status = init.status;
@@ -1058,7 +1195,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     CK(cudaStreamSynchronize(h->stream));
 
     // ---- block loop
-    const bool graphs = o.use_graphs && !o.timing;
+    const bool graphs = o.use_graphs && !o.timing && (!h->tp || h->tp->capturable());
     // timing mode of a fused kernel set: the graph's launches issued explicitly, in the graph's
     // order, with an event pair around each (the kernels the product runs, timed one by one)
     const bool fused_expl = o.timing && h->kf.fused;
@@ -1146,7 +1283,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
     {
         TimeMark tm(h, PH_RESID);
-        K1Args a{sp.rowptr, sp.col, sp.val, sp.X, nullptr, h->M[0], n, h->st, nullptr, 0, 0, h->tpw};
+        const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);   // (V slots are free now)
+        K1Args a{sp.rowptr, sp.col, sp.val, Xe, nullptr, h->M[0], n, h->st, nullptr, 0, 0, h->tpw};
         h->kf.k1plain<<<h->nb4, NT, 0, h->stream>>>(a);
         check_launch(h, "k1_spmm(plain)");
         launch_colsq(h, B, h->M[0], n, p, h->dsc);
@@ -1362,6 +1500,65 @@ size_t bminres_workspace_bytes(int64_t n_loc, int32_t p, int32_t pool_size) {
            sizeof(double) * (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8) + sizeof(DevState);
 }
 
+int bminres_get_unique_id(uint8_t out[128]) {
+    if (!out) return BMINRES_EINVAL;
+    std::string err;
+    NcclApi& a = nccl_api();
+    if (!a.load(err)) {
+        g_create_err = err;
+        return BMINRES_ENCCL;
+    }
+    const int r = a.getUniqueId(out);
+    if (r != 0) {
+        g_create_err = "ncclGetUniqueId failed";
+        return BMINRES_ENCCL;
+    }
+    return BMINRES_OK;
+}
+
+int bminres_init_nccl(bminres_handle h, const uint8_t id[128]) {
+    if (!h || !id) return BMINRES_EINVAL;
+    if (h->opt.world < 1 || h->opt.rank < 0 || h->opt.rank >= h->opt.world) return BMINRES_EINVAL;
+    cudaSetDevice(h->device);
+    auto* t = new NcclTransport();
+    std::string err;
+    if (!t->init(id, h->opt.rank, h->opt.world, err)) {
+        delete t;
+        h->err = err;
+        return BMINRES_ENCCL;
+    }
+    delete h->tp;
+    h->tp = t;
+    return BMINRES_OK;
+}
+
+int bminres_set_comm_callbacks(bminres_handle h, const bminres_comm_callbacks* cb) {
+    if (!h || !cb || !cb->allreduce || !cb->alltoallv || !cb->exchange) return BMINRES_EINVAL;
+    auto* t = new CallbackTransport();
+    t->cb = *cb;
+    t->rank = h->opt.rank;
+    t->world = h->opt.world;
+    delete h->tp;
+    h->tp = t;
+    return BMINRES_OK;
+}
+
+int bminres_halo_plan(int32_t world, int32_t rank, const int64_t* offsets, int64_t nnz, const int32_t* col_idx,
+                      int32_t* local_col, int64_t* halo_rows, int64_t* n_halo, int64_t* halo_count) {
+    if (world < 1 || rank < 0 || rank >= world || !offsets || nnz < 0 || (nnz > 0 && !col_idx) || !n_halo)
+        return BMINRES_EINVAL;
+    for (int q = 0; q < world; ++q)
+        if (offsets[q + 1] < offsets[q]) return BMINRES_EINVAL;
+    HaloPlan pl;
+    if (!build_halo_plan(world, rank, reinterpret_cast<const long long*>(offsets), nnz, col_idx, pl))
+        return BMINRES_EINVAL;
+    *n_halo = pl.n_halo;
+    if (local_col) std::copy(pl.local_col.begin(), pl.local_col.end(), local_col);
+    if (halo_rows) std::copy(pl.halo_rows.begin(), pl.halo_rows.end(), halo_rows);
+    if (halo_count) std::copy(pl.recv_count.begin(), pl.recv_count.end(), halo_count);
+    return BMINRES_OK;
+}
+
 const char* bminres_last_error(bminres_handle h) {
     if (!h) return g_create_err.c_str();
     return h->err.c_str();
@@ -1377,6 +1574,10 @@ void bminres_destroy(bminres_handle h) {
         if (p) cudaFree(p);
     if (h->trace) cudaFree(h->trace);
     if (h->trace_tick) cudaFree(h->trace_tick);
+    if (h->d_lcol) cudaFree(h->d_lcol);
+    if (h->d_send_rows) cudaFree(h->d_send_rows);
+    if (h->d_sendbuf) cudaFree(h->d_sendbuf);
+    delete h->tp;
     if (h->a_rowptr) cudaFree(h->a_rowptr);
     if (h->a_col) cudaFree(h->a_col);
     if (h->dcnt) cudaFree(h->dcnt);

@@ -33,13 +33,14 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     from paper_1301_2102_b200 import binding
     c = tmp_path / "sz.c"
-    c.write_text('#include <stdio.h>\n#include "bminres.h"\nint main(){printf("%zu %zu %zu %zu\\n",'
-                 'sizeof(bminres_options), sizeof(bminres_stats_t), sizeof(bminres_event), sizeof(bminres_csr));}\n')
+    c.write_text('#include <stdio.h>\n#include "bminres.h"\nint main(){printf("%zu %zu %zu %zu %zu\\n",'
+                 'sizeof(bminres_options), sizeof(bminres_stats_t), sizeof(bminres_event), sizeof(bminres_csr),'
+                 'sizeof(bminres_comm_callbacks));}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
     got = subprocess.check_output([str(exe)]).decode().split()
     want = [ctypes.sizeof(binding.Options), ctypes.sizeof(binding.Stats), ctypes.sizeof(binding.Event),
-            ctypes.sizeof(binding.CsrStruct)]
+            ctypes.sizeof(binding.CsrStruct), ctypes.sizeof(binding.CommCallbacks)]
     assert [int(x) for x in got] == want
 
 
