@@ -9,13 +9,15 @@ Gaussian B from seed 0), synthetic, fp64.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
 
-`value`   = banded iterations of all ranks / max-over-ranks device time (CUDA events).
+`value`   = banded iterations of the solve / max-over-ranks device time (CUDA events).
 `e2e`     = the same metric through the C ABI with HOST buffers (A, B in; X out).
 `roofline`= the dominant kernel's algorithmic bytes per launch / its mean launch time
             (CUDA events around every launch inside the timed region) vs MEASURED_PEAKS.
 `cpu_baseline` = the C oracle (tests' reference implementation) on a bounded sample.
-With N > 1 (torchrun) every rank solves its own replica (weak scaling; the row-partitioned
-path is not implemented in this version — DESIGN.md "Multi-GPU").
+With N > 1 (torchrun) the ranks run ONE solve of the workload with the rows partitioned over
+them (halo exchange + allreduces over NCCL; strong scaling).  Testing
+aids: BENCH_BACKEND=gloo + BENCH_COMM=gloo run the same path with the host-callback transport
+(e.g. two ranks sharing one GPU).
 """
 from __future__ import annotations
 
@@ -161,7 +163,7 @@ def run_reference(args):
     value = total / dt
     line = {"impl": "reference", "metric": "block-MINRES iterations/s (fp64)", "value": value,
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": P.name, "n": P.n, "p": P.p, "iters_per_step": iters},
             "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": 1, "kind": "oracle",
@@ -174,24 +176,36 @@ def run_reference(args):
 def run_ours(args):
     import torch
     world, rank, local = dist_init()
+    local = local % max(1, torch.cuda.device_count())   # (ranks may share a GPU when testing)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1301_2102_b200 import DeviceCsr, Solver
 
     P = problem(args.config)
     n, p = P.n, P.p
-    A = DeviceCsr.from_host(P.A, dev)
-    B = torch.from_numpy(P.B).to(dev)
+    # N > 1: one solve of the workload, rows partitioned over the ranks (halo exchange and
+    # allreduces over NCCL) -- strong scaling
+    off = [n * q // world for q in range(world + 1)]
+    r0, r1 = off[rank], off[rank + 1]
+    A = DeviceCsr.from_host(P.A, dev) if world == 1 else DeviceCsr.rows_from_host(P.A, r0, r1, dev)
+    Bh_full = np.ascontiguousarray(P.B[r0:r1])
+    B = torch.from_numpy(Bh_full).to(dev)
     X = torch.zeros_like(B)
+    comm = None
+    if world > 1:
+        from paper_1301_2102_b200 import TorchComm
+        comm = TorchComm() if os.environ.get("BENCH_COMM", "nccl") == "gloo" else "nccl"
+    n_loc = r1 - r0
     stream = torch.cuda.Stream(device=dev)
     iters = args.iters
     peak, peak_kind = load_peaks()
-    abytes = 12.0 * P.A.nnz + 4.0 * (n + 1)
-    panel = 8.0 * n * p
+    nnz_loc = int(P.A.indptr[r1]) - int(P.A.indptr[r0])
+    abytes = 12.0 * nnz_loc + 4.0 * (n_loc + 1)   # this rank's CSR rows
+    panel = 8.0 * n_loc * p
 
     # ---- timed region: the product's launch mode (CUDA graphs, main/side branches overlapped)
     solver = Solver(local, pool_size=1, use_graphs=not args.no_graphs, timing=False, record_history=False,
-                    stream=stream.cuda_stream)
+                    stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
 
     def step(s):
         return s.solve(A, B, X, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
@@ -219,7 +233,7 @@ def run_ours(args):
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms, world, dev)
-    value = total_iters * world / (ms_max / 1e3)
+    value = total_iters / (ms_max / 1e3)   # iterations of the (one, partitioned) solve per second
     solver.close()
 
     # ---- kernel-timing region: the same steps with a CUDA event pair around every kernel
@@ -227,7 +241,7 @@ def run_ours(args):
     roof = None
     if not args.no_kernel_timing:
         st_t = Solver(local, pool_size=1, use_graphs=False, timing=True, record_history=False,
-                      stream=stream.cuda_stream)
+                      stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
         step(st_t)
         phase_ms, phase_n = {}, {}
         for _ in range(args.steps):
@@ -267,22 +281,24 @@ def run_ours(args):
     # end to end through the C ABI with host buffers (pinned B and X; A from host arrays)
     e2e = None
     if not args.no_e2e:
-        Bh = torch.from_numpy(P.B).pin_memory()
+        from paper_1301_2102_b200 import HostCsrRows
+        Ahost = P.A if world == 1 else HostCsrRows.from_host(P.A, r0, r1)
+        Bh = torch.from_numpy(Bh_full).pin_memory()
         Xh = torch.zeros_like(Bh).pin_memory()
         s2 = Solver(local, pool_size=1, use_graphs=True, timing=False, record_history=False,
-                    stream=stream.cuda_stream)
-        s2.solve(P.A, Bh, Xh, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
+                    stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
+        s2.solve(Ahost, Bh, Xh, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
         e_iters = 0
         for _ in range(args.steps):
-            r = s2.solve(P.A, Bh, Xh, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
+            r = s2.solve(Ahost, Bh, Xh, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
             e_iters += r.iterations
         dt = time.perf_counter() - t0
         dt = max_over_ranks(dt, world, dev)
         s2.close()
-        e2e = {"value": e_iters * world / dt, "unit": "iterations/s",
+        e2e = {"value": e_iters / dt, "unit": "iterations/s",
                "h2d_bytes_per_step": int(abytes + panel), "d2h_bytes_per_step": int(panel)}
 
     cpu = None
@@ -292,14 +308,17 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": "block-MINRES iterations/s (fp64)", "value": value, "unit": "iterations/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": P.name, "n": n, "p": p, "nnz": P.A.nnz, "iters_per_step": iters,
                            "tol": P.tol, "deflation_tol": P.tau, "pool_size": 1,
                            "l2": "inputs larger than L2 (working set per block step "
                                  f"{blk_bytes / 1e6:.0f} MB > 126 MB L2); no flush",
-                           "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                           "launch_mode": "plain launches" if args.no_graphs else "CUDA graphs (main/side branches)"},
+                           "parallelism": (f"row-partitioned x{world} (halo + allreduce over "
+                                           f"{'NCCL' if comm == 'nccl' else 'host callbacks, testing'})")
+                           if world > 1 else "single GPU",
+                           "launch_mode": "plain launches" if (args.no_graphs or (world > 1 and comm != "nccl"))
+                           else "CUDA graphs (main/side branches)"},
                 "gpu_launches": launches, "slow_blocks": slow,
                 "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "hbm_peak_GBps": peak}

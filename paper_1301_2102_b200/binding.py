@@ -159,6 +159,26 @@ class DeviceCsr:
                    row_begin, int(A.n))
 
 
+@dataclass
+class HostCsrRows:
+    """Rows [row_begin, row_begin + n) of an n_global x n_global host CSR (global columns):
+    the host-memory form of one rank's rows (the library stages them)."""
+    n: int
+    indptr: np.ndarray
+    indices: np.ndarray
+    data: np.ndarray
+    row_begin: int
+    n_global: int
+
+    @classmethod
+    def from_host(cls, A, row_begin: int, row_end: int):
+        ip = np.asarray(A.indptr, dtype=np.int64)
+        k0, k1 = int(ip[row_begin]), int(ip[row_end])
+        return cls(row_end - row_begin, (ip[row_begin:row_end + 1] - k0).astype(np.int32),
+                   np.ascontiguousarray(A.indices[k0:k1], dtype=np.int32),
+                   np.ascontiguousarray(A.data[k0:k1], dtype=np.float64), row_begin, int(A.n))
+
+
 def _csr_struct(A) -> CsrStruct:
     s = CsrStruct()
     if isinstance(A, DeviceCsr):
@@ -175,6 +195,8 @@ def _csr_struct(A) -> CsrStruct:
         s.row_ptr, s.col_idx, s.values = ip.ctypes.data, ix.ctypes.data, dv.ctypes.data
         keep = (ip, ix, dv)
     s.row_begin, s.n_loc = 0, s.n
+    if isinstance(A, HostCsrRows):
+        s.row_begin, s.n_loc, s.n = A.row_begin, A.n, A.n_global
     s._keep = keep
     return s
 
