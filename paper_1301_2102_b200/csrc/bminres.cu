@@ -1186,6 +1186,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     halo_exchange(h, h->V[1], p, h->stream);   // U_1 rows the peers' first SpMM reads
     if (hist_cap) CK(cudaMemcpyAsync(h->hist, h0.data(), p * sizeof(double), cudaMemcpyHostToDevice, h->stream));
     h->hf->side_done = finished ? 1 : 0;
+    h->hf->stop_blk = KINF;
     h->hf->status = init.status;
     h->hf->need_slow = 0;
     h->hf->bd_at = KINF;
@@ -1241,6 +1242,10 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // update of block s-1; updates of blocks < b were applied explicitly)
         if (h->kf.fused) SET_STATE(h, k_upd_min, b);
         long long launched = 0;
+        // The host stops launching on a stop / breakdown seen in a graph it has synchronised
+        // with, i.e. of a block <= the last side block of graph `launched - LAG`: the decision
+        // depends only on completed graphs, so every rank of a partitioned solve launches the
+        // same graphs (their collectives match).
         for (long long s = b; s <= nblocks && graphs; s += GB) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
             h->launches += GB * (h->kf.fused ? 5 : 6);
@@ -1248,7 +1253,10 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             launched++;
             if (launched >= LAG) {
                 CK(cudaEventSynchronize(lag_ev[launched % LAG]));
-                if (h->hf->side_done || h->hf->need_slow) break;
+                const long long done_last = b + (launched - LAG + 1) * GB - 1;   // last side block synced
+                if ((h->hf->side_done && h->hf->stop_blk <= done_last) ||
+                    (h->hf->need_slow && h->hf->bd_at <= done_last))
+                    break;
             }
         }
         for (long long s = b; s <= nblocks && !graphs; ++s) {   // fused_expl (timing mode)

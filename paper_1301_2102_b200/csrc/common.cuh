@@ -55,6 +55,7 @@ struct HostFlags {
     volatile long long j_done;
     volatile long long k_side;
     volatile long long k_main;
+    volatile long long stop_blk;   // the block whose K3b ended the solve (side_done)
 };
 
 // Device-resident solver state.  p x p matrices are row-major [a*MAXP + b].

@@ -728,7 +728,10 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         st->hflags->status = status;
         st->hflags->j_done = jd;
         st->hflags->k_side = st->k_side;
-        if (end) st->hflags->side_done = 1;
+        if (end) {
+            st->hflags->stop_blk = k;
+            st->hflags->side_done = 1;
+        }
         __threadfence_system();
     }
     trace_pt(tr, 5);
