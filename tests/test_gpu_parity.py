@@ -272,3 +272,36 @@ def test_invalid_arguments():
     P = synth.config("1c")
     assert gpu_solve(P.A, np.ones((P.n, 9)), tol=1e-8, maxit=10).status_name == "EINVAL"  # p = 9 not compiled
     assert gpu_solve(P.A, P.B, tol=float("nan"), maxit=10).status_name == "EINVAL"
+
+
+# ----------------------------------------------------------------------------- configs 4 and 5 at full size
+
+
+def _p6_closed_form(A, B, jmax):
+    """Pin P6: for j <= p (no step-0 deflation) X_j lies in span(B(:, 1..j)), so column i's
+    relative residual is min_y ||b_i - A B(:,1:j) y|| / ||b_i|| (a tall-skinny least squares)."""
+    import scipy.sparse as sp
+    S = sp.csr_matrix((A.data, A.indices, A.indptr), shape=(A.n, A.n))
+    AB = np.asarray(S @ B[:, :jmax])
+    beta2 = np.einsum("ij,ij->j", B, B)
+    out = []
+    for j in range(1, jmax + 1):
+        Q, _ = np.linalg.qr(AB[:, :j])
+        proj = Q.T @ B
+        out.append(np.sqrt(np.maximum(beta2 - np.einsum("ij,ij->j", proj, proj), 0.0) / beta2))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_config_closed_form_and_invariants(cfg):
+    """Configs 4 (3-D 256^3, p = 32, n = 16.8M) and 5 (unstructured, n = 4.19M, p = 16) at full
+    size: iterations 1..4 against the P6 closed form, monotone histories (P3), and the computed
+    residual equal to the true residual (P4) after 200 iterations."""
+    P = synth.config(cfg)
+    r = gpu_solve(P.A, P.B, tol=0.0, maxit=200, deflation_tol=P.tau)
+    assert r.iterations == 200 and r.status_name == "MAXIT"
+    ref = _p6_closed_form(P.A, P.B, 4)
+    np.testing.assert_allclose(r.history[1:5], ref, rtol=1e-9, atol=1e-14)
+    h = r.history
+    assert np.all(h[1:] <= h[:-1] * (1 + 1e-12) + 1e-15), "residual histories must not increase (P3)"
+    np.testing.assert_allclose(r.stats["comp_res"], r.stats["true_res"], rtol=0, atol=1e-8)
