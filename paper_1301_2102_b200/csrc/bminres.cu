@@ -67,10 +67,10 @@ Kfn make_kfn(int q) {
             f.k1 = k1_dmma<P>;
             f.fused = getenv("BMINRES_NO_FUSE") == nullptr;
             f.smem1 = K1DSmem<P>::bytes;
-            f.nt1 = 256;
+            f.nt1 = K1DSmem<P>::WARPS * 32;
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
-            f.nt2 = 128;
+            f.nt2 = K2DSmem<P>::WARPS * 32;
         }
         f.k4b = k4b_dmma<P>;
         f.smem4b = K4bDSmem<P>::bytes;

@@ -308,8 +308,21 @@ __global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par
     const double* part = which == 1 ? st->part1 : st->part2[par];
     double* out = which == 1 ? st->red1 : st->red2[par];
     if (e >= E) return;
+    // all of a lane's rows are loaded before the first add (one L2 round trip, not ncl/32);
+    // the sum order is unchanged: b = lane, lane + 32, ... then the fixed shuffle tree
+    constexpr int U = 8;   // rows per lane in flight (ncl <= 256 in one round: cluster size >= 2)
     double s = 0.0;
-    for (int b = lane; b < ncl; b += 32) s += __ldcg(part + (size_t)b * E + e);
+    for (int b0 = 0; b0 < ncl; b0 += 32 * U) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int b = b0 + lane + 32 * u;
+            v[u] = b < ncl ? __ldcg(part + (size_t)b * E + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (b0 + lane + 32 * u < ncl) s += v[u];
+    }
     s = warp_sum(s);
     if (lane == 0) out[e] = s;
     trace_pt(tr, 5);
@@ -477,9 +490,10 @@ __device__ __forceinline__ void store_pp(double* dst, const double* src) {
     for (int t = threadIdx.x; t < P * P; t += blockDim.x) dst[(t / P) * MAXP + t % P] = src[t];
 }
 
-// Scratch (doubles) the K1 / K2 prologues need.
+// Scratch (doubles) the K1 / K2 prologues need: K1's is the largest -- totals (P*P + MAXQ*P),
+// C, C^{-1}, Tr_{k-1} (3 P*P), pool coefficients (P*MAXQ), ||A u_j||^2 (P).
 template <int P>
-__host__ __device__ constexpr int prologue_scratch() { return (P * P + MAXQ * P) + 6 * P * P + P * MAXQ + P; }
+__host__ __device__ constexpr int prologue_scratch() { return (P * P + MAXQ * P) + 3 * P * P + P * MAXQ + P; }
 
 // K1 prologue, block k: C_{k-1}, Tr_k = C_{k-1}^{-1}, coef_{k-1} from K2(k-1)'s partials (or the
 // host's values after the column path), and D = Tr_{k-1} C_{k-1}^T.  Writes sTk and sD (P x P,

@@ -200,17 +200,18 @@ __device__ __forceinline__ void frag_acc(double* sAcc, int base, int ld, int m0,
 
 template <int P>
 struct K2DSmem {
-    static constexpr int WARPS = 4;
+    static constexpr int WARPS = P >= 16 ? 8 : 4;   // large p: more warps to hide the DMMA chains
+    static constexpr int NS = P >= 32 ? 2 : NSTAGE;  // cp.async stages (shared-memory budget)
     static constexpr int RSQ = 12;                        // pool tile row stride (8 columns + pad)
     static constexpr int TQ = DM<P>::TR * RSQ;
-    static constexpr int pipe = WARPS * NSTAGE * (2 * DM<P>::TILE + TQ);
+    static constexpr int pipe = WARPS * NS * (2 * DM<P>::TILE + TQ);
     static constexpr int LD = P + 1;
-    static constexpr int tail = 4 * P * P + prologue_scratch<P>();
+    static constexpr int tail = 5 * P * P + P * MAXQ + P;   // sGs, sTk, sX, sG, sCo, k2_prologue (P*P + P)
     static constexpr size_t bytes = sizeof(double) * (DM<P>::FR + DM<P>::KC * 32 + pipe + P * P + MAXQ * P + tail);
 };
 
 template <int P>
-__global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
+__global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
     using D = DM<P>;
     using S = K2DSmem<P>;
     constexpr int WARPS = S::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR, RSQ = S::RSQ;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
     double* pipe = fF + KC * 32;
     double* sAcc = pipe + S::pipe;
     double* sTail = sAcc + P * P + MAXQ * P;
-    double* wb = pipe + warp * NSTAGE * (2 * D::TILE + S::TQ);
+    double* wb = pipe + warp * S::NS * (2 * D::TILE + S::TQ);
     const long long ntiles = (a.n + TR - 1) / TR;
     const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
     auto issue = [&](long long it, int slot) {
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
     // the first stages stream in during the wait and the prologue (K1 completed before
     // reduce1 started; only the totals come from reduce1)
 #pragma unroll
-    for (int s = 0; s < NSTAGE - 1; ++s) issue(s, s);
+    for (int s = 0; s < S::NS - 1; ++s) issue(s, s);
     pdl_wait();   // red1 (reduce1) is ready
     {
         // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
@@ -289,10 +290,10 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
         for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
     }
     for (long long it = 0; t0 + it * ts < ntiles; ++it) {
-        issue(it + NSTAGE - 1, (int)((it + NSTAGE - 1) % NSTAGE));
-        cp_wait<NSTAGE - 1>();
+        issue(it + S::NS - 1, (int)((it + S::NS - 1) % S::NS));
+        cp_wait<S::NS - 1>();
         __syncwarp();
-        double* sl = wb + (int)(it % NSTAGE) * (2 * D::TILE + S::TQ);
+        double* sl = wb + (int)(it % S::NS) * (2 * D::TILE + S::TQ);
         double* tW = sl;
         const double* tV = sl + D::TILE;
         double* tR = sl + 2 * D::TILE;
@@ -379,8 +380,10 @@ __global__ void __launch_bounds__(128) k2_dmma(K2Args a) {
 
 template <int P>
 struct K1DSmem {
-    static constexpr int WARPS = 8;
-    static constexpr int UNS = 2;                            // cp.async stages of the fused update
+    // p = 32: one 512-thread CTA per SM (16 warps, <= 128 registers) instead of one 256-thread
+    // CTA at 209 registers -- the gathers need the warps; the fused update single-staged
+    static constexpr int WARPS = P >= 32 ? 16 : 8;
+    static constexpr int UNS = P >= 32 ? 1 : 2;              // cp.async stages of the fused update
     static constexpr int pipe = WARPS * 3 * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile per warp
     static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
     static constexpr int upd = UpdSmem<P, WARPS, UNS>::doubles;   // the update runs first, then the SpMM
@@ -398,7 +401,7 @@ struct K1DSmem {
 // q+2 are loaded.  The SpMM of the warp's first tile runs before the prologue (the Cholesky of
 // the previous block's Gram), which only the epilogue needs.
 template <int P>
-__global__ void __launch_bounds__(256, P <= 8 ? 2 : 1) k1_dmma(K1Args a) {
+__global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dmma(K1Args a) {
     using D = DM<P>;
     using C = PC<P>;
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
