@@ -28,7 +28,7 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_sb"),
     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier"),
 ]
-KNAMES = {"k1_spmm": "spmm", "k2_orth": "orth", "k3b_smallqr": "smallqr", "k4a_basis": "basis",
+KNAMES = {"k1_dmma": "spmm_fused", "k2_row": "orth", "k2_dmma": "orth", "k_reduce": "reduce", "k1_spmm": "spmm", "k2_orth": "orth", "k3b_smallqr": "smallqr", "k4a_basis": "basis",
           "k4b_update": "update", "k3_smallqr": "smallqr", "k4_update": "update"}
 
 
