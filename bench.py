@@ -36,8 +36,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # algorithmic panel transfers per launch; K1 also streams CSR A
-PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 9, "orth": 3, "update": 6}
-PHASE_READS_A = {"spmm", "spmm_fused"}
+PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 9, "orth": 3, "update": 6,
+                      # split mode (large panels): K1a reads V_k once (gathers) and writes AV; K1 then
+                      # streams AV, V_k, V_{k-1} and writes W (+ the 6 panels of the fused update)
+                      "spmm_av": 2, "epilogue": 4, "epilogue_fused": 10}
+PHASE_READS_A = {"spmm", "spmm_fused", "spmm_av"}
 
 
 def load_peaks():
@@ -262,8 +265,8 @@ def run_ours(args):
                 traffic = json.load(open(tpath)).get(f"{P.name}:{dom}")
             except Exception:
                 traffic = None
-        step_ms = sum(phase_ms[k] for k in ("spmm", "spmm_fused", "orth", "smallqr", "update", "reduce")
-                      if k in phase_ms)
+        step_ms = sum(phase_ms[k] for k in ("spmm", "spmm_fused", "orth", "smallqr", "update", "reduce", "spmm_av",
+                                            "epilogue", "epilogue_fused") if k in phase_ms)
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "bytes_per_launch": bytes_launch, "mean_launch_us": per_launch_ms * 1e3,

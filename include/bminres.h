@@ -77,7 +77,10 @@ typedef struct {
     int32_t record_history;  /* 1: keep (iterations+1) x p computed relative residuals */
     int32_t use_graphs;      /* 1: replay each block step as a CUDA graph (default); 0: plain launches */
     int32_t timing;          /* 1: CUDA events around every kernel launch, per-phase totals in stats */
-    int32_t reserved[7];
+    int32_t split_spmm;      /* p in {8,16,32}: 0 auto (split when the n x p panel is >= 128 MB), 1 always,
+                                2 never.  Split: the SpMM A V_k runs alone at full occupancy (K1a) and K1
+                                streams its result; same arithmetic, bitwise */
+    int32_t reserved[6];
 } bminres_options;
 
 /* One dependence event: candidate h_{j+p,j} <= gamma * ||A u_j||. */
@@ -90,8 +93,10 @@ typedef struct {
     double ratio;    /* h / omega */
 } bminres_event;
 
-#define BMINRES_NPHASE 10  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
-                              reduce (k_reduce), spmm_fused (K1 with the M/X update of block k-2) */
+#define BMINRES_NPHASE 13  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
+                              reduce (k_reduce), spmm_fused (K1 with the M/X update of block k-2),
+                              split mode (large panels): spmm_av (K1a, A V_k alone), epilogue (K1 streaming
+                              A V_k), epilogue_fused (the same with the M/X update of block k-2) */
 
 typedef struct {
     int32_t status;           /* return code of the last solve */

@@ -15,8 +15,9 @@ import numpy as np
 from . import _build
 
 MAX_P = 32
-NPHASE = 10
-PHASES = ["spmm", "orth", "smallqr", "update", "slowpath", "start", "resid", "other", "reduce", "spmm_fused"]
+NPHASE = 13
+PHASES = ["spmm", "orth", "smallqr", "update", "slowpath", "start", "resid", "other", "reduce", "spmm_fused",
+          "spmm_av", "epilogue", "epilogue_fused"]
 STATUS = {0: "OK", 1: "MAXIT", -1: "EINVAL", -2: "ECUDA", -3: "ENCCL", -4: "ENOMEM", -5: "EPOOL",
           -6: "ESINGULAR_R"}
 SUPPORTED_P = (1, 2, 3, 4, 5, 6, 7, 8, 16, 32)
@@ -30,7 +31,7 @@ class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("stream", C.c_void_p),
                 ("seed", C.c_uint64), ("pool_size", C.c_int32), ("use_x0", C.c_int32),
                 ("record_history", C.c_int32), ("use_graphs", C.c_int32), ("timing", C.c_int32),
-                ("reserved", C.c_int32 * 7)]
+                ("split_spmm", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 class CsrStruct(C.Structure):
@@ -319,11 +320,12 @@ class Solver:
 
     def __init__(self, device: int = 0, *, pool_size: int = 1, seed: int = 0, use_graphs: bool = True,
                  timing: bool = False, record_history: bool = True, use_x0: bool = False, stream=None,
-                 rank: int = 0, world: int = 1, comm=None):
+                 rank: int = 0, world: int = 1, comm=None, split_spmm: int = 0):
         L = lib()
         o = Options()
         L.bminres_default_options(C.byref(o))
         o.device, o.pool_size, o.seed = device, pool_size, seed
+        o.split_spmm = split_spmm
         o.use_graphs, o.timing, o.record_history, o.use_x0 = int(use_graphs), int(timing), int(record_history), int(use_x0)
         o.stream = stream
         o.rank, o.world = rank, world

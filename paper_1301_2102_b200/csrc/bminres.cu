@@ -32,7 +32,7 @@ using namespace bmr;
 namespace {
 
 enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER, PH_REDUCE,
-             PH_SPMM_FUSED };
+             PH_SPMM_FUSED, PH_SPMM_AV, PH_EPI, PH_EPI_FUSED };
 
 struct Retained {
     double* v;
@@ -42,6 +42,9 @@ struct Retained {
 struct Kfn {  // per-p kernel table
     void (*k1)(K1Args);
     void (*k1plain)(K1Args);
+    void (*k1a)(K1Args);     // split mode: the SpMM alone (null: no split kernels for this p)
+    void (*k1pre)(K1Args);   // split mode: K1 streaming A V_k
+    size_t smem1pre;
     void (*k2)(K2Args);
     void (*k3b)(DevState*);
     void (*k4b)(K4bArgs);
@@ -54,6 +57,9 @@ template <int P>
 Kfn make_kfn(int q) {
     Kfn f;
     f.fused = false;
+    f.k1a = nullptr;
+    f.k1pre = nullptr;
+    f.smem1pre = 0;
     f.k1 = k1_spmm<P, true>;
     f.nt1 = NT;
     f.smem1 = K1Smem<P>::bytes;
@@ -68,6 +74,9 @@ Kfn make_kfn(int q) {
             f.fused = getenv("BMINRES_NO_FUSE") == nullptr;
             f.smem1 = K1DSmem<P>::bytes;
             f.nt1 = K1DSmem<P>::WARPS * 32;
+            f.k1a = k1a_spmm<P>;
+            f.k1pre = k1_dmma<P, true>;
+            f.smem1pre = K1DSmem<P, true>::bytes;
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
             f.nt2 = K2DSmem<P>::WARPS * 32;
@@ -163,6 +172,10 @@ struct bminres_ctx {
     size_t ev_used = 0;
     std::vector<std::pair<int, size_t>> ev_marks;   // (phase, index of start event)
     int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
+    // split mode: K1a (SpMM alone, full occupancy) -> AV, then K1<P, true>
+    bool split = false;
+    int nb1a = 0;
+    double* AV = nullptr;
     bool pdl = true;   // programmatic dependent launch of the block-step kernels
     int gblocks = 2;   // block steps per captured graph (halves the graph-boundary gaps)
     int prio_hi = 0;   // greatest stream priority (side branch)
@@ -335,6 +348,20 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     for (int s = 0; s < 3; ++s) dalloc(h, &h->V[s], vpanel);
     dalloc(h, &h->M[0], panel);
     dalloc(h, &h->M[1], panel);
+    // split mode for large panels (the gathers of a big SpMM need more warps per SM than the fused
+    // K1 has; below ~128 MB the extra AV write + read costs more than it saves)
+    {
+        const char* se = getenv("BMINRES_SPLIT");
+        const bool can = h->kf.k1a != nullptr;
+        const int mode = se ? (atoi(se) != 0 ? 1 : 2) : h->opt.split_spmm;
+        h->split = can && (mode == 1 || (mode == 0 && (double)n * p * 8.0 >= 128e6));
+        if (h->split) {
+            dalloc(h, &h->AV, panel);
+        } else if (h->AV) {
+            cudaFree(h->AV);
+            h->AV = nullptr;
+        }
+    }
     for (int s = 0; s < 2; ++s) {
         if (h->scr[s]) cudaFree(h->scr[s]);
         h->scr[s] = nullptr;
@@ -384,6 +411,13 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     h->nb1 = (std::min(NB_MAX, h->n_sm * o1) - (o1 > 1 ? h->csz : 0)) / h->csz * h->csz;
     h->nb2 = (std::min(NB_MAX, h->n_sm * o2) - (o2 > 1 ? h->csz : 0)) / h->csz * h->csz;
     h->nb4 = h->n_sm * o4;
+    if (h->split) {
+        int oa = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, (const void*)h->kf.k1a, NT, 0);
+        h->nb1a = h->n_sm * std::max(1, oa);
+        const int o1p = std::min(cap, occ_of((const void*)h->kf.k1pre, h->kf.nt1, h->kf.smem1pre));
+        h->nb1 = (std::min(NB_MAX, h->n_sm * o1p) - (o1p > 1 ? h->csz : 0)) / h->csz * h->csz;
+    }
     (void)cluster_grid;
 
 }
@@ -509,7 +543,40 @@ void halo_exchange(bminres_ctx* h, double* V, int p, cudaStream_t s) {
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
-             par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X};
+             par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X, nullptr};
+    if (h->split) {
+        // K1a: AV = A V_k (PDL after reduce2 / K2), then K1 streams AV
+        K1Args aa = a;
+        aa.Vprev = nullptr;
+        aa.Y = h->AV;
+        aa.fuse = 0;
+        cudaStream_t keep = h->stream;
+        h->stream = s;
+        {
+            TimeMark tm(h, PH_SPMM_AV);
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+            cfg.gridDim = dim3(h->nb1a);
+            cfg.blockDim = dim3(NT);
+            cfg.dynamicSmemBytes = 0;
+            cfg.stream = s;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k1a, aa);
+            if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k1a_spmm: ") + cudaGetErrorString(e));
+            h->launches++;
+        }
+        a.AV = h->AV;
+        {
+            TimeMark tm(h, fuse ? PH_EPI_FUSED : PH_EPI);
+            launch_cluster(h, h->kf.k1pre, h->nb1, h->kf.nt1, h->kf.smem1pre, a, "k1_dmma(split)");
+        }
+        h->stream = keep;
+        launch_reduce(h, s, 1, k);
+        return;
+    }
     {
         TimeMark tm(h, fuse ? PH_SPMM_FUSED : PH_SPMM);
         cudaStream_t keep = h->stream;
@@ -1248,7 +1315,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // same graphs (their collectives match).
         for (long long s = b; s <= nblocks && graphs; s += GB) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
-            h->launches += GB * (h->kf.fused ? 5 : 6);
+            h->launches += GB * ((h->kf.fused ? 5 : 6) + (h->split ? 1 : 0));
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -1390,6 +1457,10 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
         g_create_err = "bad device ordinal";
         return BMINRES_EINVAL;
     }
+    if (o.split_spmm < 0 || o.split_spmm > 2) {
+        g_create_err = "split_spmm must be 0 (auto), 1 (always) or 2 (never)";
+        return BMINRES_EINVAL;
+    }
     auto* h = new bminres_ctx();
     h->opt = o;
     h->device = o.device;
@@ -1416,6 +1487,9 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
             Kfn f;
             kfn_for(p, &f, qv);
             CK(cudaFuncSetAttribute((const void*)f.k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem1));
+            if (f.k1pre)
+                CK(cudaFuncSetAttribute((const void*)f.k1pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)f.smem1pre));
             CK(cudaFuncSetAttribute((const void*)f.k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem2));
             CK(cudaFuncSetAttribute((const void*)f.k3b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
             CK(cudaFuncSetAttribute((const void*)f.k4b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4b));
@@ -1577,7 +1651,7 @@ void bminres_destroy(bminres_handle h) {
     cudaSetDevice(h->device);
     for (int s = 0; s < 6; ++s)
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
-    for (double* p : {h->V[0], h->V[1], h->V[2], h->M[0], h->M[1], h->scr[0], h->scr[1], h->pool, h->part, h->dsc,
+    for (double* p : {h->V[0], h->V[1], h->V[2], h->M[0], h->M[1], h->AV, h->scr[0], h->scr[1], h->pool, h->part, h->dsc,
                       h->gdev, h->a_val, h->bx, h->xx, h->hist})
         if (p) cudaFree(p);
     if (h->trace) cudaFree(h->trace);

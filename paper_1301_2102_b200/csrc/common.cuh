@@ -119,7 +119,7 @@ struct DevState {
 };
 
 // kernel types of the trace buffer
-enum TraceKind { TR_K1 = 0, TR_RED1, TR_K2, TR_RED2, TR_K3B, TR_K4B, TR_NKIND };
+enum TraceKind { TR_K1 = 0, TR_RED1, TR_K2, TR_RED2, TR_K3B, TR_K4B, TR_K1A, TR_NKIND };
 constexpr int TRACE_PTS = 8;
 constexpr int TRACE_CTAS = 1024;
 

@@ -376,15 +376,99 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
 }
 
 
-// ------------------------------------------------------------------ K1 on DMMA (epilogue)
+// ------------------------------------------------------------------ K1a: the SpMM alone (split mode)
+//
+// Row a1's operator product AV = A V_k (eqn.block-Lanczos-recurr's A u_j, applied to the
+// p vectors of the block at once), for large panels: a register-light kernel at full
+// occupancy (no shared memory, no epilogue) keeps ~2.5x more gathers in flight per SM than the
+// fused K1 can; K1<P, true> then streams AV like a panel.  Rows are summed
+// in CSR order with fma from 0, exactly as K1's own gathers, so AV is bitwise the same.
+// Order: CTA chunks of WARPS*KU consecutive row groups, round-robin over the CTAs -- neighbouring
+// rows stay in one SM's L1 and all SMs sweep the matrix together, so far (z-plane) neighbours are
+// re-read from L2.
+template <int P>
+struct K1aCfg {
+    static constexpr int CH = P >= 32 ? 4 : 8;   // CSR entries per gather batch
+    static constexpr int KU = 8;                 // row groups per warp per CTA chunk
+    static constexpr int MINB = P >= 32 ? 6 : 5; // CTAs per SM (<= 40 / 48 registers)
+};
 
 template <int P>
+__global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
+    using C = PC<P>;
+    constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
+    constexpr int CH = K1aCfg<P>::CH, KU = K1aCfg<P>::KU;
+    DevState* st = a.st;
+    unsigned long long* tr = trace_begin(st, TR_K1A);
+    pdl_wait();   // V_k (K2 of block k-1) is complete and visible
+    trace_pt(tr, 1);
+    if (!st->run_main) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int sub = lane % LP, rsub = lane / LP;
+    const bool act = sub < LANES;
+    const int c0 = sub * VEC;
+    const long long ngroups = (a.n + RPW - 1) / RPW;
+    const long long chunk = (long long)nw * KU;
+    long long cidx = blockIdx.x;
+    int cpos = warp;
+    for (long long g = cidx * chunk + cpos; g < ngroups;) {
+        const long long i = g * RPW + rsub;
+        const bool live = act && i < a.n;
+        const int r0 = live ? __ldg(a.rowptr + i) : 0;
+        const int r1 = live ? __ldg(a.rowptr + i + 1) : 0;
+        double acc[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+        for (int kb = r0; __any_sync(FULL, kb < r1); kb += CH) {
+            int c[CH];
+            double av[CH];
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                const bool pr = kb + t < r1;
+                c[t] = pr ? __ldg(a.col + kb + t) : -1;
+                av[t] = pr ? __ldg(a.val + kb + t) : 0.0;
+            }
+            double xv[CH][VEC];
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                if (c[t] >= 0) {
+                    ldv<VEC>(a.X + (long long)c[t] * P + c0, xv[t]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < CH; ++t)
+                if (c[t] >= 0) {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
+                }
+        }
+        if (live) stv<VEC>(a.Y + i * P + c0, acc);   // Y = the AV panel
+        cpos += nw;
+        if (cpos >= chunk) {
+            cpos = warp;
+            cidx += gridDim.x;
+        }
+        g = cidx * chunk + cpos;
+    }
+    trace_pt(tr, 4);
+    pdl_trigger();
+    trace_pt(tr, 5);
+}
+
+// ------------------------------------------------------------------ K1 on DMMA (epilogue)
+
+template <int P, bool PRE = false>
 struct K1DSmem {
     // p = 32: one 512-thread CTA per SM (16 warps, <= 128 registers) instead of one 256-thread
     // CTA at 209 registers -- the gathers need the warps; the fused update single-staged
     static constexpr int WARPS = P >= 32 ? 16 : 8;
     static constexpr int UNS = P >= 32 ? 1 : 2;              // cp.async stages of the fused update
-    static constexpr int pipe = WARPS * 3 * DM<P>::TILE;   // V_k, V_{k-1} tiles + A V tile per warp
+    // split mode (PRE): the A V_k rows are staged like the panels; two stages where they fit
+    static constexpr int NSP = (PRE && P < 32) ? 2 : 1;
+    static constexpr int pipe = WARPS * 3 * DM<P>::TILE * NSP;   // V_k, V_{k-1} tiles + A V tile per warp
     static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
     static constexpr int upd = UpdSmem<P, WARPS, UNS>::doubles;   // the update runs first, then the SpMM
     static constexpr int region = (pipe + scr > upd) ? pipe + scr : upd;
@@ -400,10 +484,11 @@ struct K1DSmem {
 // q are in flight, the column indices and values of group q+1 and the row pointers of group
 // q+2 are loaded.  The SpMM of the warp's first tile runs before the prologue (the Cholesky of
 // the previous block's Gram), which only the epilogue needs.
-template <int P>
+template <int P, bool PRE = false>
 __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dmma(K1Args a) {
     using D = DM<P>;
     using C = PC<P>;
+    using KS = K1DSmem<P, PRE>;
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int E = P * P + P;
@@ -420,8 +505,8 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
     double* fT = dynd1;            // Tr_k
     double* fD = fT + FR;          // -(Tr_{k-1} C_{k-1}^T)
     double* pipe = fD + FR;
-    double* scr = pipe + K1DSmem<P>::pipe;
-    double* sAcc = pipe + K1DSmem<P>::region;
+    double* scr = pipe + KS::pipe;
+    double* sAcc = pipe + KS::region;
     // each CTA owns a contiguous slab of tiles (its warps interleave inside it), so the
     // gathers of neighbouring rows (stencil offsets +-1, +-nx) hit this SM's L1
     const long long ntiles = (a.n + TR - 1) / TR;
@@ -436,7 +521,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
         if (b >= st->k_upd_min && b < st->k_side && b < st->stop_side_at) {
             if (blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = b;
             K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b};
-            dmma_update<P, WARPS, K1DSmem<P>::UNS>(u, cbeg, WARPS, cend, pipe);
+            dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe);
             __syncthreads();   // the region is reused by the SpMM
         }
     }
@@ -539,35 +624,20 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             for (int v = 0; v < VEC; ++v) tA[rl * RS + c0 + v] = acc[v];
         }
     };
-    // pipeline fill, then the SpMM of the first tile (no dependence on the prologue)
-    load_rp(0, k0, k1);
-    load_rp(1, rn0, rn1);
-    load_cv(k0, k1, cc, av);
-    long long q = 0;
-    for (; q < G && q < nq; ++q) process_group(q);
-    pdl_wait();   // red2 (reduce2 of block k-1) is ready
-    trace_pt(tr, 2);
-    {
-        // C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D
+    // ---- the prologue: C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D
+    auto prologue = [&]() -> bool {
         double* sTk = scr;
         double* sD = scr + P * P;
-        if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, scr + 2 * P * P)) {
-            cp_wait<0>();
-            return;
-        }
+        if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, scr + 2 * P * P)) return false;
         to_frag<P>(sTk, P, 1.0, fT);
         to_frag<P>(sD, P, -1.0, fD);
         __syncthreads();
-    }
-    trace_pt(tr, 3);
-    for (long long it = 0; it < my_tiles; ++it) {
-        if (it > 0)
-            for (int gq = 0; gq < G; ++gq, ++q) process_group(q);
+        return true;
+    };
+    // ---- epilogue of tile `it`: tAV holds its A V_k rows (overwritten by its W rows), tV / tP its
+    // V_k / V_{k-1} rows
+    auto epilogue = [&](long long it, const double* tV, const double* tP, double* tAV) {
         const long long base = (t0 + it * ts) * TR;
-        cp_wait<0>();
-        __syncwarp();
-        const double* tV = wb;
-        const double* tP = wb + D::TILE;
 #pragma unroll
         for (int mc = 0; mc < TR / 8; ++mc) {
             const int r0 = mc * 8;
@@ -580,7 +650,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
                 // W = (A V_k) Tr_k = A U_k, the raw candidates; ||A u_j||^2 (C14)
 #pragma unroll
                 for (int kc = 0; kc < KC; ++kc)
-                    dmma(w[nc][0], w[nc][1], tA[(r0 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
+                    dmma(w[nc][0], w[nc][1], tAV[(r0 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
                 om[nc][0] = fma(w[nc][0], w[nc][0], om[nc][0]);
                 om[nc][1] = fma(w[nc][1], w[nc][1], om[nc][1]);
                 // W -= U_{k-1} C_{k-1}^T = V_{k-1} D  (h_{i,j} = h_{j,i})
@@ -594,8 +664,8 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 const int col = nc * 8 + 2 * fc;
-                tA[(r0 + fr) * RS + col] = w[nc][0];
-                tA[(r0 + fr) * RS + col + 1] = w[nc][1];
+                tAV[(r0 + fr) * RS + col] = w[nc][0];
+                tAV[(r0 + fr) * RS + col + 1] = w[nc][1];
                 if (rok) *reinterpret_cast<double2*>(a.Y + row * P + col) = make_double2(w[nc][0], w[nc][1]);
             }
         }
@@ -604,7 +674,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
 #pragma unroll
         for (int k0 = 0; k0 < TR; k0 += 4) {
             const double* rv = tV + (k0 + fc) * RS;
-            const double* rw = tA + (k0 + fc) * RS;
+            const double* rw = tAV + (k0 + fc) * RS;
 #pragma unroll
             for (int i = 0; i < NC; ++i) {
                 const double av = rv[i * 8 + fr];
@@ -613,6 +683,59 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             }
         }
         __syncwarp();
+    };
+    if constexpr (PRE) {
+        // split mode: A V_k (k1a_spmm, the predecessor) is streamed like the panels -- NSP-deep
+        // cp.async ring of {V_k, V_{k-1}, A V_k} tiles per warp
+        constexpr int NSP = KS::NSP;
+        double* wpre = pipe + warp * 3 * D::TILE * NSP;
+        auto stage3 = [&](long long it) {
+            if (it < my_tiles) {
+                double* sl = wpre + (int)(it % NSP) * 3 * D::TILE;
+                const long long base = (t0 + it * ts) * TR;
+                stage_tile<P>(sl, a.X, base, a.n, lane);
+                if (has_prev) stage_tile<P>(sl + D::TILE, a.Vprev, base, a.n, lane);
+                stage_tile<P>(sl + 2 * D::TILE, a.AV, base, a.n, lane);
+            }
+            cp_commit();
+        };
+        pdl_wait();   // A V_k (k1a) and, through it, red2 of block k-1 are complete
+        trace_pt(tr, 2);
+#pragma unroll
+        for (int s = 0; s < NSP; ++s) stage3(s);   // the first tiles stream in during the prologue
+        if (!prologue()) {
+            cp_wait<0>();
+            return;
+        }
+        trace_pt(tr, 3);
+        for (long long it = 0; it < my_tiles; ++it) {
+            cp_wait<NSP - 1>();
+            __syncwarp();
+            double* sl = wpre + (int)(it % NSP) * 3 * D::TILE;
+            epilogue(it, sl, sl + D::TILE, sl + 2 * D::TILE);
+            stage3(it + NSP);
+        }
+    } else {
+        // pipeline fill, then the SpMM of the first tile (no dependence on the prologue)
+        load_rp(0, k0, k1);
+        load_rp(1, rn0, rn1);
+        load_cv(k0, k1, cc, av);
+        long long q = 0;
+        for (; q < G && q < nq; ++q) process_group(q);
+        pdl_wait();   // red2 (reduce2 of block k-1) is ready
+        trace_pt(tr, 2);
+        if (!prologue()) {
+            cp_wait<0>();
+            return;
+        }
+        trace_pt(tr, 3);
+        for (long long it = 0; it < my_tiles; ++it) {
+            if (it > 0)
+                for (int gq = 0; gq < G; ++gq, ++q) process_group(q);
+            cp_wait<0>();
+            __syncwarp();
+            epilogue(it, wb, wb + D::TILE, tA);
+        }
     }
     cp_wait<0>();
     trace_pt(tr, 4);

@@ -46,6 +46,8 @@ struct K1Args {
     double* Mk2;          // M slot k mod 2: M_{k-4} in, M_{k-2} out
     const double* Mk1;    // M slot (k+1) mod 2: M_{k-3}
     double* Xs;           // solution panel
+    // split mode (k1_dmma<P, true>): A V_k was computed by k1a_spmm into AV; K1 stages its rows
+    const double* AV;
 };
 
 template <int P>

@@ -113,7 +113,14 @@ __global__ void __launch_bounds__(256) spmm_a(const int* __restrict__ rp, const 
         uend = nunits;
         ustep = (long long)gridDim.x * nw;
     }
-    for (long long u = ubeg; u < uend; u += ustep) {
+    constexpr int KU = 8;   // ORDER 2: CTA chunks of nw*KU consecutive units, round-robin over CTAs
+    const long long chunk = (long long)nw * KU;
+    long long cidx = blockIdx.x, cpos = warp;
+    if (ORDER == 2) {
+        ubeg = blockIdx.x * chunk + warp;
+        uend = nunits;
+    }
+    for (long long u = ubeg; u < uend;) {
         int r0[U], r1[U];
 #pragma unroll
         for (int x = 0; x < U; ++x) {
@@ -164,7 +171,159 @@ __global__ void __launch_bounds__(256) spmm_a(const int* __restrict__ rp, const 
             const long long i = u * ROWS + x * RPW + rsub;
             if (i < n) *reinterpret_cast<double2*>(Y + i * P + c0) = make_double2(acc[x][0], acc[x][1]);
         }
+        if (ORDER == 2) {
+            cpos += nw;
+            if (cpos >= chunk) {
+                cpos = warp;
+                cidx += gridDim.x;
+            }
+            u = cidx * chunk + cpos;
+        } else {
+            u += ustep;
+        }
     }
+}
+
+
+__device__ __forceinline__ void cpa16(void* sdst, const void* gsrc, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    const int nb = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(nb) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* sdst, const void* gsrc, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    const int nb = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(nb) : "memory");
+}
+__device__ __forceinline__ void cpcommit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpwait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Variant C: cp.async gather ring.  A unit = one CH-entry chunk of the warp's RPW rows; D units
+// in flight per warp (no registers held per in-flight gather).  Column indices of the next unit
+// are loaded one step ahead, row pointers two groups ahead.
+template <int P, int CH, int D>
+struct CSm {
+    static constexpr int RPW = PCx<P>::RPW;
+    static constexpr int SLOT = CH * RPW * P + CH * RPW;   // doubles: x rows, then vals
+    static constexpr int WARP = D * SLOT;
+};
+template <int P, int CH, int D, int ORDER, int MINB>
+__global__ void __launch_bounds__(256, MINB) spmm_c(const int* __restrict__ rp, const int* __restrict__ ci,
+                                              const double* __restrict__ va, const double* __restrict__ X,
+                                              double* __restrict__ Y, long long n) {
+    using C = PCx<P>;
+    using S = CSm<P, CH, D>;
+    constexpr int RPW = C::RPW;
+    extern __shared__ __align__(16) double smc[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int sub = lane % C::LP, rsub = lane / C::LP;
+    const int c0 = sub * 2;
+    double* ring = smc + warp * S::WARP;
+    int* meta = reinterpret_cast<int*>(smc + nw * S::WARP) + warp * D * 2;
+    const long long ngroups = (n + RPW - 1) / RPW;
+    long long gbeg, gend, gstep;
+    if (ORDER == 0) {
+        const long long per = (ngroups + gridDim.x - 1) / gridDim.x;
+        gbeg = blockIdx.x * per + warp;
+        gend = min(ngroups, (long long)(blockIdx.x + 1) * per);
+        gstep = nw;
+    } else {
+        gbeg = (long long)blockIdx.x * nw + warp;
+        gend = ngroups;
+        gstep = (long long)gridDim.x * nw;
+    }
+    // issuer state
+    long long gi = gbeg;           // group being issued
+    int ci_ = 0, mc = 0;           // chunk, chunks of the group
+    int k0 = 0, k1 = 0;            // lane's row range (group gi)
+    int nk0 = 0, nk1 = 0;          // row pointers of the next group
+    int cn[CH];
+    auto rowp = [&](long long g, int& a, int& b) {
+        a = b = 0;
+        if (g < gend) {
+            const long long i = g * RPW + rsub;
+            if (i < n) {
+                a = __ldg(rp + i);
+                b = __ldg(rp + i + 1);
+            }
+        }
+    };
+    auto chunks = [&](int a, int b) { return __reduce_max_sync(0xffffffffu, (unsigned)((b - a + CH - 1) / CH)); };
+    auto loadc = [&]() {
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const int k = k0 + ci_ * CH + t;
+            cn[t] = k < k1 ? __ldg(ci + k) : -1;
+        }
+    };
+    rowp(gi, k0, k1);
+    rowp(gi + gstep, nk0, nk1);
+    mc = chunks(k0, k1);
+    loadc();
+    auto advance = [&]() {
+        if (++ci_ >= mc) {
+            ci_ = 0;
+            gi += gstep;
+            k0 = nk0;
+            k1 = nk1;
+            rowp(gi + gstep, nk0, nk1);
+            mc = chunks(k0, k1);
+            if (gi < gend && mc == 0) mc = 1;   // empty rows: one (empty) unit to write zeros
+        }
+        loadc();
+    };
+    if (mc == 0 && gi < gend) mc = 1;
+    auto issue = [&](int slot) {
+        if (gi < gend) {
+            double* sx = ring + slot * S::SLOT;
+            double* sv = sx + CH * RPW * P;
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                const bool ok = cn[t] >= 0;
+                cpa16(sx + (t * RPW + rsub) * P + c0, X + (long long)(ok ? cn[t] : 0) * P + c0, ok);
+                if (sub == 0) {
+                    const int k = k0 + ci_ * CH + t;
+                    cpa8(sv + t * RPW + rsub, va + (ok ? k : 0), ok);
+                }
+            }
+            if (lane == 0) {
+                meta[slot * 2] = (int)((gi - gbeg) / gstep);
+                meta[slot * 2 + 1] = (ci_ == mc - 1) ? 1 : 0;
+            }
+            advance();
+        } else if (lane == 0) {
+            meta[slot * 2] = -1;
+        }
+        cpcommit();
+    };
+#pragma unroll
+    for (int s = 0; s < D - 1; ++s) issue(s);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int u = 0;; ++u) {
+        issue((u + D - 1) % D);
+        cpwait<D - 1>();
+        __syncwarp();
+        const int slot = u % D;
+        const int gl = meta[slot * 2];
+        if (gl < 0) break;
+        const double* sx = ring + slot * S::SLOT;
+        const double* sv = sx + CH * RPW * P;
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const double a = sv[t * RPW + rsub];
+            const double2 x = *reinterpret_cast<const double2*>(sx + (t * RPW + rsub) * P + c0);
+            acc0 = fma(a, x.x, acc0);
+            acc1 = fma(a, x.y, acc1);
+        }
+        if (meta[slot * 2 + 1]) {
+            const long long i = (gbeg + (long long)gl * gstep) * RPW + rsub;
+            if (i < n) *reinterpret_cast<double2*>(Y + i * P + c0) = make_double2(acc0, acc1);
+            acc0 = acc1 = 0.0;
+        }
+        __syncwarp();
+    }
+    cpwait<0>();
 }
 
 __global__ void copyk(const double2* __restrict__ a, double2* __restrict__ b, long long m) {
@@ -218,6 +377,42 @@ static void run_a(const Dev& d, int ctas_per_sm, const char* tag) {
     CK(cudaMemset(d.Y, 0, d.n * P * 8));
 }
 
+
+template <int P, int CH, int D, int ORDER, int MINB>
+static void run_c(const Dev& d, int ctas_per_sm, const char* tag) {
+    auto k = spmm_c<P, CH, D, ORDER, MINB>;
+    const size_t smem = sizeof(double) * 8 * CSm<P, CH, D>::WARP + 8 * D * 2 * 4;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+    const int per = std::min(occ, ctas_per_sm);
+    if (per < 1) { printf("%s: no occupancy\n", tag); return; }
+    const int grid = 148 * per;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 7; ++r) {
+        cudaEventRecord(e0);
+        k<<<grid, 256, smem>>>(d.rp, d.ci, d.va, d.X, d.Y, d.n);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+    }
+    CK(cudaGetLastError());
+    std::vector<double> y(d.n * P), yr(d.n * P);
+    CK(cudaMemcpy(y.data(), d.Y, y.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(yr.data(), d.Yref, yr.size() * 8, cudaMemcpyDeviceToHost));
+    bool ok = memcmp(y.data(), yr.data(), y.size() * 8) == 0;
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    printf("%-28s CH=%2d D=%d order=%d occ=%d/%d regs=%3d smem=%6zu %8.1f us  %7.1f GB/s  %s\n", tag, CH, D, ORDER, per, occ,
+           fa.numRegs, smem, best * 1e3, d.bytes / (best * 1e-3) / 1e9, ok ? "ok" : "MISMATCH");
+    CK(cudaMemset(d.Y, 0, d.n * P * 8));
+}
+
 template <int P>
 static void lab(const Csr& A) {
     Dev d;
@@ -266,16 +461,14 @@ static void lab(const Csr& A) {
         cudaFree(a);
         cudaFree(b);
     }
-    for (int cps : {2, 4, 8}) {
+    for (int cps : {4, 8}) {
         printf("-- ctas/SM cap %d\n", cps);
         run_a<P, 1, 8, 0>(d, cps, "A slab");
         run_a<P, 1, 8, 1>(d, cps, "A stride");
-        run_a<P, 2, 8, 0>(d, cps, "A slab");
-        run_a<P, 2, 8, 1>(d, cps, "A stride");
-        run_a<P, 4, 8, 0>(d, cps, "A slab");
-        run_a<P, 4, 8, 1>(d, cps, "A stride");
-        run_a<P, 1, 16, 0>(d, cps, "A slab");
-        run_a<P, 2, 4, 1>(d, cps, "A stride");
+        run_a<P, 1, 8, 2>(d, cps, "A chunked");
+        run_a<P, 1, 4, 2>(d, cps, "A chunked");
+        run_a<P, 1, 16, 2>(d, cps, "A chunked");
+        run_a<P, 2, 4, 2>(d, cps, "A chunked");
     }
     cudaFree(d.rp);
     cudaFree(d.ci);

@@ -18,12 +18,12 @@ X = torch.zeros_like(B)
 with Solver(0, pool_size=1, record_history=False) as s:
     s.solve(A, B, X, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
     s.solve(A, B, X, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
-t = np.fromfile(f, dtype=np.uint64).reshape(6, 1024, -1).astype(np.int64)
-names = ["K1", "red1", "K2", "red2", "K3b", "K4b"]
+t = np.fromfile(f, dtype=np.uint64).reshape(7, 1024, -1).astype(np.int64)
+names = ["K1", "red1", "K2", "red2", "K3b", "K4b", "K1a"]
 pts = ["start", "pt1", "pt2", "pt3", "pt4", "end", "cpart", "tail0", "t_sum", "t_ld", "t_mm", "t_end", "x12", "x13", "x14", "x15"]
 t0 = None
 rows = []
-for k in range(6):
+for k in range(7):
     x = t[k]
     live = x[:, 0] > 0
     if not live.any():
