@@ -196,6 +196,17 @@ __device__ __forceinline__ void frag_acc(double* sAcc, int base, int ld, int m0,
     d[1] = (first ? 0.0 : d[1]) + c[1];
 }
 
+// The transpose of one accumulator block: C(r, c) of block (m0, n0) goes to sAcc[(n0+c)*ld + m0+r]
+// (the mirrored half of a symmetric Gram), same fixed warp order as frag_acc.
+__device__ __forceinline__ void frag_acc_t(double* sAcc, int ld, int m0, int n0, const double (&c)[2], bool first,
+                                           int lane) {
+    const int r = m0 + (lane >> 2), col = n0 + 2 * (lane & 3);
+    double* d0 = sAcc + col * ld + r;
+    double* d1 = sAcc + (col + 1) * ld + r;
+    *d0 = (first ? 0.0 : *d0) + c[0];
+    *d1 = (first ? 0.0 : *d1) + c[1];
+}
+
 // ------------------------------------------------------------------ K2 on DMMA
 
 template <int P>
@@ -204,10 +215,16 @@ struct K2DSmem {
     static constexpr int NS = P >= 32 ? 2 : NSTAGE;  // cp.async stages (shared-memory budget)
     static constexpr int RSQ = 12;                        // pool tile row stride (8 columns + pad)
     static constexpr int TQ = DM<P>::TR * RSQ;
-    static constexpr int pipe = WARPS * NS * (2 * DM<P>::TILE + TQ);
+    static constexpr int STG = 2 * DM<P>::TILE + TQ;         // one stage of one warp
+    // slot-major: stage s of warp w at pipe + (s * WARPS + w) * STG
+    static constexpr int pipe = WARPS * NS * STG;
     static constexpr int LD = P + 1;
-    static constexpr int tail = 5 * P * P + P * MAXQ + P;   // sGs, sTk, sX, sG, sCo, k2_prologue (P*P + P)
-    static constexpr size_t bytes = sizeof(double) * (DM<P>::FR + DM<P>::KC * 32 + pipe + P * P + MAXQ * P + tail);
+    // prologue scratch: sTk, sX, sG, sCo, k2_prologue's (P*P + P, then sGs).  It overlays the last
+    // pipeline slot, which is first issued after the prologue (2 CTAs/SM at p = 16, 32)
+    static constexpr int tail = 4 * P * P + P * MAXQ + P;
+    static constexpr bool OVERLAY = tail <= WARPS * STG;
+    static constexpr size_t bytes =
+        sizeof(double) * (DM<P>::FR + DM<P>::KC * 32 + pipe + P * P + MAXQ * P + (OVERLAY ? 0 : tail));
 };
 
 template <int P>
@@ -217,6 +234,7 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
     constexpr int WARPS = S::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR, RSQ = S::RSQ;
     DevState* st = a.st;
     if (!st->run_main) return;
+    unsigned long long* tr = trace_begin(st, TR_K2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane >> 2, fc = lane & 3;
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
@@ -226,14 +244,14 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
     double* fF = fE + FR;            // -(Tr_k coef_{k-1}) (P x 8) in fragment order (KC blocks)
     double* pipe = fF + KC * 32;
     double* sAcc = pipe + S::pipe;
-    double* sTail = sAcc + P * P + MAXQ * P;
-    double* wb = pipe + warp * S::NS * (2 * D::TILE + S::TQ);
+    double* sTail = S::OVERLAY ? pipe + (S::NS - 1) * WARPS * S::STG : sAcc + P * P + MAXQ * P;
+    double* wb = pipe + warp * S::STG;
     const long long ntiles = (a.n + TR - 1) / TR;
     const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
     auto issue = [&](long long it, int slot) {
         const long long t = t0 + it * ts;
         if (t < ntiles) {
-            double* sl = wb + slot * (2 * D::TILE + S::TQ);
+            double* sl = wb + slot * WARPS * S::STG;
             const long long base = t * TR;
             stage_tile<P>(sl, a.W, base, a.n, lane);
             stage_tile<P>(sl + D::TILE, a.V, base, a.n, lane);
@@ -252,15 +270,16 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
 #pragma unroll
     for (int s = 0; s < S::NS - 1; ++s) issue(s, s);
     pdl_wait();   // red1 (reduce1) is ready
+    trace_pt(tr, 1);
     {
         // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
         // computes h_{i,j} for i >= j)
-        double* sGs = sTail;
-        double* sTk = sTail + P * P;
-        double* sX = sTail + 2 * P * P;
-        double* sG = sTail + 3 * P * P;
-        double* sCo = sTail + 4 * P * P;                // P x MAXQ
-        double* sScr = sCo + P * MAXQ;
+        double* sTk = sTail;
+        double* sX = sTail + P * P;
+        double* sG = sTail + 2 * P * P;
+        double* sCo = sTail + 3 * P * P;                // P x MAXQ
+        double* sScr = sCo + P * MAXQ;                  // k2_prologue's red1 copy, then sGs
+        double* sGs = sScr;
         const double* Co = st->coef[a.par ^ 1];
         for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) sCo[t] = Co[t];
         k2_prologue<P>(st, a.par, a.sk, sG, sTk, sScr);   // (syncs after its loads)
@@ -282,6 +301,7 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
         to_frag<P>(sX, P, -1.0, fE);
         __syncthreads();
     }
+    trace_pt(tr, 3);
     double g[NC][NC][2], pq[NC][2];
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -293,7 +313,7 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
         issue(it + S::NS - 1, (int)((it + S::NS - 1) % S::NS));
         cp_wait<S::NS - 1>();
         __syncwarp();
-        double* sl = wb + (int)(it % S::NS) * (2 * D::TILE + S::TQ);
+        double* sl = wb + (int)(it % S::NS) * WARPS * S::STG;
         double* tW = sl;
         const double* tV = sl + D::TILE;
         double* tR = sl + 2 * D::TILE;
@@ -336,8 +356,9 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
 #pragma unroll
             for (int i = 0; i < NC; ++i) {
                 const double av = rw[i * 8 + fr];
+                // W'^T W' is symmetric: the blocks j <= i only (mirrored in the CTA sum)
 #pragma unroll
-                for (int j = 0; j < NC; ++j) dmma(g[i][j][0], g[i][j][1], av, rw[j * 8 + fr]);
+                for (int j = 0; j <= i; ++j) dmma(g[i][j][0], g[i][j][1], av, rw[j * 8 + fr]);
             }
             if (Q > 0) {
                 const double ar = tR[(k0 + fc) * RSQ + fr];
@@ -348,6 +369,7 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
         __syncwarp();
     }
     cp_wait<0>();
+    trace_pt(tr, 4);
     pdl_trigger();   // the dependent (reduce2) launches while this grid reduces its partials
     // rows past n were zero-filled, so they contribute nothing; reduce across warps (fixed order)
     for (int w = 0; w < WARPS; ++w) {
@@ -355,7 +377,10 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
 #pragma unroll
             for (int i = 0; i < NC; ++i)
 #pragma unroll
-                for (int j = 0; j < NC; ++j) frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
+                for (int j = 0; j <= i; ++j) {
+                    frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
+                    if (j < i) frag_acc_t(sAcc, P, i * 8, j * 8, g[i][j], w == 0, lane);
+                }
             if (Q > 0) {
                 // pdot(q, m) = (R^T W')(q, m) at P*P + q*P + m, q < Q
                 const int q = fr;
@@ -373,6 +398,7 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
         __syncthreads();
     }
     cluster_partials(sAcc, E, st->part2[a.par]);   // reduce2, then K1(k+1) and K3b(k) factor W' from these
+    trace_pt(tr, 5);
 }
 
 
