@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) k_dots(DotArgs a) {
         if (k < a.K) {
             const double* vp = a.v[k].p;
             const long long vs = a.v[k].stride;
+#pragma unroll 8
             for (long long i = (long long)blockIdx.x * 8 + ty; i < a.n; i += (long long)gridDim.x * 8)
                 s = fma(vp[i * vs], a.t[i * a.ts], s);
         }

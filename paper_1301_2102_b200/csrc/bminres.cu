@@ -45,6 +45,10 @@ struct Kfn {  // per-p kernel table
     void (*k1a)(K1Args);     // split mode: the SpMM alone (null: no split kernels for this p)
     void (*k1pre)(K1Args);   // split mode: K1 streaming A V_k
     size_t smem1pre;
+    // start block / exit residual: Gram, V R^{-1}, plain SpMM (DMMA / K1a versions for p = 8, 16, 32)
+    void (*gram)(const double*, long long, int, double*, int, double*, unsigned*);
+    void (*mat)(const double*, const double*, double*, long long, int);
+    size_t smem_gram, smem_mat;
     void (*k2)(K2Args);
     void (*k3b)(DevState*);
     void (*k4b)(K4bArgs);
@@ -60,6 +64,9 @@ Kfn make_kfn(int q) {
     f.k1a = nullptr;
     f.k1pre = nullptr;
     f.smem1pre = 0;
+    f.gram = k_gram;
+    f.mat = k_materialize;
+    f.smem_gram = f.smem_mat = 0;
     f.k1 = k1_spmm<P, true>;
     f.nt1 = NT;
     f.smem1 = K1Smem<P>::bytes;
@@ -83,6 +90,11 @@ Kfn make_kfn(int q) {
         }
         f.k4b = k4b_dmma<P>;
         f.smem4b = K4bDSmem<P>::bytes;
+        f.k1a = k1a_spmm<P>;   // (also the plain SpMM of the start / exit residual)
+        f.gram = k_gram_dmma<P>;
+        f.smem_gram = GramDSmem<P>::bytes;
+        f.mat = k_materialize_dmma<P>;
+        f.smem_mat = mat_dmma_smem<P>();
         f.nt4b = 128;
     } else {
         f.k4b = k4b_update<P>;
@@ -352,7 +364,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     // K1 has; below ~128 MB the extra AV write + read costs more than it saves)
     {
         const char* se = getenv("BMINRES_SPLIT");
-        const bool can = h->kf.k1a != nullptr;
+        const bool can = h->kf.k1pre != nullptr;
         const int mode = se ? (atoi(se) != 0 ? 1 : 2) : h->opt.split_spmm;
         h->split = can && (mode == 1 || (mode == 0 && (double)n * p * 8.0 >= 128e6));
         if (h->split) {
@@ -540,6 +552,25 @@ void halo_exchange(bminres_ctx* h, double* V, int p, cudaStream_t s) {
     if (!h->tp->exchange(h->d_sendbuf, h->sc_d.data(), V + h->plan.n_loc * p, h->rc_d.data(), s, err))
         fail(h, BMINRES_ENCCL, err);
 }
+// Y = A X alone (start block with X0, exit residual, bminres_spmm): the full-occupancy K1a kernel
+// for p in {8, 16, 32}, else the plain variant of the generic K1.  Both sum each row in CSR order
+// with fma from 0 (bitwise the same A X as the block steps' SpMM).
+void spmm_plain(bminres_ctx* h, const Kfn& f, const int* rowptr, const int* col, const double* val, const double* X,
+                double* Y, long long n, cudaStream_t s, int tpw) {
+    K1Args a{rowptr, col, val, X, nullptr, Y, n, nullptr, nullptr, 0, 0, tpw};
+    if (f.k1a) {
+        int oa = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, (const void*)f.k1a, NT, 0);
+        const long long groups = (n + 3) / 4;   // >= one row group per warp
+        const long long g = std::min<long long>((long long)h->n_sm * std::max(1, oa), std::max(1ll, (groups + 7) / 8));
+        f.k1a<<<(unsigned)g, NT, 0, s>>>(a);
+        check_launch(h, "k1a_spmm(plain)");
+    } else {
+        f.k1plain<<<(unsigned)(h->nb4 > 0 ? h->nb4 : 4 * h->n_sm), NT, 0, s>>>(a);   // grid-stride
+        check_launch(h, "k1_spmm(plain)");
+    }
+}
+
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
@@ -714,8 +745,8 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
         const int slots[2] = {(sk + 2) % 3, sk};
         for (int s2 = 0; s2 < 2; ++s2) {
             const double* Tr = (const double*)((char*)h->st + offsetof(DevState, Tr)) + (size_t)slots[s2] * MAXP * MAXP;
-            k_materialize<<<grid_for(h, n * p, 256, 8 * h->n_sm), 256, 0, h->stream>>>(h->V[slots[s2]], Tr,
-                                                                                          h->scr[s2], n, p);
+            h->kf.mat<<<grid_for(h, n * p, 256, 8 * h->n_sm), 256, h->kf.smem_mat, h->stream>>>(
+                h->V[slots[s2]], Tr, h->scr[s2], n, p);
             check_launch(h, "k_materialize");
         }
         have_window = true;
@@ -843,7 +874,7 @@ void flush_updates(bminres_ctx* h, const StepPtrs& sp, long long n) {
 // Gram G = F^T F of a row-major n x p panel (one k_gram launch), copied to the host (synchronising).
 std::vector<double> panel_gram(bminres_ctx* h, const double* F, long long n, int p) {
     const int nb = grid_for(h, n, 64, std::min(NB_MAX, 2 * h->n_sm));
-    k_gram<<<nb, 256, 0, h->stream>>>(F, n, p, h->part, nb, h->gdev, h->dcnt + 2);
+    h->kf.gram<<<nb, 256, h->kf.smem_gram, h->stream>>>(F, n, p, h->part, nb, h->gdev, h->dcnt + 2);
     check_launch(h, "k_gram");
     allred(h, h->gdev, (long long)p * p, h->stream);
     std::vector<double> G((size_t)p * p);
@@ -892,11 +923,11 @@ bool fast_start(bminres_ctx* h, double* F, long long n, int p, std::vector<doubl
     double* U = h->V[0];   // free until block 3
     const int g = grid_for(h, n * p, 256, 8 * h->n_sm);
     upload_inverse(R1);
-    k_materialize<<<g, 256, 0, h->stream>>>(F, h->gdev + MAXP * MAXP, U, n, p);
+    h->kf.mat<<<g, 256, h->kf.smem_mat, h->stream>>>(F, h->gdev + MAXP * MAXP, U, n, p);
     check_launch(h, "k_materialize");
     if (!host_chol(panel_gram(h, U, n, p), p, 0.5, R2)) return false;
     upload_inverse(R2);
-    k_materialize<<<g, 256, 0, h->stream>>>(U, h->gdev + MAXP * MAXP, F, n, p);
+    h->kf.mat<<<g, 256, h->kf.smem_mat, h->stream>>>(U, h->gdev + MAXP * MAXP, F, n, p);
     check_launch(h, "k_materialize");
     CK(cudaMemsetAsync(U, 0, (size_t)n * p * sizeof(double), h->stream));
     std::fill(S.begin(), S.end(), 0.0);
@@ -1155,18 +1186,19 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         double* F = h->V[1];
         if (o.use_x0) {
             const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);
-            K1Args a{sp.rowptr, sp.col, sp.val, Xe, nullptr, F, n, h->st, nullptr, 0, 0, h->tpw};
-            h->kf.k1plain<<<h->nb4, NT, 0, h->stream>>>(a);
-            check_launch(h, "k1_spmm(plain)");
+            spmm_plain(h, h->kf, sp.rowptr, sp.col, sp.val, Xe, F, n, h->stream, h->tpw);
             k_sub_from<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(B, F, (long long)panel);
             check_launch(h, "k_sub_from");
         } else {
             CK(cudaMemcpyAsync(F, B, panel * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
         }
-        launch_colsq(h, F, nullptr, n, p, h->dsc);
         std::vector<double> f2(p);
-        CK(cudaMemcpyAsync(f2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        if (o.use_x0) {
+            launch_colsq(h, F, nullptr, n, p, h->dsc);
+            CK(cudaMemcpyAsync(f2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        }
         CK(cudaStreamSynchronize(h->stream));
+        if (!o.use_x0) f2 = b2;   // F0 = B (bitwise)
         for (int c = 0; c < p; ++c) {
             beta[c] = std::sqrt(b2[c]);
             f0n[c] = std::sqrt(f2[c]);
@@ -1359,9 +1391,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     {
         TimeMark tm(h, PH_RESID);
         const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);   // (V slots are free now)
-        K1Args a{sp.rowptr, sp.col, sp.val, Xe, nullptr, h->M[0], n, h->st, nullptr, 0, 0, h->tpw};
-        h->kf.k1plain<<<h->nb4, NT, 0, h->stream>>>(a);
-        check_launch(h, "k1_spmm(plain)");
+        spmm_plain(h, h->kf, sp.rowptr, sp.col, sp.val, Xe, h->M[0], n, h->stream, h->tpw);
         launch_colsq(h, B, h->M[0], n, p, h->dsc);
     }
     std::vector<double> r2(p);
@@ -1552,10 +1582,7 @@ int bminres_spmm(bminres_handle h, const bminres_csr* A, const double* X, double
         while (lp < lanes) lp <<= 1;
         const long long rpw = 32 / lp, ntiles = (n + rpw - 1) / rpw, warps = NT / 32;
         const int tpw = (int)std::max<long long>(4, (ntiles + warps * 65536 - 1) / (warps * 65536));
-        const long long ctas = std::max<long long>(1, (ntiles + warps * tpw - 1) / (warps * tpw));
-        K1Args a{A->row_ptr, A->col_idx, A->values, X, nullptr, Y, n, nullptr, nullptr, 0, 0, tpw};
-        f.k1plain<<<(unsigned)ctas, NT, 0, h->stream>>>(a);
-        check_launch(h, "k1_spmm(plain)");
+        spmm_plain(h, f, A->row_ptr, A->col_idx, A->values, X, Y, n, h->stream, tpw);
         CK(cudaStreamSynchronize(h->stream));
         return BMINRES_OK;
     } catch (Err& x) {

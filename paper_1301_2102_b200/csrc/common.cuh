@@ -516,6 +516,7 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
     double* sCo = sTp + P * P;
     double* sOm = sCo + P * MAXQ;
     const int pp = par ^ 1;                      // parity of block k-1
+    load_pp<P>(sTp, st->Tr[(sk + 2) % 3]);       // Tr_{k-1} (in flight with the totals)
     if (st->given_blk == k - 1) {
         load_pp<P>(sC, st->Ck[pp]);
         load_pp<P>(sTk, st->Tr[sk]);
@@ -535,7 +536,6 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
             for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[pp][t] = sCo[t];
         }
     }
-    load_pp<P>(sTp, st->Tr[(sk + 2) % 3]);       // Tr_{k-1}
     __syncthreads();
     smm_nn<P>(sTp, sC, sD, true);                // D = Tr_{k-1} C_{k-1}^T
     __syncthreads();

@@ -402,6 +402,136 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
 }
 
 
+// ------------------------------------------------------------------ start block on DMMA
+//
+// The start block's CholQR2 (eqn.init-QR, reading C13): the Gram F^T F of the n x p
+// panel and U = F R^{-1}, with the row-local products on DMMA (once per solve; they replace the
+// generic k_gram / k_materialize for p in {8, 16, 32}).
+
+template <int P>
+struct GramDSmem {
+    static constexpr int WARPS = 8, NS = 2;
+    static constexpr size_t bytes = sizeof(double) * (WARPS * NS * DM<P>::TILE + P * P);
+};
+
+// out = F^T F: per-CTA partials (part[e*nb + cta]), the last CTA sums them in fixed order
+template <int P>
+__global__ void __launch_bounds__(256) k_gram_dmma(const double* X, long long n, int, double* part, int nb, double* out,
+                                                   unsigned* cnt) {
+    using D = DM<P>;
+    using S = GramDSmem<P>;
+    constexpr int TR = D::TR, RS = D::RS, NC = D::NC, NS = S::NS, WARPS = S::WARPS, E = P * P;
+    extern __shared__ __align__(16) double dyng[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    double* wb = dyng + warp * NS * D::TILE;
+    double* sAcc = dyng + WARPS * NS * D::TILE;
+    const long long ntiles = (n + TR - 1) / TR;
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    auto issue = [&](long long it) {
+        const long long t = t0 + it * ts;
+        if (t < ntiles) stage_tile<P>(wb + (int)(it % NS) * D::TILE, X, t * TR, n, lane);
+        cp_commit();
+    };
+    double g[NC][NC][2];
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    issue(0);
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + 1);
+        cp_wait<1>();
+        __syncwarp();
+        const double* tl = wb + (int)(it % NS) * D::TILE;
+#pragma unroll
+        for (int k0 = 0; k0 < TR; k0 += 4) {
+            const double* rw = tl + (k0 + fc) * RS;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const double av = rw[i * 8 + fr];
+#pragma unroll
+                for (int j = 0; j <= i; ++j) dmma(g[i][j][0], g[i][j][1], av, rw[j * 8 + fr]);
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+    for (int w = 0; w < WARPS; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j) {
+                    frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w == 0, lane);
+                    if (j < i) frag_acc_t(sAcc, P, i * 8, j * 8, g[i][j], w == 0, lane);
+                }
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < E; e += blockDim.x) part[(size_t)e * nb + blockIdx.x] = sAcc[e];
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(cnt, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int e = warp; e < E; e += WARPS) {
+        double t = 0.0;
+        for (int b = lane; b < nb; b += 32) t += __ldcg(part + (size_t)e * nb + b);
+        t = warp_sum(t);
+        if (lane == 0) out[e] = t;
+    }
+    if (threadIdx.x == 0) *cnt = 0u;
+}
+
+// out = V Tr (n x P row-major panels; Tr P x P with leading dimension MAXP)
+template <int P>
+__global__ void __launch_bounds__(256) k_materialize_dmma(const double* V, const double* Tr, double* out, long long n,
+                                                          int) {
+    using D = DM<P>;
+    constexpr int TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, NS = 2, WARPS = 8;
+    extern __shared__ __align__(16) double dynm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    double* fT = dynm;
+    double* wb = fT + D::FR + warp * NS * D::TILE;
+    to_frag<P>(Tr, MAXP, 1.0, fT);
+    __syncthreads();
+    const long long ntiles = (n + TR - 1) / TR;
+    const long long t0 = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    auto issue = [&](long long it) {
+        const long long t = t0 + it * ts;
+        if (t < ntiles) stage_tile<P>(wb + (int)(it % NS) * D::TILE, V, t * TR, n, lane);
+        cp_commit();
+    };
+    issue(0);
+    for (long long it = 0; t0 + it * ts < ntiles; ++it) {
+        issue(it + 1);
+        cp_wait<1>();
+        __syncwarp();
+        const double* tl = wb + (int)(it % NS) * D::TILE;
+        const long long base = (t0 + it * ts) * TR;
+#pragma unroll
+        for (int mc = 0; mc < TR / 8; ++mc) {
+            const long long row = base + mc * 8 + fr;
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                    dmma(c0, c1, tl[(mc * 8 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
+                if (row < n) *reinterpret_cast<double2*>(out + row * P + nc * 8 + 2 * fc) = make_double2(c0, c1);
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+}
+template <int P>
+constexpr size_t mat_dmma_smem() { return sizeof(double) * (DM<P>::FR + 8 * 2 * DM<P>::TILE); }
+
 // ------------------------------------------------------------------ K1a: the SpMM alone (split mode)
 //
 // Row a1's operator product AV = A V_k (eqn.block-Lanczos-recurr's A u_j, applied to the
@@ -424,11 +554,11 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
     using C = PC<P>;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int CH = K1aCfg<P>::CH, KU = K1aCfg<P>::KU;
-    DevState* st = a.st;
-    unsigned long long* tr = trace_begin(st, TR_K1A);
+    DevState* st = a.st;   // null: plain SpMM (exit residual, bminres_spmm)
+    unsigned long long* tr = st ? trace_begin(st, TR_K1A) : nullptr;
     pdl_wait();   // V_k (K2 of block k-1) is complete and visible
     trace_pt(tr, 1);
-    if (!st->run_main) return;
+    if (st && !st->run_main) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
