@@ -544,16 +544,34 @@ constexpr size_t mat_dmma_smem() { return sizeof(double) * (DM<P>::FR + 8 * 2 * 
 // re-read from L2.
 template <int P>
 struct K1aCfg {
-    static constexpr int CH = P >= 32 ? 4 : 8;   // CSR entries per gather batch
-    static constexpr int KU = 8;                 // row groups per warp per CTA chunk
-    static constexpr int MINB = P >= 32 ? 6 : 5; // CTAs per SM (<= 40 / 48 registers)
+    // a lane gathers 32 bytes of a row per entry (one 256-bit load, LDG.E.ENL2.256) when 4 | p:
+    // half the lanes per row of the 16-byte mapping, so half the redundant column-index / value
+    // loads and address arithmetic per gathered byte (ncu: the 16-byte version issued 55-58%)
+    static constexpr int VEC = (P % 4 == 0) ? 4 : (P % 2 == 0 ? 2 : 1);
+    static constexpr int LANES = P / VEC;
+    static constexpr int LP = LANES <= 1 ? 1 : LANES <= 2 ? 2 : LANES <= 4 ? 4 : LANES <= 8 ? 8 : LANES <= 16 ? 16 : 32;
+    static constexpr int RPW = 32 / LP;
+    static constexpr int CH = VEC == 4 ? 4 : 8;   // CSR entries per gather batch
+    static constexpr int KU = 8;                  // row groups per warp per CTA chunk
+    static constexpr int MINB = 5;                // CTAs per SM (<= 48 registers)
 };
+
+template <int VEC>
+__device__ __forceinline__ void ldg_vec(const double* p, double (&r)[VEC]) {
+    if constexpr (VEC == 4) {
+        asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                     : "l"(p));
+    } else {
+        ldv<VEC>(p, r);
+    }
+}
 
 template <int P>
 __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
-    using C = PC<P>;
+    using C = K1aCfg<P>;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
-    constexpr int CH = K1aCfg<P>::CH, KU = K1aCfg<P>::KU;
+    constexpr int CH = C::CH, KU = C::KU;
     DevState* st = a.st;   // null: plain SpMM (exit residual, bminres_spmm)
     unsigned long long* tr = st ? trace_begin(st, TR_K1A) : nullptr;
     pdl_wait();   // V_k (K2 of block k-1) is complete and visible
@@ -588,7 +606,7 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
 #pragma unroll
             for (int t = 0; t < CH; ++t) {
                 if (c[t] >= 0) {
-                    ldv<VEC>(a.X + (long long)c[t] * P + c0, xv[t]);
+                    ldg_vec<VEC>(a.X + (long long)c[t] * P + c0, xv[t]);
                 } else {
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
@@ -601,7 +619,15 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
                     for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
                 }
         }
-        if (live) stv<VEC>(a.Y + i * P + c0, acc);   // Y = the AV panel
+        if (live) {
+            double* y = a.Y + i * P + c0;   // Y = the AV panel
+            if constexpr (VEC == 4) {
+                *reinterpret_cast<double2*>(y) = make_double2(acc[0], acc[1]);
+                *reinterpret_cast<double2*>(y + 2) = make_double2(acc[2], acc[3]);
+            } else {
+                stv<VEC>(y, acc);
+            }
+        }
         cpos += nw;
         if (cpos >= chunk) {
             cpos = warp;
