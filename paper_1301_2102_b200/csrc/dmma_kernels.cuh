@@ -556,6 +556,14 @@ struct K1aCfg {
     static constexpr int MINB = 5;                // CTAs per SM (<= 48 registers)
 };
 
+template <int P>
+struct K1Gather {
+    static constexpr int VEC = P == 16 ? 4 : PC<P>::VEC;
+    static constexpr int LANES = P / VEC;
+    static constexpr int LP = LANES <= 1 ? 1 : LANES <= 2 ? 2 : LANES <= 4 ? 4 : LANES <= 8 ? 8 : LANES <= 16 ? 16 : 32;
+    static constexpr int RPW = 32 / LP;
+};
+
 template <int VEC>
 __device__ __forceinline__ void ldg_vec(const double* p, double (&r)[VEC]) {
     if constexpr (VEC == 4) {
@@ -669,7 +677,9 @@ struct K1DSmem {
 template <int P, bool PRE = false>
 __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dmma(K1Args a) {
     using D = DM<P>;
-    using C = PC<P>;
+    // gather mapping: 32 bytes per lane and entry (256-bit loads) at p = 16 (95k vs 86k it/s at
+    // config 3); 16 bytes at p = 8 and 32, where the wider batch spills at 128 registers
+    using C = K1Gather<P>;
     using KS = K1DSmem<P, PRE>;
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
@@ -759,7 +769,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
 #pragma unroll
         for (int t = 0; t < CH; ++t) {
             if (cc[t] >= 0) {
-                ldv<VEC>(a.X + (long long)cc[t] * P + c0, xv[t]);
+                ldg_vec<VEC>(a.X + (long long)cc[t] * P + c0, xv[t]);
             } else {
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
@@ -789,7 +799,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
 #pragma unroll
             for (int t = 0; t < CH; ++t) {
                 if (c2[t] >= 0) {
-                    ldv<VEC>(a.X + (long long)c2[t] * P + c0, xv[t]);
+                    ldg_vec<VEC>(a.X + (long long)c2[t] * P + c0, xv[t]);
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) acc[v] = fma(a2[t], xv[t][v], acc[v]);
                 }
