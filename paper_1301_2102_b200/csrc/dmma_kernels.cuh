@@ -558,7 +558,7 @@ struct K1aCfg {
 
 template <int P>
 struct K1Gather {
-    static constexpr int VEC = P == 16 ? 4 : PC<P>::VEC;
+    static constexpr int VEC = (P == 16 || P == 8) ? 4 : PC<P>::VEC;
     static constexpr int LANES = P / VEC;
     static constexpr int LP = LANES <= 1 ? 1 : LANES <= 2 ? 2 : LANES <= 4 ? 4 : LANES <= 8 ? 8 : LANES <= 16 ? 16 : 32;
     static constexpr int RPW = 32 / LP;
@@ -677,14 +677,16 @@ struct K1DSmem {
 template <int P, bool PRE = false>
 __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dmma(K1Args a) {
     using D = DM<P>;
-    // gather mapping: 32 bytes per lane and entry (256-bit loads) at p = 16 (95k vs 86k it/s at
-    // config 3); 16 bytes at p = 8 and 32, where the wider batch spills at 128 registers
+    // gather mapping: 32 bytes per lane and entry (256-bit loads) at p = 8 and 16 (config 2:
+    // 108.8k -> 112.8k it/s; config 3: 86k -> 95k); 16 bytes at p = 32 (spills at 128 registers)
     using C = K1Gather<P>;
     using KS = K1DSmem<P, PRE>;
     constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int E = P * P + P;
-    constexpr int CH = P <= 8 ? 8 : 4;
+    // CSR entries per gather batch: 7 at p = 8 (a 7-point stencil row in one batch, 28 doubles in
+    // flight per lane at 128 registers; 8 spills), 4 at p = 16 / 32
+    constexpr int CH = P <= 8 ? 7 : 4;
     constexpr int G = TR / RPW;   // row groups per tile
     DevState* st = a.st;
     unsigned long long* tr = trace_begin(st, TR_K1);
