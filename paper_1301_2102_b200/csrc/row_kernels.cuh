@@ -19,9 +19,31 @@ __host__ __device__ __forceinline__ unsigned bulk_bytes(long long rows, int p) {
     return (unsigned)((rows * p * 8 + 15) & ~15ll);
 }
 
+// p = 8: a thread's row is 64 B, so the 32 rows a warp reads in one instruction fall on two
+// 16-byte bank groups (16-way conflict).  The chunk order is rotated by (lane >> 1) & 3: in each
+// instruction lanes 0..7 touch 8 distinct bank groups (4 wavefronts, the minimum for 16-byte
+// accesses), and the chunks are put back in place with selects (no dynamic register indexing).
+__device__ __forceinline__ double2 sel4(const double2 (&t)[4], int k) {
+    double2 x = t[3];
+    x = k == 2 ? t[2] : x;
+    x = k == 1 ? t[1] : x;
+    x = k == 0 ? t[0] : x;
+    return x;
+}
 template <int P>
 __device__ __forceinline__ void row_ld(const double* s, double (&r)[P]) {
-    if constexpr (P % 2 == 0) {
+    if constexpr (P == 8) {
+        const int rot = (threadIdx.x >> 1) & 3;
+        double2 t[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) t[c] = *reinterpret_cast<const double2*>(s + 2 * ((c + rot) & 3));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double2 x = sel4(t, (j - rot) & 3);
+            r[2 * j] = x.x;
+            r[2 * j + 1] = x.y;
+        }
+    } else if constexpr (P % 2 == 0) {
 #pragma unroll
         for (int c = 0; c < P / 2; ++c) {
             const double2 v = *reinterpret_cast<const double2*>(s + 2 * c);
@@ -35,7 +57,14 @@ __device__ __forceinline__ void row_ld(const double* s, double (&r)[P]) {
 }
 template <int P>
 __device__ __forceinline__ void row_st(double* s, const double (&r)[P]) {
-    if constexpr (P % 2 == 0) {
+    if constexpr (P == 8) {   // rotated chunk order (see row_ld)
+        const int rot = (threadIdx.x >> 1) & 3;
+        double2 t[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = make_double2(r[2 * j], r[2 * j + 1]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) *reinterpret_cast<double2*>(s + 2 * ((c + rot) & 3)) = sel4(t, (c + rot) & 3);
+    } else if constexpr (P % 2 == 0) {
 #pragma unroll
         for (int c = 0; c < P / 2; ++c) *reinterpret_cast<double2*>(s + 2 * c) = make_double2(r[2 * c], r[2 * c + 1]);
     } else {
