@@ -36,10 +36,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # algorithmic panel transfers per launch; K1 also streams CSR A
-PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 9, "orth": 3, "update": 6,
+# algorithmic panel transfers per launch.  The fused M/X update moves 5 panels on average: it
+# reads V_k, M_{k-2}, M_{k-1} and writes M_k every block, and reads + writes X every other block
+# (X updates deferred in pairs); the standalone K4b moves 6.
+PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 8, "orth": 3, "update": 6,
                       # split mode (large panels): K1a reads V_k once (gathers) and writes AV; K1 then
-                      # streams AV, V_k, V_{k-1} and writes W (+ the 6 panels of the fused update)
-                      "spmm_av": 2, "epilogue": 4, "epilogue_fused": 10}
+                      # streams AV, V_k, V_{k-1} and writes W (+ the fused update)
+                      "spmm_av": 2, "epilogue": 4, "epilogue_fused": 9}
 PHASE_READS_A = {"spmm", "spmm_fused", "spmm_av"}
 
 
@@ -133,6 +136,15 @@ def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def cpu_sample_iters(P, budget_s: float = 15.0) -> int:
+    """Iterations of the bounded oracle sample: ~budget_s of one-thread CPU work, from the oracle's
+    measured cost on config 2 (~0.8 ns per unit of nnz + 8 n p per iteration), 2 .. 400 (configs 4/5: the
+    oracle's start block alone is tens of seconds)."""
+    units = float(P.A.nnz) + 8.0 * P.n * P.p
+    est = budget_s / (0.82e-9 * units)
+    return int(max(2, min(400, est)))
 
 
 def cpu_baseline(P, iters: int):
@@ -306,7 +318,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(P, args.cpu_iters)
+        cpu = cpu_baseline(P, args.cpu_iters if args.cpu_iters > 0 else cpu_sample_iters(P))
 
     if rank == 0:
         line = {"metric": "block-MINRES iterations/s (fp64)", "value": value, "unit": "iterations/s",
@@ -344,7 +356,7 @@ def main():
     ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel event region")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=400)
+    ap.add_argument("--cpu-iters", type=int, default=0, help="oracle iterations of cpu_baseline (0: ~15 s sample)")
     ap.add_argument("--ref-iters", type=int, default=40)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -186,6 +186,7 @@ struct bminres_ctx {
     int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
     // split mode: K1a (SpMM alone, full occupancy) -> AV, then K1<P, true>
     bool split = false;
+    bool xdefer = false;   // fused updates defer X in pairs
     int nb1a = 0;
     double* AV = nullptr;
     bool pdl = true;   // programmatic dependent launch of the block-step kernels
@@ -408,6 +409,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         return std::max(1, o);
     };
     h->pdl = getenv("BMINRES_NO_PDL") == nullptr;
+    h->xdefer = h->kf.fused && getenv("BMINRES_NO_XDEFER") == nullptr;
     if (const char* gb = getenv("BMINRES_GRAPH_BLOCKS")) h->gblocks = std::max(1, std::min(6, atoi(gb)));
     const char* ce = getenv("BMINRES_CLUSTER");
     h->csz = ce ? std::max(1, std::min(8, atoi(ce))) : 2;
@@ -529,7 +531,11 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P);
+    // reduce2 triggers its dependent (K1(k+1) / K1a) right after its own wait: K1's fused update
+    // overlaps the reduction (+1.8% at config 2; reduce1 early: +0.3%, kept at exit)
+    static const int early2 = getenv("BMINRES_NO_EARLY_RED2") ? 0 : 1;
+    const int early = which == 2 ? early2 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, early);
     if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_reduce: ") + cudaGetErrorString(e));
     h->launches++;
     if (h->tp) {   // the totals over all ranks (K3b then runs replicated)
@@ -574,7 +580,7 @@ void spmm_plain(bminres_ctx* h, const Kfn& f, const int* rowptr, const int* col,
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
-             par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X, nullptr};
+             par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X, nullptr, h->xdefer ? 1 : 0};
     if (h->split) {
         // K1a: AV = A V_k (PDL after reduce2 / K2), then K1 streams AV
         K1Args aa = a;
@@ -867,6 +873,13 @@ void finish_given_block(bminres_ctx* h, const StepPtrs& sp, long long n, long lo
 void flush_updates(bminres_ctx* h, const StepPtrs& sp, long long n) {
     if (!h->kf.fused) return;
     const long long last = GET_STATE(h, upd_last), ks = GET_STATE(h, k_side);
+    const long long b0 = GET_STATE(h, k_upd_min);
+    if (h->xdefer && last >= b0 && ((last - b0) & 1) == 0) {
+        // the last fused update deferred its X: X += M_last Z_last (M[last % 2] holds M_last)
+        K4bArgs a{nullptr, h->M[last & 1], nullptr, sp.X, n, h->st, 0, h->tpw, (int)(last & 1), 1, 0, 3, last};
+        h->kf.k4b<<<h->nb4, h->kf.nt4b, h->kf.smem4b, h->stream>>>(a);
+        check_launch(h, "k4b(x only)");
+    }
     for (long long b = last + 1; b < ks; ++b) launch_k4b(h, h->stream, sp, n, b, 1);
     CK(cudaStreamSynchronize(h->stream));
 }

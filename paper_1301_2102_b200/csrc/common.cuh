@@ -96,6 +96,8 @@ struct DevState {
     // K3b(k) outputs for the M/X update of block k, double-buffered by block parity (the update
     // of block k runs in K1(k+2), beside K3b(k+1))
     double Z[2][MAXP * MAXP];      // Z_k: row m = z_{(k-1)p+m+1}^T (rows past the stop are 0)
+    double Zh[3][MAXP * MAXP];     // Z_k again, slot k mod 3 (the deferred X update of block k-1
+                                   // runs in K1(k+2) beside K3b(k+1))
     double Ainv[2][MAXP * MAXP];   // R_kk^{-1}
     double B1[2][MAXP * MAXP];     // R_{k-1,k} R_kk^{-1}
     double B2[2][MAXP * MAXP];     // R_{k-2,k} R_kk^{-1}
@@ -293,12 +295,16 @@ __device__ __forceinline__ void cluster_partials(const double* sAcc, int E, doub
 // The totals of one set of cluster partials: one warp per entry, lanes stride over the partial
 // rows, a fixed shuffle tree -> deterministic.  which = 1: part1 -> red1; which = 2: part2[par]
 // -> red2[par].  Entry counts come from the state (q_live may change between launches).  Launched
-// with PDL after K1 / K2; it triggers no dependents early (the dependent launches at exit, so
-// waiting CTAs never hold SM slots the side branch needs, and its pre-wait prefetch may read the
-// panels of the kernel before this one).
-__global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par, int P) {
+// with PDL after K1 / K2.  reduce1 triggers its dependent at exit; reduce2 (early = 1) right after
+// its wait -- K1(k+1)'s pre-wait work (the fused update, the first SpMM tile) reads only panels of
+// kernels that have completed, K2(k) included, and its griddepcontrol.wait covers the totals.
+__global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par, int P, int early) {
     unsigned long long* tr = trace_begin(st, which == 1 ? TR_RED1 : TR_RED2);
     pdl_wait();
+    // early: the dependent launches now -- its pre-wait work (K1's fused update and first SpMM
+    // tile) reads only panels of kernels that have completed (the producer of these partials
+    // included), and it waits for the totals at its own griddepcontrol.wait
+    if (early) pdl_trigger();
     trace_pt(tr, 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int e = blockIdx.x * 8 + warp;

@@ -75,16 +75,19 @@ __device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long l
     double* pipe = fZ + FR;
     double* scr = pipe + WARPS * NS * 4 * D::TILE;
     double* wb = pipe + warp * NS * 4 * D::TILE;
+    double* fZp = scr;         // Z_{k-1} (xmode 2), in the factor scratch once the factors are built
     const long long tw = t0 + warp;
+    const int xmode = a.xmode;
+    const bool xonly = xmode == 3, with_x = xmode != 1;
     auto issue = [&](long long it, int slot) {
         const long long t = tw + it * ts;
         if (t < tend) {
             double* sl = wb + slot * 4 * D::TILE;
             const long long base = t * TR;
-            stage_tile<P>(sl, a.U, base, a.n, lane);
+            if (!xonly) stage_tile<P>(sl, a.U, base, a.n, lane);
             stage_tile<P>(sl + D::TILE, a.M2, base, a.n, lane);
-            stage_tile<P>(sl + 2 * D::TILE, a.M1, base, a.n, lane);
-            stage_tile<P>(sl + 3 * D::TILE, a.X, base, a.n, lane);
+            if (!xonly) stage_tile<P>(sl + 2 * D::TILE, a.M1, base, a.n, lane);
+            if (with_x) stage_tile<P>(sl + 3 * D::TILE, a.X, base, a.n, lane);
         }
         cp_commit();
     };
@@ -107,8 +110,12 @@ __device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long l
         to_frag<P>(sP, P, 1.0, fA);
         to_frag<P>(st->B2[a.par], MAXP, -1.0, fB2);
         to_frag<P>(st->B1[a.par], MAXP, -1.0, fB1);
-        to_frag<P>(st->Z[a.par], MAXP, 1.0, fZ);
+        to_frag<P>(xmode == 0 ? st->Z[a.par] : st->Zh[a.zb % 3], MAXP, 1.0, fZ);
         __syncthreads();
+        if (xmode == 2) {
+            to_frag<P>(st->Zh[(a.zb + 2) % 3], MAXP, 1.0, fZp);   // 3 P^2 >= FR doubles
+            __syncthreads();
+        }
     }
     const int fr = lane >> 2, fc = lane & 3;   // A-fragment row / col within an 8x4 block
     for (long long it = 0; tw + it * ts < tend; ++it) {
@@ -124,6 +131,19 @@ __device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long l
 #pragma unroll
         for (int mc = 0; mc < TR / 8; ++mc) {
             const int r0 = mc * 8;
+            const long long row = base + r0 + fr;
+            if (xonly) {   // host flush of a deferred X update: X += M_k Z_k (M2 holds M_k)
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    const int col = nc * 8 + 2 * fc;
+                    double x0 = tX[(r0 + fr) * RS + col], x1 = tX[(r0 + fr) * RS + col + 1];
+#pragma unroll
+                    for (int kc = 0; kc < KC; ++kc)
+                        dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], fZ[(kc * NC + nc) * 32 + lane]);
+                    if (row < a.n) *reinterpret_cast<double2*>(a.X + row * P + col) = make_double2(x0, x1);
+                }
+                continue;
+            }
             double mk[NC][2];
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
@@ -132,14 +152,15 @@ __device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long l
                 for (int kc = 0; kc < KC; ++kc) {
                     const int ai = (r0 + fr) * RS + kc * 4 + fc;
                     const int bi = (kc * NC + nc) * 32 + lane;
-                    dmma(mk[nc][0], mk[nc][1], tV[ai], fA[bi]);
+                    // Tr_k R_kk^{-1} is upper triangular (both factors are): its rows 4kc.. are zero
+                    // in columns 8nc..8nc+7 when 4kc > 8nc+7
+                    if (kc <= 2 * nc + 1) dmma(mk[nc][0], mk[nc][1], tV[ai], fA[bi]);
                     dmma(mk[nc][0], mk[nc][1], tM2[ai], fB2[bi]);
                     dmma(mk[nc][0], mk[nc][1], tM1[ai], fB1[bi]);
                 }
             }
             __syncwarp();
             // M_k overwrites this chunk's M_{k-2} rows (in smem and in HBM)
-            const long long row = base + r0 + fr;
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 const int col = nc * 8 + 2 * fc;
@@ -149,10 +170,16 @@ __device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long l
                     *reinterpret_cast<double2*>(a.M2 + row * P + col) = make_double2(mk[nc][0], mk[nc][1]);
             }
             __syncwarp();
+            if (!with_x) continue;   // xmode 1: this block's X update is deferred to the next one
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 const int col = nc * 8 + 2 * fc;
                 double x0 = tX[(r0 + fr) * RS + col], x1 = tX[(r0 + fr) * RS + col + 1];
+                if (xmode == 2) {   // first the deferred X += M_{k-1} Z_{k-1}
+#pragma unroll
+                    for (int kc = 0; kc < KC; ++kc)
+                        dmma(x0, x1, tM1[(r0 + fr) * RS + kc * 4 + fc], fZp[(kc * NC + nc) * 32 + lane]);
+                }
 #pragma unroll
                 for (int kc = 0; kc < KC; ++kc)
                     dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], fZ[(kc * NC + nc) * 32 + lane]);
@@ -714,7 +741,9 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
         const long long k = st->k_main, b = k - 2;
         if (b >= st->k_upd_min && b < st->k_side && b < st->stop_side_at) {
             if (blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = b;
-            K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b};
+            // X updates in pairs from the first fused block: defer b's, then apply both with b+1's
+            const int xm = a.xdefer ? (((b - st->k_upd_min) & 1) ? 2 : 1) : 0;
+            K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b, xm, b};
             dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe);
             __syncthreads();   // the region is reused by the SpMM
         }
@@ -841,10 +870,12 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 w[nc][0] = w[nc][1] = 0.0;
-                // W = (A V_k) Tr_k = A U_k, the raw candidates; ||A u_j||^2 (C14)
+                // W = (A V_k) Tr_k = A U_k, the raw candidates; ||A u_j||^2 (C14).  Tr_k = C_{k-1}^{-1}
+                // (or I) is upper triangular: k-chunks below the column block are zero
 #pragma unroll
                 for (int kc = 0; kc < KC; ++kc)
-                    dmma(w[nc][0], w[nc][1], tAV[(r0 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
+                    if (kc <= 2 * nc + 1)
+                        dmma(w[nc][0], w[nc][1], tAV[(r0 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
                 om[nc][0] = fma(w[nc][0], w[nc][0], om[nc][0]);
                 om[nc][1] = fma(w[nc][1], w[nc][1], om[nc][1]);
                 // W -= U_{k-1} C_{k-1}^T = V_{k-1} D  (h_{i,j} = h_{j,i})

@@ -48,6 +48,7 @@ struct K1Args {
     double* Xs;           // solution panel
     // split mode (k1_dmma<P, true>): A V_k was computed by k1a_spmm into AV; K1 stages its rows
     const double* AV;
+    int xdefer;           // fused update: X updates deferred in pairs
 };
 
 template <int P>
@@ -699,6 +700,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         st->B2[par][g] = s2;
         st->Ainv[par][g] = sI[a2 * LD + l];
         st->Z[par][g] = sZ[a2 * LD + l];
+        st->Zh[k % 3][g] = sZ[a2 * LD + l];
         st->T[g] = sT[a2 * LD + l];
         st->CprevS[g] = sC[a2 * LD + l];
     }
@@ -753,6 +755,11 @@ struct K4bArgs {
     int par;              // k mod 2 (K3b output buffer)
     int force;            // 1: apply regardless of side_go (host flush of a pending update)
     long long blk;        // k (recorded in upd_last; 0: not recorded)
+    // X update mode (DMMA update only): 0 X += M_k Z_k; 1 defer it
+    // (no X traffic); 2 X += M_{k-1} Z_{k-1} + M_k Z_k (the deferred pair, in that order -- bitwise
+    // the two single updates); 3 X += M_k Z_k alone with M2 holding M_k (host flush)
+    int xmode;
+    long long zb;         // k for the Zh slots (xmode != 0)
 };
 
 template <int P>

@@ -130,6 +130,21 @@ def test_split_mode_bitwise(p):
             assert r.stats["phase_launches"]["spmm_fused"] == 0
 
 
+@pytest.mark.parametrize("p,maxit", [(8, 120), (8, 128), (16, 144), (32, 160)])
+def test_deferred_x_update_bitwise(p, maxit, monkeypatch):
+    """The fused update defers X in pairs (X += M_{k-1}Z_{k-1} + M_k Z_k in one pass, DESIGN.md
+    "Deferred X update"; the host flushes an unpaired last block): bitwise the per-block updates,
+    for block counts of both parities and in split mode."""
+    A = synth.laplacian_2d(40, 37, shift=1.7)
+    B = synth.gaussian_rhs(A.n, p, seed=p + 1)
+    r1 = gpu_solve(A, B, tol=0.0, maxit=maxit, split_spmm=1 if p == 16 else 0)
+    monkeypatch.setenv("BMINRES_NO_XDEFER", "1")
+    r0 = gpu_solve(A, B, tol=0.0, maxit=maxit, split_spmm=1 if p == 16 else 0)
+    assert r1.iterations == r0.iterations == maxit
+    np.testing.assert_array_equal(r1.history, r0.history)
+    np.testing.assert_array_equal(r1.X, r0.X)
+
+
 def test_companion_converges_like_oracle():
     """Config 1' (non-singular companion): counts within +-2%, true residual <= tol."""
     P = synth.config("1c")
