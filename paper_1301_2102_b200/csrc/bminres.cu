@@ -46,6 +46,7 @@ struct Kfn {  // per-p kernel table
     void (*k1pre)(K1Args);   // split mode: K1 streaming A V_k
     size_t smem1pre;
     // start block / exit residual: Gram, V R^{-1}, plain SpMM (DMMA / K1a versions for p = 8, 16, 32)
+    void (*red2f)(DevState*, int);   // reduce2 + factorisation for the DMMA K1 (null: k_reduce)
     void (*gram)(const double*, long long, int, double*, int, double*, unsigned*);
     void (*mat)(const double*, const double*, double*, long long, int);
     size_t smem_gram, smem_mat;
@@ -64,6 +65,7 @@ Kfn make_kfn(int q) {
     f.k1a = nullptr;
     f.k1pre = nullptr;
     f.smem1pre = 0;
+    f.red2f = nullptr;
     f.gram = k_gram;
     f.mat = k_materialize;
     f.smem_gram = f.smem_mat = 0;
@@ -83,6 +85,7 @@ Kfn make_kfn(int q) {
             f.nt1 = K1DSmem<P>::WARPS * 32;
             f.k1a = k1a_spmm<P>;
             f.k1pre = k1_dmma<P, true>;
+            if constexpr (P <= 16) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;   // (static smem)
             f.smem1pre = K1DSmem<P, true>::bytes;
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
@@ -186,6 +189,7 @@ struct bminres_ctx {
     int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
     // split mode: K1a (SpMM alone, full occupancy) -> AV, then K1<P, true>
     bool split = false;
+    bool red2_fac = false;   // reduce2 factors the new block once (k_red2f)
     bool xdefer = false;   // fused updates defer X in pairs
     int nb1a = 0;
     double* AV = nullptr;
@@ -535,7 +539,9 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     // overlaps the reduction (+1.8% at config 2; reduce1 early: +0.3%, kept at exit)
     static const int early2 = getenv("BMINRES_NO_EARLY_RED2") ? 0 : 1;
     const int early = which == 2 ? early2 : 0;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, early);
+    cudaError_t e = (which == 2 && h->red2_fac)
+                        ? cudaLaunchKernelEx(&cfg, h->kf.red2f, h->st, (int)(k & 1))
+                        : cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, early);
     if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_reduce: ") + cudaGetErrorString(e));
     h->launches++;
     if (h->tp) {   // the totals over all ranks (K3b then runs replicated)
@@ -670,7 +676,7 @@ void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n,
 // update of block s-1 and the side branch is K3b alone.
 void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
     const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->V[0], h->M[0], (const void*)(intptr_t)n,
-                          (const void*)(intptr_t)(h->p_ws * 16 + h->gblocks)};
+                          (const void*)(intptr_t)((h->p_ws * 16 + h->gblocks) * 2 + (h->red2_fac ? 1 : 0))};
     bool same = h->gexec[0] && std::equal(key, key + 8, h->gkey);
     if (same) return;
     for (int q = 0; q < 6; ++q) {
@@ -1163,6 +1169,11 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     init.part2[1] = h->part2[1];
     init.ncl1 = h->nb1 / h->csz;
     init.ncl2 = h->nb2 / h->csz;
+    // reduce2 factors the new block once (single rank: a partition's totals are allreduced after
+    // the reduce kernel, so each rank's K1 factors them itself)
+    h->red2_fac = h->kf.red2f && !h->tp && !getenv("BMINRES_NO_RED2F");
+    init.red2_fac = h->red2_fac ? 1 : 0;
+    init.fac_bad = 0;
     init.given_blk = -1;
     init.k_upd_min = KINF;
     init.upd_last = 0;

@@ -81,7 +81,12 @@ struct DevState {
     long long maxit;
     long long hist_cap;
     double tol, tau;
-    unsigned cnt1, cnt2, cnt3, cnt4;   // tickets of the cluster reductions
+    unsigned cnt1, cnt2, cnt3, cnt4;   // tickets (cnt2: k_red2f's last CTA)
+    // k_red2f (single rank): reduce2's last CTA factors the new block once -- C_k, Tr_{k+1},
+    // coef_k in the state, and K1(k+1)'s fragments of Tr_{k+1} and -(Tr_k C_k^T) below; fac_bad:
+    // breakdown / cancellation of the block (published as by K1's own prologue)
+    int red2_fac, fac_bad;
+    double fT[MAXP * MAXP], fD[MAXP * MAXP];
     // ---- written by the main branch, double-buffered by block parity
     double G[2][MAXP * MAXP];      // G(a,m) = u_{(k-1)p+a}^T w_m (K1, after the known subtraction)
     double om2[2][MAXP];           // ||A u_j||^2, raw candidate norms (C14)
@@ -546,6 +551,89 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
     smm_nn<P>(sTp, sC, sD, true);                // D = Tr_{k-1} C_{k-1}^T
     __syncthreads();
     return true;
+}
+
+// reduce2 with the factorisation (red2_fac, single rank): the totals of K2(k)'s partials as
+// k_reduce computes them (same order), then the last CTA to finish (ticket) factors the new block
+// exactly as K1(k+1)'s prologue would -- factor_block on the totals, C_k, Tr_{k+1} = C_k^{-1},
+// coef_k, D = Tr_k C_k^T -- and stores Tr_{k+1} and -D in fragment order (to_frag of the DMMA K1),
+// so K1(k+1), which launches at this kernel's early trigger and runs its fused update meanwhile,
+// only loads them.  k = k_main - 1 (K2(k) advanced k_main).
+template <int P, int FRN, int NCF>
+__global__ void __launch_bounds__(256) k_red2f(DevState* st, int par) {
+    unsigned long long* tr = trace_begin(st, TR_RED2);
+    pdl_wait();
+    pdl_trigger();   // K1(k+1) may launch now (see k_reduce's early trigger)
+    trace_pt(tr, 1);
+    if (!st->run_main) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Q = st->q_live;
+    const int E = P * P + Q * P;
+    const int ncl = st->ncl2;
+    const double* part = st->part2[par];
+    for (int e = blockIdx.x * 8 + warp; e < E; e += gridDim.x * 8) {
+        constexpr int U = 8;
+        double s = 0.0;
+        for (int b0 = 0; b0 < ncl; b0 += 32 * U) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int b = b0 + lane + 32 * u;
+                v[u] = b < ncl ? __ldcg(part + (size_t)b * E + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b0 + lane + 32 * u < ncl) s += v[u];
+        }
+        s = warp_sum(s);
+        if (lane == 0) st->red2[par][e] = s;
+    }
+    // last CTA: factor
+    __shared__ int s_last;
+    __shared__ double sm[P * P + MAXQ * P + 3 * P * P + P * MAXQ + P + 2 * P * P];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&st->cnt2, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) st->cnt2 = 0u;
+    double* sRed = sm;                           // totals (P*P + MAXQ*P)
+    double* sC = sRed + P * P + MAXQ * P;
+    double* sCi = sC + P * P;
+    double* sTp = sCi + P * P;
+    double* sCo = sTp + P * P;
+    double* sOm = sCo + P * MAXQ;
+    double* sD = sOm + P;
+    const long long k = st->k_main - 1;
+    const int sk1 = (int)((k + 1) % 3), sk = (int)(k % 3);
+    for (int t = threadIdx.x; t < E; t += blockDim.x) sRed[t] = __ldcg(st->red2[par] + t);
+    for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
+    load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
+    __syncthreads();
+    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo);
+    if (bad) {
+        if (threadIdx.x == 0) {
+            st->fac_bad = 1;
+            publish_breakdown(st, k);
+        }
+        trace_pt(tr, 5);
+        return;
+    }
+    store_pp<P>(st->Ck[par], sC);
+    store_pp<P>(st->Tr[sk1], sCi);
+    for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[par][t] = sCo[t];
+    smm_nn<P>(sTp, sC, sD, true);                // D = Tr_k C_k^T
+    __syncthreads();
+    // fragment order of the DMMA K1 (to_frag: 4 x 8 blocks, KC = P/4 k-chunks, NCF = P/8 n-chunks)
+    for (int t = threadIdx.x; t < FRN; t += blockDim.x) {
+        const int blk = t / 32, l = t % 32, kc = blk / NCF, nc = blk % NCF;
+        const int r = kc * 4 + l % 4, c = nc * 8 + l / 4;
+        st->fT[t] = sCi[r * P + c];
+        st->fD[t] = -sD[r * P + c];
+    }
+    if (threadIdx.x == 0) st->fac_bad = 0;
+    trace_pt(tr, 5);
 }
 
 // K2 prologue, block k: G = Tr_k^T (V_k^T W) from K1's partials, om2; CTA 0 publishes G, om2 for

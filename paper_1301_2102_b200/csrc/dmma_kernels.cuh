@@ -849,6 +849,16 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
     };
     // ---- the prologue: C_{k-1} (Cholesky of K2(k-1)'s W'^T W' partials), Tr_k, D
     auto prologue = [&]() -> bool {
+        if (st->red2_fac && st->k_main > 1 && st->given_blk != st->k_main - 1) {
+            // reduce2 factored the block: load Tr_k and -D in fragment order
+            if (st->fac_bad) return false;   // (breakdown published by reduce2)
+            for (int t = threadIdx.x; t < FR; t += blockDim.x) {
+                fT[t] = st->fT[t];
+                fD[t] = st->fD[t];
+            }
+            __syncthreads();
+            return true;
+        }
         double* sTk = scr;
         double* sD = scr + P * P;
         if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, scr + 2 * P * P)) return false;
