@@ -46,7 +46,7 @@ struct Kfn {  // per-p kernel table
     void (*k1pre)(K1Args);   // split mode: K1 streaming A V_k
     size_t smem1pre;
     // start block / exit residual: Gram, V R^{-1}, plain SpMM (DMMA / K1a versions for p = 8, 16, 32)
-    void (*red2f)(DevState*, int);   // reduce2 + factorisation for the DMMA K1 (null: k_reduce)
+    void (*red2f)(DevState*, int, int);   // reduce2 + factorisation for the DMMA K1 (null: k_reduce)
     void (*gram)(const double*, long long, int, double*, int, double*, unsigned*);
     void (*mat)(const double*, const double*, double*, long long, int);
     size_t smem_gram, smem_mat;
@@ -85,7 +85,9 @@ Kfn make_kfn(int q) {
             f.nt1 = K1DSmem<P>::WARPS * 32;
             f.k1a = k1a_spmm<P>;
             f.k1pre = k1_dmma<P, true>;
-            if constexpr (P <= 16) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;   // (static smem)
+            // p = 8 only: the register Cholesky keeps the serial tail short (p = 16: 98.5k vs 96.2k it/s
+            // at config 3 without / with)
+            if constexpr (P <= 8) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
             f.smem1pre = K1DSmem<P, true>::bytes;
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
@@ -432,7 +434,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     if (h->split) {
         int oa = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, (const void*)h->kf.k1a, NT, 0);
-        h->nb1a = h->n_sm * std::max(1, oa);
+        h->nb1a = h->n_sm * std::max(1, oa) - 1;   // one CTA slot left for K3b (side stream)
         const int o1p = std::min(cap, occ_of((const void*)h->kf.k1pre, h->kf.nt1, h->kf.smem1pre));
         h->nb1 = (std::min(NB_MAX, h->n_sm * o1p) - (o1p > 1 ? h->csz : 0)) / h->csz * h->csz;
     }
@@ -537,10 +539,12 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     cfg.numAttrs = 1;
     // reduce2 triggers its dependent (K1(k+1) / K1a) right after its own wait: K1's fused update
     // overlaps the reduction (+1.8% at config 2; reduce1 early: +0.3%, kept at exit)
+    // (not in split mode: its dependent K1a has no pre-wait work, and its early-resident CTAs would
+    // take the SM slots K3b needs)
     static const int early2 = getenv("BMINRES_NO_EARLY_RED2") ? 0 : 1;
-    const int early = which == 2 ? early2 : 0;
+    const int early = (which == 2 && !h->split) ? early2 : 0;
     cudaError_t e = (which == 2 && h->red2_fac)
-                        ? cudaLaunchKernelEx(&cfg, h->kf.red2f, h->st, (int)(k & 1))
+                        ? cudaLaunchKernelEx(&cfg, h->kf.red2f, h->st, (int)(k & 1), early)
                         : cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, early);
     if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_reduce: ") + cudaGetErrorString(e));
     h->launches++;

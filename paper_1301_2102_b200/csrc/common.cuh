@@ -103,6 +103,10 @@ struct DevState {
     double Z[2][MAXP * MAXP];      // Z_k: row m = z_{(k-1)p+m+1}^T (rows past the stop are 0)
     double Zh[3][MAXP * MAXP];     // Z_k again, slot k mod 3 (the deferred X update of block k-1
                                    // runs in K1(k+2) beside K3b(k+1))
+    // the M/X update's DMMA factors in fragment order (p = 8, 16, 32), written by K3b(k): by block
+    // parity Tr_k R_kk^{-1}, -R_{k-2,k}R_kk^{-1}, -R_{k-1,k}R_kk^{-1}; Z_k by k mod 3
+    double uf[2][3][MAXP * MAXP];
+    double ufz[3][MAXP * MAXP];
     double Ainv[2][MAXP * MAXP];   // R_kk^{-1}
     double B1[2][MAXP * MAXP];     // R_{k-1,k} R_kk^{-1}
     double B2[2][MAXP * MAXP];     // R_{k-2,k} R_kk^{-1}
@@ -560,10 +564,10 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
 // so K1(k+1), which launches at this kernel's early trigger and runs its fused update meanwhile,
 // only loads them.  k = k_main - 1 (K2(k) advanced k_main).
 template <int P, int FRN, int NCF>
-__global__ void __launch_bounds__(256) k_red2f(DevState* st, int par) {
+__global__ void __launch_bounds__(256) k_red2f(DevState* st, int par, int early) {
     unsigned long long* tr = trace_begin(st, TR_RED2);
     pdl_wait();
-    pdl_trigger();   // K1(k+1) may launch now (see k_reduce's early trigger)
+    if (early) pdl_trigger();   // K1(k+1) may launch now (see k_reduce's early trigger)
     trace_pt(tr, 1);
     if (!st->run_main) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

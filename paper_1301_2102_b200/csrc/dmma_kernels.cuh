@@ -95,27 +95,22 @@ __device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long l
 #pragma unroll
     for (int s = 0; s < NS - 1; ++s) issue(s, s);
     {
-        double* sT = scr;
-        double* sR = scr + P * P;
-        double* sP = scr + 2 * P * P;
-        const double* Tk = st->Tr[a.sk];
-        for (int t = threadIdx.x; t < P * P; t += blockDim.x) {
-            const int g = (t / P) * MAXP + t % P;
-            sT[t] = Tk[g];
-            sR[t] = st->Ainv[a.par][g];
+        // K3b(k) left the factors in fragment order (one load instead of a p x p product and four
+        // reorderings on the critical path)
+        static_assert(FR == P * P, "fragment order of a p x p factor");
+        const double* zf = st->ufz[a.zb % 3];   // (xmode != 0)
+        for (int t = threadIdx.x; t < FR; t += blockDim.x) {
+            fA[t] = st->uf[a.par][0][t];
+            fB2[t] = st->uf[a.par][1][t];
+            fB1[t] = st->uf[a.par][2][t];
+            fZp[t] = xmode == 2 ? st->ufz[(a.zb + 2) % 3][t] : 0.0;   // 3 P^2 >= FR doubles
+        }
+        if (xmode == 0) {
+            to_frag<P>(st->Z[a.par], MAXP, 1.0, fZ);
+        } else {
+            for (int t = threadIdx.x; t < FR; t += blockDim.x) fZ[t] = zf[t];
         }
         __syncthreads();
-        cta_matmul_nn<P>(sT, P, sR, P, sP, P);
-        __syncthreads();
-        to_frag<P>(sP, P, 1.0, fA);
-        to_frag<P>(st->B2[a.par], MAXP, -1.0, fB2);
-        to_frag<P>(st->B1[a.par], MAXP, -1.0, fB1);
-        to_frag<P>(xmode == 0 ? st->Z[a.par] : st->Zh[a.zb % 3], MAXP, 1.0, fZ);
-        __syncthreads();
-        if (xmode == 2) {
-            to_frag<P>(st->Zh[(a.zb + 2) % 3], MAXP, 1.0, fZp);   // 3 P^2 >= FR doubles
-            __syncthreads();
-        }
     }
     const int fr = lane >> 2, fc = lane & 3;   // A-fragment row / col within an 8x4 block
     for (long long it = 0; tw + it * ts < tend; ++it) {

@@ -704,6 +704,22 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         st->T[g] = sT[a2 * LD + l];
         st->CprevS[g] = sC[a2 * LD + l];
     }
+    if constexpr (P % 8 == 0) {
+        // the update's factors in the DMMA fragment order (dmma_update loads them as they are):
+        // Tr_k Ainv in cta_matmul_nn's arithmetic order, -B2, -B1, Z_k
+        __syncthreads();   // B1 / B2 / Ainv of this block are in st
+        const double* Tk = st->Tr[k % 3];
+        for (int t = tid; t < P * P; t += K3T) {
+            const int blk = t / 32, l = t % 32, kc = blk / (P / 8), nc = blk % (P / 8);
+            const int r = kc * 4 + l % 4, c = nc * 8 + l / 4, g = r * MAXP + c;
+            double s = 0.0;
+            for (int i = 0; i < P; ++i) s = fma(Tk[r * MAXP + i], st->Ainv[par][i * MAXP + c], s);
+            st->uf[par][0][t] = s;
+            st->uf[par][1][t] = -st->B2[par][g];
+            st->uf[par][2][t] = -st->B1[par][g];
+            st->ufz[k % 3][t] = st->Zh[k % 3][g];
+        }
+    }
     for (int t = tid; t < W2 * (P + 1); t += K3T) {
         const int s = t / (P + 1), q = t % (P + 1);
         st->rv[s * (MAXP + 1) + q] = sV[s * (P + 2) + q];
