@@ -310,6 +310,49 @@ def test_invalid_arguments():
     assert gpu_solve(P.A, P.B, tol=float("nan"), maxit=10).status_name == "EINVAL"
 
 
+# ----------------------------------------------------------------------------- degenerate inputs
+
+
+def _same_as_oracle(A, B, *, tol, maxit, **kw):
+    r = gpu_solve(A, B, tol=tol, maxit=maxit, **kw)
+    ref = oracle.solve(A, B, tol=tol, maxit=maxit)
+    assert r.status_name == ref.status_name, (r.status_name, ref.status_name)
+    assert r.iterations == ref.iterations
+    if ref.status_name != "EINVAL":
+        assert_hist_close(r.history, ref.history)
+        same_events(r.events, ref.events)
+        np.testing.assert_allclose(r.X, ref.X, rtol=1e-7, atol=1e-9 * max(np.abs(ref.X).max(), 1.0))
+    return r, ref
+
+
+def test_zero_rhs_column():
+    """A zero right-hand side column: ||b_i|| = 0 counts as converged (reading C7) and its start
+    column is a step-0 exact event replaced by a random vector (C13, C17)."""
+    A = synth.laplacian_2d(40, 37, shift=1.7)
+    B = synth.gaussian_rhs(A.n, 4, seed=3)
+    B[:, 2] = 0.0
+    _same_as_oracle(A, B, tol=1e-8, maxit=120)
+
+
+def test_all_zero_rhs_and_maxit_zero():
+    """B = 0 converges at the start (X = 0, no iterations); maxit = 0 returns MAXIT at once."""
+    A = synth.laplacian_2d(40, 37, shift=1.7)
+    r, _ = _same_as_oracle(A, np.zeros((A.n, 4)), tol=1e-8, maxit=100)
+    assert r.iterations == 0 and not np.any(r.X)
+    _same_as_oracle(A, synth.gaussian_rhs(A.n, 4, seed=1), tol=1e-8, maxit=0)
+
+
+@pytest.mark.parametrize("n,p", [(1, 1), (8, 8), (5, 8), (24, 8), (40, 16)])
+def test_tiny_systems(n, p):
+    """n = 1; n = p (the block Krylov space is exhausted after one block -> EPOOL, P:718-726);
+    n < p (EINVAL, as the oracle); a few blocks on a dense random symmetric indefinite matrix."""
+    rng = np.random.default_rng(n * 100 + p)
+    D = rng.standard_normal((n, n))
+    A = synth.dense_to_csr(D + D.T)
+    B = rng.standard_normal((n, p))
+    _same_as_oracle(A, B, tol=1e-10, maxit=60)
+
+
 # ----------------------------------------------------------------------------- configs 4 and 5 at full size
 
 
