@@ -258,6 +258,8 @@ void dalloc(bminres_ctx* h, T** p, size_t elems) {
     *p = nullptr;
     if (elems == 0) return;
     CK(cudaMalloc((void**)p, elems * sizeof(T)));
+    static const char* poison = getenv("BMINRES_POISON");   // debugging: NaN-fill new buffers
+    if (poison && (poison[0] == '*' || strstr(poison, "dalloc"))) CK(cudaMemset(*p, 0xFF, elems * sizeof(T)));
 }
 
 cudaEvent_t next_event(bminres_ctx* h) {
@@ -364,7 +366,10 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     // the V slots also hold the halo rows of a row partition (n_ext >= n)
     size_t panel = (size_t)n * p + 32;
     const size_t vpanel = (size_t)std::max(n, h->n_ext) * p + 32;
-    for (int s = 0; s < 3; ++s) dalloc(h, &h->V[s], vpanel);
+    for (int s = 0; s < 3; ++s) {
+        dalloc(h, &h->V[s], vpanel);
+        CK(cudaMemset(h->V[s], 0, vpanel * sizeof(double)));   // (defined contents, incl. the slack)
+    }
     dalloc(h, &h->M[0], panel);
     dalloc(h, &h->M[1], panel);
     // split mode for large panels (the gathers of a big SpMM need more warps per SM than the fused
@@ -386,6 +391,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         h->scr[s] = nullptr;
     }
     dalloc(h, &h->pool, (size_t)n * std::max(q, 1) + 32);
+    CK(cudaMemset(h->pool, 0, ((size_t)n * std::max(q, 1) + 32) * sizeof(double)));
     // generic-kernel partials, then K1 partials (ncl1 x (p*p+p)) and K2 partials x 2 parities
     h->part_elems = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8);
     const size_t e1 = (size_t)NB_MAX * (MAXP * MAXP + MAXP), e2 = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP);
@@ -757,7 +763,10 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
     auto materialise = [&]() {
         if (have_window) return;
         for (int s2 = 0; s2 < 2; ++s2)
-            if (!h->scr[s2]) CK(cudaMalloc((void**)&h->scr[s2], (size_t)n * p * sizeof(double)));
+            if (!h->scr[s2]) {
+                CK(cudaMalloc((void**)&h->scr[s2], ((size_t)n * p + 32) * sizeof(double)));
+                CK(cudaMemset(h->scr[s2], 0, ((size_t)n * p + 32) * sizeof(double)));
+            }
         const int slots[2] = {(sk + 2) % 3, sk};
         for (int s2 = 0; s2 < 2; ++s2) {
             const double* Tr = (const double*)((char*)h->st + offsetof(DevState, Tr)) + (size_t)slots[s2] * MAXP * MAXP;

@@ -465,6 +465,13 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
     return s_bad != 0;
 }
 
+// The main branch has stopped (breakdown of a block, run_main = 0): K2 still advances k_main, so
+// the K1 launches still in flight compute later blocks and never re-apply the fused M/X update
+// of a block that has been applied (their update condition b < k_side then fails).
+__device__ __forceinline__ void k2_stopped(DevState* st) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->k_main = st->k_main + 1;
+}
+
 // Publish a breakdown of block b (main branch stops; the host runs the column path).
 __device__ __forceinline__ void publish_breakdown(DevState* st, long long b) {
     st->need_slow = 1;

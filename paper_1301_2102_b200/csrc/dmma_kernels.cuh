@@ -62,126 +62,146 @@ struct UpdSmem {
     static constexpr int doubles = 4 * DM<P>::FR + WARPS * NS * 4 * DM<P>::TILE + 3 * P * P;
 };
 
-template <int P, int WARPS, int NS>
-__device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long long tend, double* smem) {
+// The update in three pieces (shared by the pipelined dmma_update below and the interleaved K1):
+// upd_setup loads the factors (all threads of the calling group, then a barrier by the caller),
+// upd_issue stages one tile's rows of V_k, M_{k-2}, M_{k-1}, X into a 4-tile slot (cp.async, one
+// commit group), upd_compute runs the tile's DMMAs from the slot and stores M_k and X.
+template <int P>
+struct UpdF {   // factor pointers in shared memory (FR doubles each)
+    double *fA, *fB2, *fB1, *fZ, *fZp;
+};
+template <int P>
+__device__ __forceinline__ void upd_setup(const K4bArgs& a, const UpdF<P>& f, int tid, int nth) {
     using D = DM<P>;
-    constexpr int TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
+    constexpr int FR = D::FR;
+    static_assert(FR == P * P, "fragment order of a p x p factor");
     DevState* st = a.st;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* fA = smem;         // Tr_k R_kk^{-1}
-    double* fB2 = fA + FR;     // -R_{k-2,k} R_kk^{-1}
-    double* fB1 = fB2 + FR;    // -R_{k-1,k} R_kk^{-1}
-    double* fZ = fB1 + FR;     // Z_k
-    double* pipe = fZ + FR;
-    double* scr = pipe + WARPS * NS * 4 * D::TILE;
-    double* wb = pipe + warp * NS * 4 * D::TILE;
-    double* fZp = scr;         // Z_{k-1} (xmode 2), in the factor scratch once the factors are built
-    const long long tw = t0 + warp;
+    const int xmode = a.xmode;
+    // K3b(k) left the factors in fragment order (one load instead of a p x p product and four
+    // reorderings on the critical path)
+    const double* zf = st->ufz[a.zb % 3];   // (xmode != 0)
+    for (int t = tid; t < FR; t += nth) {
+        f.fA[t] = st->uf[a.par][0][t];
+        f.fB2[t] = st->uf[a.par][1][t];
+        f.fB1[t] = st->uf[a.par][2][t];
+        f.fZp[t] = xmode == 2 ? st->ufz[(a.zb + 2) % 3][t] : 0.0;
+        if (xmode != 0) f.fZ[t] = zf[t];
+    }
+    if (xmode == 0)
+        for (int t = tid; t < FR; t += nth) {
+            const int blk = t / 32, l = t % 32, kc = blk / D::NC, nc = blk % D::NC;
+            f.fZ[t] = st->Z[a.par][(kc * 4 + l % 4) * MAXP + nc * 8 + l / 4];
+        }
+}
+template <int P>
+__device__ __forceinline__ void upd_issue(const K4bArgs& a, long long t, double* sl, int lane) {
+    using D = DM<P>;
     const int xmode = a.xmode;
     const bool xonly = xmode == 3, with_x = xmode != 1;
-    auto issue = [&](long long it, int slot) {
-        const long long t = tw + it * ts;
-        if (t < tend) {
-            double* sl = wb + slot * 4 * D::TILE;
-            const long long base = t * TR;
-            if (!xonly) stage_tile<P>(sl, a.U, base, a.n, lane);
-            stage_tile<P>(sl + D::TILE, a.M2, base, a.n, lane);
-            if (!xonly) stage_tile<P>(sl + 2 * D::TILE, a.M1, base, a.n, lane);
-            if (with_x) stage_tile<P>(sl + 3 * D::TILE, a.X, base, a.n, lane);
-        }
-        cp_commit();
-    };
-    // the first stages stream in while the p x p factors are formed
-#pragma unroll
-    for (int s = 0; s < NS - 1; ++s) issue(s, s);
-    {
-        // K3b(k) left the factors in fragment order (one load instead of a p x p product and four
-        // reorderings on the critical path)
-        static_assert(FR == P * P, "fragment order of a p x p factor");
-        const double* zf = st->ufz[a.zb % 3];   // (xmode != 0)
-        for (int t = threadIdx.x; t < FR; t += blockDim.x) {
-            fA[t] = st->uf[a.par][0][t];
-            fB2[t] = st->uf[a.par][1][t];
-            fB1[t] = st->uf[a.par][2][t];
-            fZp[t] = xmode == 2 ? st->ufz[(a.zb + 2) % 3][t] : 0.0;   // 3 P^2 >= FR doubles
-        }
-        if (xmode == 0) {
-            to_frag<P>(st->Z[a.par], MAXP, 1.0, fZ);
-        } else {
-            for (int t = threadIdx.x; t < FR; t += blockDim.x) fZ[t] = zf[t];
-        }
-        __syncthreads();
-    }
+    const long long base = t * D::TR;
+    if (!xonly) stage_tile<P>(sl, a.U, base, a.n, lane);
+    stage_tile<P>(sl + D::TILE, a.M2, base, a.n, lane);
+    if (!xonly) stage_tile<P>(sl + 2 * D::TILE, a.M1, base, a.n, lane);
+    if (with_x) stage_tile<P>(sl + 3 * D::TILE, a.X, base, a.n, lane);
+}
+template <int P>
+__device__ __forceinline__ void upd_compute(const K4bArgs& a, const UpdF<P>& f, long long t, double* sl, int lane) {
+    using D = DM<P>;
+    constexpr int TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC;
+    const int xmode = a.xmode;
+    const bool xonly = xmode == 3, with_x = xmode != 1;
     const int fr = lane >> 2, fc = lane & 3;   // A-fragment row / col within an 8x4 block
-    for (long long it = 0; tw + it * ts < tend; ++it) {
-        issue(it + NS - 1, (int)((it + NS - 1) % NS));
-        cp_wait<NS - 1>();
-        __syncwarp();
-        double* sl = wb + (int)(it % NS) * 4 * D::TILE;
-        const double* tV = sl;
-        double* tM2 = sl + D::TILE;
-        const double* tM1 = sl + 2 * D::TILE;
-        const double* tX = sl + 3 * D::TILE;
-        const long long base = (tw + it * ts) * TR;
+    const double* tV = sl;
+    double* tM2 = sl + D::TILE;
+    const double* tM1 = sl + 2 * D::TILE;
+    const double* tX = sl + 3 * D::TILE;
+    const long long base = t * TR;
 #pragma unroll
-        for (int mc = 0; mc < TR / 8; ++mc) {
-            const int r0 = mc * 8;
-            const long long row = base + r0 + fr;
-            if (xonly) {   // host flush of a deferred X update: X += M_k Z_k (M2 holds M_k)
-#pragma unroll
-                for (int nc = 0; nc < NC; ++nc) {
-                    const int col = nc * 8 + 2 * fc;
-                    double x0 = tX[(r0 + fr) * RS + col], x1 = tX[(r0 + fr) * RS + col + 1];
-#pragma unroll
-                    for (int kc = 0; kc < KC; ++kc)
-                        dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], fZ[(kc * NC + nc) * 32 + lane]);
-                    if (row < a.n) *reinterpret_cast<double2*>(a.X + row * P + col) = make_double2(x0, x1);
-                }
-                continue;
-            }
-            double mk[NC][2];
-#pragma unroll
-            for (int nc = 0; nc < NC; ++nc) {
-                mk[nc][0] = mk[nc][1] = 0.0;
-#pragma unroll
-                for (int kc = 0; kc < KC; ++kc) {
-                    const int ai = (r0 + fr) * RS + kc * 4 + fc;
-                    const int bi = (kc * NC + nc) * 32 + lane;
-                    // Tr_k R_kk^{-1} is upper triangular (both factors are): its rows 4kc.. are zero
-                    // in columns 8nc..8nc+7 when 4kc > 8nc+7
-                    if (kc <= 2 * nc + 1) dmma(mk[nc][0], mk[nc][1], tV[ai], fA[bi]);
-                    dmma(mk[nc][0], mk[nc][1], tM2[ai], fB2[bi]);
-                    dmma(mk[nc][0], mk[nc][1], tM1[ai], fB1[bi]);
-                }
-            }
-            __syncwarp();
-            // M_k overwrites this chunk's M_{k-2} rows (in smem and in HBM)
-#pragma unroll
-            for (int nc = 0; nc < NC; ++nc) {
-                const int col = nc * 8 + 2 * fc;
-                tM2[(r0 + fr) * RS + col] = mk[nc][0];
-                tM2[(r0 + fr) * RS + col + 1] = mk[nc][1];
-                if (row < a.n)
-                    *reinterpret_cast<double2*>(a.M2 + row * P + col) = make_double2(mk[nc][0], mk[nc][1]);
-            }
-            __syncwarp();
-            if (!with_x) continue;   // xmode 1: this block's X update is deferred to the next one
+    for (int mc = 0; mc < TR / 8; ++mc) {
+        const int r0 = mc * 8;
+        const long long row = base + r0 + fr;
+        if (xonly) {   // host flush of a deferred X update: X += M_k Z_k (M2 holds M_k)
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 const int col = nc * 8 + 2 * fc;
                 double x0 = tX[(r0 + fr) * RS + col], x1 = tX[(r0 + fr) * RS + col + 1];
-                if (xmode == 2) {   // first the deferred X += M_{k-1} Z_{k-1}
-#pragma unroll
-                    for (int kc = 0; kc < KC; ++kc)
-                        dmma(x0, x1, tM1[(r0 + fr) * RS + kc * 4 + fc], fZp[(kc * NC + nc) * 32 + lane]);
-                }
 #pragma unroll
                 for (int kc = 0; kc < KC; ++kc)
-                    dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], fZ[(kc * NC + nc) * 32 + lane]);
+                    dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], f.fZ[(kc * NC + nc) * 32 + lane]);
                 if (row < a.n) *reinterpret_cast<double2*>(a.X + row * P + col) = make_double2(x0, x1);
+            }
+            continue;
+        }
+        double mk[NC][2];
+#pragma unroll
+        for (int nc = 0; nc < NC; ++nc) {
+            mk[nc][0] = mk[nc][1] = 0.0;
+#pragma unroll
+            for (int kc = 0; kc < KC; ++kc) {
+                const int ai = (r0 + fr) * RS + kc * 4 + fc;
+                const int bi = (kc * NC + nc) * 32 + lane;
+                // Tr_k R_kk^{-1} is upper triangular (both factors are): its rows 4kc.. are zero
+                // in columns 8nc..8nc+7 when 4kc > 8nc+7
+                if (kc <= 2 * nc + 1) dmma(mk[nc][0], mk[nc][1], tV[ai], f.fA[bi]);
+                dmma(mk[nc][0], mk[nc][1], tM2[ai], f.fB2[bi]);
+                dmma(mk[nc][0], mk[nc][1], tM1[ai], f.fB1[bi]);
             }
         }
         __syncwarp();
+        // M_k overwrites this chunk's M_{k-2} rows (in smem and in HBM)
+#pragma unroll
+        for (int nc = 0; nc < NC; ++nc) {
+            const int col = nc * 8 + 2 * fc;
+            tM2[(r0 + fr) * RS + col] = mk[nc][0];
+            tM2[(r0 + fr) * RS + col + 1] = mk[nc][1];
+            if (row < a.n) *reinterpret_cast<double2*>(a.M2 + row * P + col) = make_double2(mk[nc][0], mk[nc][1]);
+        }
+        __syncwarp();
+        if (!with_x) continue;   // xmode 1: this block's X update is deferred to the next one
+#pragma unroll
+        for (int nc = 0; nc < NC; ++nc) {
+            const int col = nc * 8 + 2 * fc;
+            double x0 = tX[(r0 + fr) * RS + col], x1 = tX[(r0 + fr) * RS + col + 1];
+            if (xmode == 2) {   // first the deferred X += M_{k-1} Z_{k-1}
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                    dmma(x0, x1, tM1[(r0 + fr) * RS + kc * 4 + fc], f.fZp[(kc * NC + nc) * 32 + lane]);
+            }
+#pragma unroll
+            for (int kc = 0; kc < KC; ++kc)
+                dmma(x0, x1, tM2[(r0 + fr) * RS + kc * 4 + fc], f.fZ[(kc * NC + nc) * 32 + lane]);
+            if (row < a.n) *reinterpret_cast<double2*>(a.X + row * P + col) = make_double2(x0, x1);
+        }
+    }
+    __syncwarp();
+}
+
+template <int P, int WARPS, int NS>
+__device__ void dmma_update(const K4bArgs& a, long long t0, long long ts, long long tend, double* smem) {
+    using D = DM<P>;
+    constexpr int FR = D::FR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    UpdF<P> f{smem, smem + FR, smem + 2 * FR, smem + 3 * FR, nullptr};
+    double* pipe = smem + 4 * FR;
+    double* scr = pipe + WARPS * NS * 4 * D::TILE;
+    f.fZp = scr;   // Z_{k-1} (xmode 2), in the factor scratch (3 P^2 >= FR doubles)
+    double* wb = pipe + warp * NS * 4 * D::TILE;
+    const long long tw = t0 + warp;
+    auto issue = [&](long long it, int slot) {
+        const long long t = tw + it * ts;
+        if (t < tend) upd_issue<P>(a, t, wb + slot * 4 * D::TILE, lane);
+        cp_commit();
+    };
+    // the first stages stream in while the p x p factors are loaded
+#pragma unroll
+    for (int s = 0; s < NS - 1; ++s) issue(s, s);
+    upd_setup<P>(a, f, threadIdx.x, blockDim.x);
+    __syncthreads();
+    for (long long it = 0; tw + it * ts < tend; ++it) {
+        issue(it + NS - 1, (int)((it + NS - 1) % NS));
+        cp_wait<NS - 1>();
+        __syncwarp();
+        upd_compute<P>(a, f, tw + it * ts, wb + (int)(it % NS) * 4 * D::TILE, lane);
     }
     cp_wait<0>();
 }
@@ -255,7 +275,10 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
     using S = K2DSmem<P>;
     constexpr int WARPS = S::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR, RSQ = S::RSQ;
     DevState* st = a.st;
-    if (!st->run_main) return;
+    if (!st->run_main) {
+        k2_stopped(st);
+        return;
+    }
     unsigned long long* tr = trace_begin(st, TR_K2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane >> 2, fc = lane & 3;

@@ -98,7 +98,10 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
     using S = K2RSmem<P>;
     constexpr int NG = P * (P + 1) / 2;
     DevState* st = a.st;
-    if (!st->run_main) return;
+    if (!st->run_main) {
+        k2_stopped(st);
+        return;
+    }
     unsigned long long* tr = trace_begin(st, TR_K2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;

@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(NT, P <= 8 ? 2 : 1) k2_orth(K2Args a) {
     using C = PC<P>;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW, WARPS = NT / 32;
     DevState* st = a.st;
-    if (!st->run_main) return;
+    if (!st->run_main) {
+        k2_stopped(st);
+        return;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
