@@ -343,6 +343,21 @@ def test_all_zero_rhs_and_maxit_zero():
     _same_as_oracle(A, synth.gaussian_rhs(A.n, 4, seed=1), tol=1e-8, maxit=0)
 
 
+@pytest.mark.parametrize("use_graphs", [True, False])
+def test_mid_solve_breakdown_then_graphs_x(use_graphs):
+    """An exact dependence at j = 9 (B = [b, A^2 b, ...], p = 8): the column path replaces the
+    vector from the pool, then 49 more block steps run (graph mode: fused updates).  X must match
+    the oracle -- this caught in-flight K1 launches re-applying the last fused update after the
+    breakdown (fixed: K2 advances k_main while the main branch is stopped)."""
+    A = synth.laplacian_2d(40, 37, shift=1.7)
+    D = synth.csr_to_dense(A)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(A.n)
+    B = np.stack([b, D @ (D @ b)] + [rng.standard_normal(A.n) for _ in range(6)], axis=1)
+    r, ref = _same_as_oracle(A, B, tol=1e-10, maxit=400, use_graphs=use_graphs)
+    assert [(e["j"], e["action"]) for e in r.events] == [(9, 1)]
+
+
 @pytest.mark.parametrize("n,p", [(1, 1), (8, 8), (5, 8), (24, 8), (40, 16)])
 def test_tiny_systems(n, p):
     """n = 1; n = p (the block Krylov space is exhausted after one block -> EPOOL, P:718-726);
