@@ -39,6 +39,9 @@ sys.path.insert(0, ROOT)
 # algorithmic panel transfers per launch.  The fused M/X update moves 5 panels on average: it
 # reads V_k, M_{k-2}, M_{k-1} and writes M_k every block, and reads + writes X every other block
 # (X updates deferred in pairs); the standalone K4b moves 6.
+# BASELINE.json's metric (the value is iterations/s; the achieved HBM GB/s against the roofline is
+# reported in "roofline" / "step_roofline")
+METRIC = "block-MINRES iterations/s and achieved HBM GB/s (fp64) vs roofline, 1/2/4/8 B200"
 PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 8, "orth": 3, "update": 6,
                       # split mode (large panels): K1a reads V_k once (gathers) and writes AV; K1 then
                       # streams AV, V_k, V_{k-1} and writes W (+ the fused update)
@@ -176,7 +179,7 @@ def run_reference(args):
         total += r.iterations
     dt = time.perf_counter() - t0
     value = total / dt
-    line = {"impl": "reference", "metric": "block-MINRES iterations/s (fp64)", "value": value,
+    line = {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -321,7 +324,7 @@ def run_ours(args):
         cpu = cpu_baseline(P, args.cpu_iters if args.cpu_iters > 0 else cpu_sample_iters(P))
 
     if rank == 0:
-        line = {"metric": "block-MINRES iterations/s (fp64)", "value": value, "unit": "iterations/s",
+        line = {"metric": METRIC, "value": value, "unit": "iterations/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
