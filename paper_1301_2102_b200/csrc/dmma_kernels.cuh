@@ -751,31 +751,6 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
     const long long ntiles = (a.n + TR - 1) / TR;
     const long long tpc = (ntiles + gridDim.x - 1) / gridDim.x;
     const long long cbeg = (long long)blockIdx.x * tpc, cend = cbeg + tpc < ntiles ? cbeg + tpc : ntiles;
-    if (a.fuse) {
-        // M/X update of block b = k-2 (row a5), on this CTA's slab before its W rows overwrite
-        // V_b (same slot): it needs only K3b(b) and the panels, not the red2 totals, so it runs
-        // before pdl_wait.  The condition reads state that K3b(k-1), running beside this
-        // kernel, can change only in ways that leave it unchanged (uniform over CTAs).
-        const long long k = st->k_main, b = k - 2;
-        if (b >= st->k_upd_min && b < st->k_side && b < st->stop_side_at) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = b;
-            // X updates in pairs from the first fused block: defer b's, then apply both with b+1's
-            const int xm = a.xdefer ? (((b - st->k_upd_min) & 1) ? 2 : 1) : 0;
-            K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b, xm, b};
-            dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe);
-            __syncthreads();   // the region is reused by the SpMM
-        }
-    }
-    trace_pt(tr, 1);
-    if (!st->run_main) return;
-    const bool has_prev = st->k_main > 1;
-    double g[NC][NC][2], om[NC][2];
-#pragma unroll
-    for (int i = 0; i < NC; ++i) {
-        om[i][0] = om[i][1] = 0.0;
-#pragma unroll
-        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
-    }
     double* wb = pipe + warp * 3 * D::TILE;
     double* tA = wb + 2 * D::TILE;   // A V_k rows, then W rows
     const long long t0 = cbeg + warp, ts = WARPS;
@@ -806,6 +781,38 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             v[t] = pr ? __ldg(a.val + r0 + t) : 0.0;
         }
     };
+    if constexpr (!PRE) {
+        // the first row pointers / column indices of the SpMM (A only: no dependence on the update
+        // or the wait) are in flight during the fused update
+        load_rp(0, k0, k1);
+        load_rp(1, rn0, rn1);
+        load_cv(k0, k1, cc, av);
+    }
+    if (a.fuse) {
+        // M/X update of block b = k-2 (row a5), on this CTA's slab before its W rows overwrite
+        // V_b (same slot): it needs only K3b(b) and the panels, not the red2 totals, so it runs
+        // before pdl_wait.  The condition reads state that K3b(k-1), running beside this
+        // kernel, can change only in ways that leave it unchanged (uniform over CTAs).
+        const long long k = st->k_main, b = k - 2;
+        if (b >= st->k_upd_min && b < st->k_side && b < st->stop_side_at) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = b;
+            // X updates in pairs from the first fused block: defer b's, then apply both with b+1's
+            const int xm = a.xdefer ? (((b - st->k_upd_min) & 1) ? 2 : 1) : 0;
+            K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b, xm, b};
+            dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe);
+            __syncthreads();   // the region is reused by the SpMM
+        }
+    }
+    trace_pt(tr, 1);
+    if (!st->run_main) return;
+    const bool has_prev = st->k_main > 1;
+    double g[NC][NC][2], om[NC][2];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+        om[i][0] = om[i][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    }
     // group q: gathers (first CH entries) || loads of group q+1 || row pointers of q+2
     auto process_group = [&](long long q) {
         if (q % G == 0) {   // first group of a tile: stage the tile's V_k, V_{k-1} rows
@@ -969,10 +976,8 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             stage3(it + NSP);
         }
     } else {
-        // pipeline fill, then the SpMM of the first tile (no dependence on the prologue)
-        load_rp(0, k0, k1);
-        load_rp(1, rn0, rn1);
-        load_cv(k0, k1, cc, av);
+        // (pipeline filled before the update) the SpMM of the first tile (no dependence on the
+        // prologue)
         long long q = 0;
         for (; q < G && q < nq; ++q) process_group(q);
         pdl_wait();   // red2 (reduce2 of block k-1) is ready
