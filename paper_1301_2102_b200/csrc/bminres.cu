@@ -85,9 +85,9 @@ Kfn make_kfn(int q) {
             f.nt1 = K1DSmem<P>::WARPS * 32;
             f.k1a = k1a_spmm<P>;
             f.k1pre = k1_dmma<P, true>;
-            // p = 8 only: the register Cholesky keeps the serial tail short (p = 16: 98.5k vs 96.2k it/s
-            // at config 3 without / with)
-            if constexpr (P <= 8) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
+            // p <= 16 (the register Cholesky keeps reduce2's serial tail short: config 3 98k -> 106k
+            // it/s; with the serial general Cholesky it was a loss)
+            if constexpr (P <= 16) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
             f.smem1pre = K1DSmem<P, true>::bytes;
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;

@@ -359,7 +359,7 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
                              double* sCi, double* sCo) {
     __shared__ int s_bad;
     const int tid = threadIdx.x, lane = tid & 31;
-    if constexpr (P <= 8) {
+    if constexpr (P <= 16) {
         // register version: lane j < P holds column j of the Gram (fully unrolled, the
         // trailing update takes C(m, i) from lane i by shuffle)
         if (tid < 32) {
