@@ -87,7 +87,9 @@ Kfn make_kfn(int q) {
             f.k1pre = k1_dmma<P, true>;
             // p <= 16 (the register Cholesky keeps reduce2's serial tail short: config 3 98k -> 106k
             // it/s; with the serial general Cholesky it was a loss)
-            if constexpr (P <= 16) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
+            // (p = 8: the one-cluster variant, 136k vs 134k it/s; p = 16: the ticketed one, 106k vs 103k)
+            if constexpr (P <= 8) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
+            else if constexpr (P <= 16) f.red2f = k_red2f_t<P, DM<P>::FR, DM<P>::NC>;
             f.smem1pre = K1DSmem<P, true>::bytes;
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
@@ -535,7 +537,7 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     const int P = h->p_ws;
     const int Emax = P * P + (which == 1 ? P : MAXQ * P);
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
     cfg.gridDim = dim3((Emax + 7) / 8);
@@ -543,6 +545,15 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (which == 2 && h->red2_fac && P <= 8) {   // k_red2f: one cluster of RF_CL CTAs
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = RF_CL;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(RF_CL);
+        cfg.blockDim = dim3(rf_warps<8>() * 32);
+        cfg.numAttrs = 2;
+    }
     // reduce2 triggers its dependent (K1(k+1) / K1a) right after its own wait: K1's fused update
     // overlaps the reduction (+1.8% at config 2; reduce1 early: +0.3%, kept at exit)
     // (not in split mode: its dependent K1a has no pre-wait work, and its early-resident CTAs would

@@ -570,8 +570,9 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
 // coef_k, D = Tr_k C_k^T -- and stores Tr_{k+1} and -D in fragment order (to_frag of the DMMA K1),
 // so K1(k+1), which launches at this kernel's early trigger and runs its fused update meanwhile,
 // only loads them.  k = k_main - 1 (K2(k) advanced k_main).
+// Ticketed variant (p = 16: 34 CTAs x 8 warps, one entry per warp; the last CTA to finish factors):
 template <int P, int FRN, int NCF>
-__global__ void __launch_bounds__(256) k_red2f(DevState* st, int par, int early) {
+__global__ void __launch_bounds__(256) k_red2f_t(DevState* st, int par, int early) {
     unsigned long long* tr = trace_begin(st, TR_RED2);
     pdl_wait();
     if (early) pdl_trigger();   // K1(k+1) may launch now (see k_reduce's early trigger)
@@ -619,6 +620,87 @@ __global__ void __launch_bounds__(256) k_red2f(DevState* st, int par, int early)
     const long long k = st->k_main - 1;
     const int sk1 = (int)((k + 1) % 3), sk = (int)(k % 3);
     for (int t = threadIdx.x; t < E; t += blockDim.x) sRed[t] = __ldcg(st->red2[par] + t);
+    for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
+    load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
+    __syncthreads();
+    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo);
+    if (bad) {
+        if (threadIdx.x == 0) {
+            st->fac_bad = 1;
+            publish_breakdown(st, k);
+        }
+        trace_pt(tr, 5);
+        return;
+    }
+    store_pp<P>(st->Ck[par], sC);
+    store_pp<P>(st->Tr[sk1], sCi);
+    for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[par][t] = sCo[t];
+    smm_nn<P>(sTp, sC, sD, true);                // D = Tr_k C_k^T
+    __syncthreads();
+    // fragment order of the DMMA K1 (to_frag: 4 x 8 blocks, KC = P/4 k-chunks, NCF = P/8 n-chunks)
+    for (int t = threadIdx.x; t < FRN; t += blockDim.x) {
+        const int blk = t / 32, l = t % 32, kc = blk / NCF, nc = blk % NCF;
+        const int r = kc * 4 + l % 4, c = nc * 8 + l / 4;
+        st->fT[t] = sCi[r * P + c];
+        st->fD[t] = -sD[r * P + c];
+    }
+    if (threadIdx.x == 0) st->fac_bad = 0;
+    trace_pt(tr, 5);
+}
+
+// One thread-block cluster of RF_CL CTAs x RF_W warps: each warp sums its entries (k_reduce's
+// order) and stores them into the leader CTA's shared memory (distributed shared memory); after
+// the cluster barrier the leader factors.  No global round trips between the totals and the
+// factorisation -- the tail runs while K1(k+1)'s fused update saturates HBM, where each L2 round
+// trip costs several microseconds (a ticketed last-CTA tail took ~22 us there).
+constexpr int RF_CL = 8;   // (measured: 8 x 16 warps 136k it/s at config 2; 4 x 32: 135k; 2 x 32: 134.7k)
+template <int P>
+__host__ __device__ constexpr int rf_warps() { return P <= 8 ? 16 : 32; }   // p = 16: 256 warps, <= 2 entries each
+template <int P, int FRN, int NCF>
+__global__ void __launch_bounds__(rf_warps<P>() * 32) k_red2f(DevState* st, int par, int early) {
+    constexpr int RF_W = rf_warps<P>();
+    unsigned long long* tr = trace_begin(st, TR_RED2);
+    pdl_wait();
+    if (early) pdl_trigger();   // K1(k+1) may launch now (see k_reduce's early trigger)
+    trace_pt(tr, 1);
+    if (!st->run_main) return;   // (uniform: every CTA of the cluster returns)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Q = st->q_live;
+    const int E = P * P + Q * P;
+    const int ncl = st->ncl2;
+    const double* part = st->part2[par];
+    __shared__ double sm[P * P + MAXQ * P + 3 * P * P + P * MAXQ + P + 2 * P * P];
+    cg::cluster_group cl = cg::this_cluster();
+    double* lead = cl.map_shared_rank(sm, 0);    // the leader's totals (sRed)
+    for (int e = (int)cl.block_rank() * RF_W + warp; e < E; e += RF_CL * RF_W) {
+        constexpr int U = 8;
+        double s = 0.0;
+        for (int b0 = 0; b0 < ncl; b0 += 32 * U) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int b = b0 + lane + 32 * u;
+                v[u] = b < ncl ? __ldcg(part + (size_t)b * E + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b0 + lane + 32 * u < ncl) s += v[u];
+        }
+        s = warp_sum(s);
+        if (lane == 0) lead[e] = s;
+    }
+    cl.sync();
+    if (cl.block_rank() != 0) return;   // (the leader reads only its own shared memory)
+    double* sRed = sm;                           // totals (P*P + MAXQ*P)
+    double* sC = sRed + P * P + MAXQ * P;
+    double* sCi = sC + P * P;
+    double* sTp = sCi + P * P;
+    double* sCo = sTp + P * P;
+    double* sOm = sCo + P * MAXQ;
+    double* sD = sOm + P;
+    const long long k = st->k_main - 1;
+    const int sk1 = (int)((k + 1) % 3), sk = (int)(k % 3);
+    for (int t = threadIdx.x; t < E; t += blockDim.x) st->red2[par][t] = sRed[t];   // (K3b(k) reads them)
     for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
     load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
     __syncthreads();
