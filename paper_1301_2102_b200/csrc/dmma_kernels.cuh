@@ -700,13 +700,20 @@ struct K1DSmem {
     // p = 32: one 512-thread CTA per SM (16 warps, <= 128 registers) instead of one 256-thread
     // CTA at 209 registers -- the gathers need the warps; the fused update single-staged
     static constexpr int WARPS = P >= 32 ? 16 : 8;
-    static constexpr int UNS = P >= 32 ? 1 : 2;              // cp.async stages of the fused update
+#ifndef K1_DISJ
+#define K1_DISJ 1
+#endif
+    // DISJ (p <= 16, fused): the update's staging is disjoint from the SpMM's, single-staged, so a
+    // warp starts its first SpMM tile as soon as its own update tiles are done (each warp updates
+    // exactly the rows whose W it writes later: same tiling, no cross-warp hazard)
+    static constexpr bool DISJ = K1_DISJ && !PRE && P <= 16;
+    static constexpr int UNS = (P >= 32 || DISJ) ? 1 : 2;    // cp.async stages of the fused update
     // split mode (PRE): the A V_k rows are staged like the panels; two stages where they fit
     static constexpr int NSP = (PRE && P < 32) ? 2 : 1;
     static constexpr int pipe = WARPS * 3 * DM<P>::TILE * NSP;   // V_k, V_{k-1} tiles + A V tile per warp
     static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
     static constexpr int upd = UpdSmem<P, WARPS, UNS>::doubles;   // the update runs first, then the SpMM
-    static constexpr int region = (pipe + scr > upd) ? pipe + scr : upd;
+    static constexpr int region = DISJ ? pipe + scr + upd : ((pipe + scr > upd) ? pipe + scr : upd);
     static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + region + P * P + P);
 };
 
@@ -799,8 +806,12 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             // X updates in pairs from the first fused block: defer b's, then apply both with b+1's
             const int xm = a.xdefer ? (((b - st->k_upd_min) & 1) ? 2 : 1) : 0;
             K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b, xm, b};
-            dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe);
-            __syncthreads();   // the region is reused by the SpMM
+            if constexpr (KS::DISJ) {
+                dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe + KS::pipe + KS::scr);
+            } else {
+                dmma_update<P, WARPS, KS::UNS>(u, cbeg, WARPS, cend, pipe);
+                __syncthreads();   // the region is reused by the SpMM
+            }
         }
     }
     trace_pt(tr, 1);
