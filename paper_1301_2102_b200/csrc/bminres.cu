@@ -261,7 +261,7 @@ void dalloc(bminres_ctx* h, T** p, size_t elems) {
     if (elems == 0) return;
     CK(cudaMalloc((void**)p, elems * sizeof(T)));
     static const char* poison = getenv("BMINRES_POISON");   // debugging: NaN-fill new buffers
-    if (poison && (poison[0] == '*' || strstr(poison, "dalloc"))) CK(cudaMemset(*p, 0xFF, elems * sizeof(T)));
+    if (poison && (poison[0] == '*' || strstr(poison, "dalloc"))) CK(cudaMemsetAsync(*p, 0xFF, elems * sizeof(T), h->stream));
 }
 
 cudaEvent_t next_event(bminres_ctx* h) {
@@ -370,7 +370,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     const size_t vpanel = (size_t)std::max(n, h->n_ext) * p + 32;
     for (int s = 0; s < 3; ++s) {
         dalloc(h, &h->V[s], vpanel);
-        CK(cudaMemset(h->V[s], 0, vpanel * sizeof(double)));   // (defined contents, incl. the slack)
+        CK(cudaMemsetAsync(h->V[s], 0, vpanel * sizeof(double), h->stream));   // (defined contents, incl. the slack)
     }
     dalloc(h, &h->M[0], panel);
     dalloc(h, &h->M[1], panel);
@@ -393,7 +393,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         h->scr[s] = nullptr;
     }
     dalloc(h, &h->pool, (size_t)n * std::max(q, 1) + 32);
-    CK(cudaMemset(h->pool, 0, ((size_t)n * std::max(q, 1) + 32) * sizeof(double)));
+    CK(cudaMemsetAsync(h->pool, 0, ((size_t)n * std::max(q, 1) + 32) * sizeof(double), h->stream));
     // generic-kernel partials, then K1 partials (ncl1 x (p*p+p)) and K2 partials x 2 parities
     h->part_elems = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8);
     const size_t e1 = (size_t)NB_MAX * (MAXP * MAXP + MAXP), e2 = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP);
@@ -405,7 +405,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     if (!h->gdev) CK(cudaMalloc((void**)&h->gdev, 2 * MAXP * MAXP * sizeof(double)));
     if (!h->dcnt) {
         CK(cudaMalloc((void**)&h->dcnt, 16 * sizeof(unsigned)));
-        CK(cudaMemset(h->dcnt, 0, 16 * sizeof(unsigned)));
+        CK(cudaMemsetAsync(h->dcnt, 0, 16 * sizeof(unsigned), h->stream));
     }
     if (!h->st) CK(cudaMalloc((void**)&h->st, sizeof(DevState)));
     if (!h->hf) {
@@ -731,10 +731,17 @@ void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
 }
 
 // write a few DevState fields from the host (after draining the stream)
+// Host -> device copy ordered on the solver's stream.  (A plain cudaMemcpy runs on the legacy
+// stream, which does not order against the non-blocking h->stream, and from pageable memory it
+// may return before the DMA lands: a kernel launched next on h->stream could read the old value.)
+void h2d(bminres_ctx* h, void* dst, const void* src, size_t bytes) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+}
+
 template <typename T>
 void set_state(bminres_ctx* h, size_t offset, T value) {
-    CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy((char*)h->st + offset, &value, sizeof(T), cudaMemcpyHostToDevice));
+    h2d(h, (char*)h->st + offset, &value, sizeof(T));
 }
 #define SET_STATE(h, field, val) set_state(h, offsetof(DevState, field), (decltype(DevState::field))(val))
 
@@ -776,7 +783,7 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
         for (int s2 = 0; s2 < 2; ++s2)
             if (!h->scr[s2]) {
                 CK(cudaMalloc((void**)&h->scr[s2], ((size_t)n * p + 32) * sizeof(double)));
-                CK(cudaMemset(h->scr[s2], 0, ((size_t)n * p + 32) * sizeof(double)));
+                CK(cudaMemsetAsync(h->scr[s2], 0, ((size_t)n * p + 32) * sizeof(double), h->stream));
             }
         const int slots[2] = {(sk + 2) % 3, sk};
         for (int s2 = 0; s2 < 2; ++s2) {
@@ -869,8 +876,8 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
         if (stop_after) break;
     }
     CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy((char*)h->st + offsetof(DevState, Ck) + par * MAXP * MAXP * sizeof(double), Ck.data(),
-                  MAXP * MAXP * sizeof(double), cudaMemcpyHostToDevice));
+    h2d(h, (char*)h->st + offsetof(DevState, Ck) + par * MAXP * MAXP * sizeof(double), Ck.data(),
+        MAXP * MAXP * sizeof(double));
     SET_STATE(h, q_first, q_first);
     SET_STATE(h, q_live, q_live);
     SET_STATE(h, stop_after, stop_after);
@@ -882,18 +889,21 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
     // Tr_{b+1} = I (V_{b+1} is the normalised basis block); pool coefficients of block b = 0
     std::vector<double> I(MAXP * MAXP, 0.0), Z0(MAXP * MAXQ, 0.0);
     for (int c = 0; c < MAXP; ++c) I[c * MAXP + c] = 1.0;
-    CK(cudaMemcpy((char*)h->st + offsetof(DevState, Tr) + (size_t)((sk + 1) % 3) * MAXP * MAXP * sizeof(double),
-                  I.data(), MAXP * MAXP * sizeof(double), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy((char*)h->st + offsetof(DevState, coef) + (size_t)par * MAXP * MAXQ * sizeof(double), Z0.data(),
-                  MAXP * MAXQ * sizeof(double), cudaMemcpyHostToDevice));
+    h2d(h, (char*)h->st + offsetof(DevState, Tr) + (size_t)((sk + 1) % 3) * MAXP * MAXP * sizeof(double), I.data(),
+        MAXP * MAXP * sizeof(double));
+    h2d(h, (char*)h->st + offsetof(DevState, coef) + (size_t)par * MAXP * MAXQ * sizeof(double), Z0.data(),
+        MAXP * MAXQ * sizeof(double));
     h->hf->need_slow = 0;
     h->slow_blocks++;
     halo_exchange(h, Wp, p, h->stream);   // the new U_{b+1} rows the peers read
 }
 
 // Finish block b after the column path: its side branch (K3b, K4b).
+void debug_state(bminres_ctx* h, const char* tag);
 void finish_given_block(bminres_ctx* h, const StepPtrs& sp, long long n, long long b) {
+    if (getenv("BMINRES_DEBUG_STATE")) debug_state(h, "before given K3b");
     launch_k3b(h, h->stream);
+    if (getenv("BMINRES_DEBUG_STATE")) debug_state(h, "after given K3b");
     launch_k4b(h, h->stream, sp, n, b);
     CK(cudaStreamSynchronize(h->stream));
 }
@@ -1038,12 +1048,12 @@ void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, i
             dalloc(h, &h->d_lcol, std::max<long long>(A->nnz, 1));
             h->lcol_cap = std::max<long long>(A->nnz, 1);
         }
-        CK(cudaMemcpy(h->d_lcol, pl.local_col.data(), A->nnz * sizeof(int), cudaMemcpyHostToDevice));
+        h2d(h, h->d_lcol, pl.local_col.data(), A->nnz * sizeof(int));
         if (h->send_cap < (size_t)std::max<long long>(ns, 1)) {
             dalloc(h, &h->d_send_rows, std::max<long long>(ns, 1));
             h->send_cap = std::max<long long>(ns, 1);
         }
-        CK(cudaMemcpy(h->d_send_rows, pl.send_rows.data(), ns * sizeof(long long), cudaMemcpyHostToDevice));
+        h2d(h, h->d_send_rows, pl.send_rows.data(), ns * sizeof(long long));
         std::copy(key, key + 5, h->plan_key);
     }
     const long long ns = (long long)h->plan.send_rows.size();
@@ -1070,6 +1080,26 @@ const double* extended_input(bminres_ctx* h, const double* X, long long n, int p
 }
 
 // ------------------------------------------------------------------ the solve
+
+// debugging (BMINRES_DEBUG_STATE): the side branch's state, printed to stderr
+void debug_state(bminres_ctx* h, const char* tag) {
+    CK(cudaStreamSynchronize(h->stream));
+    static DevState d;
+    CK(cudaMemcpy(&d, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    const int p = h->p_ws;
+    auto pm = [&](const char* nm, const double* M, int rows, int ld, int cols) {
+        fprintf(stderr, "%s\n", nm);
+        for (int r = 0; r < rows; ++r) {
+            for (int c = 0; c < cols; ++c) fprintf(stderr, " % .6e", M[r * ld + c]);
+            fprintf(stderr, "\n");
+        }
+    };
+    fprintf(stderr, "[%s] k_side %lld k_main %lld j_done %lld given %lld side_go %d stop_after %d\n", tag, d.k_side,
+            d.k_main, d.j_done, d.given_blk, d.side_go, d.stop_after);
+    pm("G1", d.G[1], p, MAXP, p); pm("Ck0", d.Ck[0], p, MAXP, p); pm("Ck1", d.Ck[1], p, MAXP, p); pm("CprevS", d.CprevS, p, MAXP, p);
+    pm("T", d.T, p, MAXP, p); pm("res", d.res, 1, p, p);
+    pm("ring", d.rv, 2 * p + 1, MAXP + 1, p + 1); pm("rtau", d.rtau, 1, 2 * p + 1, 2 * p + 1);
+}
 
 int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xin, int p, double tol, long long maxit,
              double tau) {
@@ -1436,6 +1466,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     // ---- exit: status, true residuals (K7), history, copy-back
     DevState* fin = &init;   // reuse the static buffer
     CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    if (getenv("BMINRES_DEBUG_STATE")) debug_state(h, "exit");
     {
         TimeMark tm(h, PH_RESID);
         const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);   // (V slots are free now)

@@ -528,6 +528,8 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             return;
         }
         for (int t = tid; t < P * P; t += K3T) sC[(t / P) * LD + t % P] = sCc[t];
+        // the scratch (sCc included) overlaps the reflector ring and the frame loaded next
+        __syncthreads();
     }
     trace_pt(tr, 2);
     for (int t = tid; t < P * P; t += K3T) {

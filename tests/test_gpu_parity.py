@@ -361,15 +361,30 @@ def test_mid_solve_breakdown_then_graphs_x(use_graphs):
 @pytest.mark.parametrize("n,p", [(1, 1), (8, 8), (5, 8), (24, 8), (40, 16)])
 def test_tiny_systems(n, p):
     """n = 1; n = p (the block Krylov space is exhausted after one block -> EPOOL, P:718-726);
-    n < p (EINVAL, as the oracle); a few blocks on a dense random symmetric indefinite matrix.
-    For n = 24, p = 8 the iterate X after the EPOOL exit is not compared (open
-    issue: it differs from the oracle's in some runs while status, counts, events and the
-    residual history agree)."""
+    n < p (EINVAL, as the oracle); a few blocks on a dense random symmetric indefinite matrix."""
     rng = np.random.default_rng(n * 100 + p)
     D = rng.standard_normal((n, n))
     A = synth.dense_to_csr(D + D.T)
     B = rng.standard_normal((n, p))
-    _same_as_oracle(A, B, tol=1e-10, maxit=60, compare_x=(n, p) != (24, 8))
+    _same_as_oracle(A, B, tol=1e-10, maxit=60)
+
+
+@pytest.mark.parametrize("use_graphs", [True, False])
+@pytest.mark.parametrize("p", [4, 7, 8])
+def test_solve_ends_inside_column_path_block(p, use_graphs):
+    """Dense n = 3p: the Krylov space is exhausted at j = 2p+1 (exact dependence, replaced by the
+    pool vector) and the pool at j = 2p+2 (EPOOL).  The solve ends inside the block the
+    column path handled -- at maxit = 2p+1 and at the EPOOL exit -- and X, history and events
+    must match the oracle's.  (Regression: K3b's prologue scratch, holding the host's C_k here,
+    overlaps its reflector ring and had no barrier before the ring load, so reflectors of the two
+    previous blocks could be overwritten -- X off by up to 0.75 relative at p = 7.)"""
+    n = 3 * p
+    rng = np.random.default_rng(n * 100 + p)
+    D = rng.standard_normal((n, n))
+    A = synth.dense_to_csr(D + D.T)
+    B = rng.standard_normal((n, p))
+    for maxit in (2 * p + 1, 60):
+        _same_as_oracle(A, B, tol=1e-10, maxit=maxit, use_graphs=use_graphs)
 
 
 # ----------------------------------------------------------------------------- configs 4 and 5 at full size
