@@ -387,6 +387,23 @@ def test_solve_ends_inside_column_path_block(p, use_graphs):
         _same_as_oracle(A, B, tol=1e-10, maxit=maxit, use_graphs=use_graphs)
 
 
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8, 16, 32])
+def test_exhausted_krylov_space_sweep(p):
+    """Every compiled p: dense symmetric indefinite n x n systems with n = 3p+1 and 4p-1, whose
+    block Krylov space is exhausted mid-solve (exact dependences replaced from the pool, then
+    EPOOL or convergence), ending at maxit = n-p+1 (inside the column-path block) and
+    at the natural exit; graphs and plain launches.  Status, counts, events, history and X as
+    the oracle's (scripts/diag_sweep.py is the wider diagnostic version)."""
+    for n in ((3, 5) if p == 1 else (3 * p + 1, 4 * p - 1)):
+        rng = np.random.default_rng(n * 1000 + p)
+        D = rng.standard_normal((n, n))
+        A = synth.dense_to_csr(D + D.T)
+        B = rng.standard_normal((n, p))
+        for maxit in (n - p + 1, 4 * n):
+            for g in (True, False):
+                _same_as_oracle(A, B, tol=1e-10, maxit=maxit, use_graphs=g)
+
+
 # ----------------------------------------------------------------------------- configs 4 and 5 at full size
 
 
