@@ -147,6 +147,8 @@ struct bminres_ctx {
     int n_sm = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // side branch during graph capture
+    cudaStream_t cstream = nullptr;   // host-A staging copies, overlapped with the start block
+    cudaEvent_t ev_a = nullptr;       // host A staged (recorded on cstream)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     std::string err;
@@ -1138,6 +1140,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     StepPtrs sp{};
     const size_t panel = (size_t)n * p;
     bool x_host = false;
+    bool a_stage = false, a_async = false;
     {
         TimeMark tm(h, PH_OTHER);
         const bool a_dev = is_device_ptr(A->row_ptr) && is_device_ptr(A->col_idx) && is_device_ptr(A->values);
@@ -1155,9 +1158,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
                 dalloc(h, &h->a_val, std::max<long long>(A->nnz, 1));
                 h->a_nnz_cap = std::max<long long>(A->nnz, 1);
             }
-            CK(cudaMemcpyAsync(h->a_rowptr, A->row_ptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, h->stream));
-            CK(cudaMemcpyAsync(h->a_col, A->col_idx, A->nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
-            CK(cudaMemcpyAsync(h->a_val, A->values, A->nnz * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+            a_stage = true;
             sp.rowptr = h->a_rowptr;
             sp.col = h->a_col;
             sp.val = h->a_val;
@@ -1182,6 +1183,23 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             sp.X = Xin;
         }
         if ((((uintptr_t)Bin) | ((uintptr_t)sp.X)) & 15) fail(h, BMINRES_EINVAL, "B and X must be 16-byte aligned");
+        if (a_stage) {
+            // A host CSR is staged after B: with X0 = 0 the start block needs only B, so (single
+            // rank) A's copies run on their own stream beside it and the block loop waits for them
+            a_async = !o.use_x0 && !h->tp;
+            cudaStream_t cs = h->stream;
+            if (a_async) {
+                if (!h->cstream) CK(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+                if (!h->ev_a) CK(cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming));
+                CK(cudaEventRecord(h->ev_a, h->stream));   // (after the buffers' (re)allocation)
+                CK(cudaStreamWaitEvent(h->cstream, h->ev_a, 0));
+                cs = h->cstream;
+            }
+            CK(cudaMemcpyAsync(h->a_rowptr, A->row_ptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, cs));
+            CK(cudaMemcpyAsync(h->a_col, A->col_idx, A->nnz * sizeof(int), cudaMemcpyHostToDevice, cs));
+            CK(cudaMemcpyAsync(h->a_val, A->values, A->nnz * sizeof(double), cudaMemcpyHostToDevice, cs));
+            if (a_async) CK(cudaEventRecord(h->ev_a, cs));
+        }
     }
     if (h->tp) {   // (a transport at world = 1 runs the same path with an empty halo)
         setup_partition(h, A, sp.col, p);   // halo plan; the SpMM reads the remapped columns
@@ -1377,6 +1395,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     // timing mode of a fused kernel set: the graph's launches issued explicitly, in the graph's
     // order, with an event pair around each (the kernels the product runs, timed one by one)
     const bool fused_expl = o.timing && h->kf.fused;
+    if (a_async) CK(cudaStreamWaitEvent(h->stream, h->ev_a, 0));   // A staged before its first use
     if (graphs && !finished) build_graphs(h, sp, n);
     CK(cudaEventRecord(e_loop0, h->stream));
     const long long nblocks = (maxit + p - 1) / p;
@@ -1776,6 +1795,8 @@ void bminres_destroy(bminres_handle h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->cstream) cudaStreamDestroy(h->cstream);
+    if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
 }

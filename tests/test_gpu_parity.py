@@ -304,6 +304,23 @@ def test_graphs_plain_and_host_pointers_bitwise():
     np.testing.assert_array_equal(r1.X, r3.X)
 
 
+def test_host_pointers_full_size_bitwise():
+    """Host A / B / X at config 2's full size (A staged on its own stream beside the start block):
+    bitwise the device-pointer path, also for a second solve on the same handle with a different
+    matrix (the staged copy must land before the first SpMM of each solve)."""
+    from paper_1301_2102_b200 import Solver
+    P = synth.config(2)
+    A2 = synth.Csr(P.A.n, P.A.indptr, P.A.indices, P.A.data * 1.5)
+    ref1 = gpu_solve(P.A, P.B, tol=0.0, maxit=48)
+    ref2 = gpu_solve(A2, P.B, tol=0.0, maxit=48)
+    with Solver(0) as s:
+        r1 = s.solve(P.A, P.B, np.zeros_like(P.B), tol=0.0, maxit=48)
+        r2 = s.solve(A2, P.B, np.zeros_like(P.B), tol=0.0, maxit=48)
+    np.testing.assert_array_equal(ref1.X, r1.X)
+    np.testing.assert_array_equal(ref2.X, r2.X)
+    np.testing.assert_array_equal(ref1.history, r1.history)
+
+
 def test_invalid_arguments():
     P = synth.config("1c")
     assert gpu_solve(P.A, np.ones((P.n, 9)), tol=1e-8, maxit=10).status_name == "EINVAL"  # p = 9 not compiled
