@@ -92,6 +92,106 @@ __global__ void __launch_bounds__(256) k_axpy(AxpyArgs a) {
     }
 }
 
+// One step of the start block's column-by-column thin QR (eqn.init-QR, reading C13)
+// on a row-major n x P panel F, one pass over the panel:
+//   1. if ncol >= 0: F(:,ncol) *= 1/sqrt(*nsrc)        (the previous column's deferred normalisation)
+//   2. if cin:      F(:,col) -= sum_{l<Kc} cin[l] F(:,l)  (one classical Gram-Schmidt pass)
+//   3. out[l] = F(:,l)^T F(:,col), l < Kd; if want_norm: out[Kd] = F(:,col)^T F(:,col)
+// Each thread owns whole rows (the row's P values in registers), so 1-3 need no ordering beyond
+// the row; the reductions are deterministic (per-thread, warp, CTA, then CTAs in order).
+struct ColStepArgs {
+    double* F;
+    long long n;
+    int col, Kc, Kd, ncol, want_norm;
+    const double* cin;
+    const double* nsrc;
+    double* part;
+    int nb;
+    double* out;
+    unsigned* cnt;
+};
+
+// Lane layout: LP = next power of two >= P lanes per row (lane sub holds F(i, sub)), 32 / LP rows
+// per warp instruction, so each load is a contiguous, coalesced run of rows.
+template <int P>
+__global__ void __launch_bounds__(256, 4) k_colstep(ColStepArgs a) {
+    constexpr int LP = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : P <= 16 ? 16 : 32;
+    constexpr int RPW = 32 / LP;
+    constexpr int UNR = 8;
+    __shared__ double sred[8][LP + 1];
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane % LP, rsub = lane / LP;
+    const int Kc = a.Kc, Kd = a.Kd, col = a.col, ncol = a.ncol;
+    const bool in = sub < P;
+    const double c = (a.cin && sub < Kc) ? a.cin[sub] : 0.0;
+    const double inv = ncol >= 0 ? 1.0 / sqrt(*a.nsrc) : 1.0;
+    const bool upd = a.cin != nullptr;
+    const int src = rsub * LP + col;
+    double acc = 0.0, accn = 0.0;
+    const long long nw = (long long)gridDim.x * 8;   // warps in the grid
+    const long long stride = nw * RPW * P;           // elements between a warp's consecutive row groups
+    // element (row, sub) of row group g: (g * RPW + rsub) * P + sub
+    const long long e0 = ((long long)blockIdx.x * 8 + warp) * RPW * P + rsub * P + sub;
+    const long long ne = a.n * P;
+    for (long long eb = e0; eb - sub - rsub * P < ne; eb += stride * UNR) {
+        double x[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const long long e = eb + u * stride;
+            x[u] = (in && e < ne) ? a.F[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const long long e = eb + u * stride;
+            const bool ok = in && e < ne;
+            if (sub == ncol) {
+                x[u] = x[u] * inv;
+                if (ok) a.F[e] = x[u];
+            }
+            double t = __shfl_sync(0xffffffffu, x[u], src);
+            if (upd) {
+                double sdot = c * x[u];
+#pragma unroll
+                for (int o = LP / 2; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+                t = t - sdot;
+                if (sub == col && ok) a.F[e] = t;
+            }
+            if (sub < Kd) acc = fma(x[u], t, acc);
+            if (sub == col) accn = fma(t, t, accn);
+        }
+    }
+    // lane sub of every row group holds column sub's partial: sum over the RPW groups, then warps
+#pragma unroll
+    for (int o = LP; o < 32; o <<= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        accn += __shfl_xor_sync(0xffffffffu, accn, o);
+    }
+    if (lane < LP) sred[warp][lane] = acc;
+    if (lane == col) sred[warp][LP] = accn;   // (lane col < LP is in row group 0)
+    __syncthreads();
+    const int nv = Kd + (a.want_norm ? 1 : 0);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int l = v < Kd ? v : LP;
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sred[w][l];
+        a.part[(size_t)v * a.nb + blockIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(a.cnt, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int v = warp; v < nv; v += 8) {
+        double s = 0.0;
+        for (int b = lane; b < a.nb; b += 32) s += __ldcg(a.part + (size_t)v * a.nb + b);
+        s = warp_sum(s);
+        if (lane == 0) a.out[v] = s;
+    }
+    if (threadIdx.x == 0) *a.cnt = 0u;
+}
+
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
     unsigned long long z = x + 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

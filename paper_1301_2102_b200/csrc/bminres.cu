@@ -1,3 +1,4 @@
+#include <chrono>
 // bminres.cu -- host driver and C ABI (include/bminres.h) of the B200 block-MINRES hot path.
 //
 // One block step k (p banded iterations) is a main branch and a side branch:
@@ -474,6 +475,39 @@ void launch_dots(bminres_ctx* h, long long n, const std::vector<Col>& v, Col t, 
     k_dots<<<a.nb, 256, 0, h->stream>>>(a);
     check_launch(h, "k_dots");
     allred(h, out, a.K, h->stream);
+}
+
+// debugging (BMINRES_DEBUG_TIMES): host wall time of the solve's segments, synchronising
+struct SegTimer {
+    bminres_ctx* h;
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    explicit SegTimer(bminres_ctx* hh) : h(hh), on(getenv("BMINRES_DEBUG_TIMES") != nullptr) {
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        CK(cudaStreamSynchronize(h->stream));
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "  [seg] %-12s %9.1f us\n", what, std::chrono::duration<double, std::micro>(t - t0).count());
+        t0 = t;
+    }
+};
+
+// k_colstep (aux_kernels.cuh) for the compiled p; out gets Kd dots (+ the norm), allreduced
+void launch_colstep(bminres_ctx* h, double* F, long long n, int p, int col, int Kc, const double* cin, int Kd,
+                    bool want_norm, int ncol, const double* nsrc, double* out) {
+    ColStepArgs a{F, n, col, Kc, Kd, ncol, want_norm ? 1 : 0, cin, nsrc, h->part, 0, out, h->dcnt + 3};
+    a.nb = grid_for(h, n, 256, std::min(NB_MAX, 4 * h->n_sm));   // one wave (4 CTAs per SM)
+    switch (p) {
+#define CS(P) case P: k_colstep<P><<<a.nb, 256, 0, h->stream>>>(a); break;
+        CS(1) CS(2) CS(3) CS(4) CS(5) CS(6) CS(7) CS(8) CS(16) CS(32)
+#undef CS
+        default: fail(h, BMINRES_EINVAL, "k_colstep: p not compiled");
+    }
+    check_launch(h, "k_colstep");
+    const int nv = Kd + (want_norm ? 1 : 0);
+    if (nv > 0) allred(h, out, nv, h->stream);
 }
 
 // host-visible dot products (synchronising)
@@ -1135,6 +1169,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     h->stats = bminres_stats_t{};
     h->slow_blocks = 0;
     CK(cudaEventRecord(e_solve0, h->stream));
+    SegTimer seg(h);
 
     // ---- inputs: device pointers are used in place; host pointers are staged
     StepPtrs sp{};
@@ -1303,22 +1338,30 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // step-0 deflation (eqn.init-QR; reading C13); CholQR2 fast path when no
         // column can deflate
         long long nrep0 = 0;
+        seg.mark("stage+norms");
         const bool fast = fast_start(h, F, n, p, S);
+        seg.mark(fast ? "fast_start" : "fast_fail");
+        // Column path: per column one pass per CGS step over the panel (k_colstep: 1 -- normalise
+        // the previous column, dots; 2 -- subtract, dots; 3 -- subtract, norm) and one host read
+        double* d1 = h->dsc + 8;
+        double* d2 = h->dsc + 8 + MAXP;
+        double* dn[2] = {h->dsc + 8 + 2 * MAXP, h->dsc + 8 + 2 * MAXP + 1};   // ||f_i||^2 by parity
+        int pend = -1;   // column whose normalisation (by 1/sqrt(*dn[pend & 1])) is pending
         for (int i = 0; i < (fast ? 0 : p); ++i) {
-            Col fi{F + i, p};
-            std::vector<Col> prev;
-            for (int l = 0; l < i; ++l) prev.push_back(Col{F + l, p});
-            if (i > 0) {
-                for (int pass = 0; pass < 2; ++pass) {
-                    launch_dots(h, n, prev, fi, h->dsc + 8 + pass * MAXP);
-                    launch_axpy(h, n, prev, nullptr, h->dsc + 8 + pass * MAXP, 1.0, fi, 1.0);
-                }
+            const double* nsrc = pend >= 0 ? dn[pend & 1] : nullptr;
+            if (i == 0) {
+                launch_colstep(h, F, n, p, 0, 0, nullptr, 0, true, -1, nullptr, dn[0]);
+            } else {
+                launch_colstep(h, F, n, p, i, 0, nullptr, i, false, pend, nsrc, d1);
+                launch_colstep(h, F, n, p, i, i, d1, i, false, -1, nullptr, d2);
+                launch_colstep(h, F, n, p, i, i, d2, 0, true, -1, nullptr, dn[i & 1]);
             }
-            std::vector<double> c2(2 * MAXP, 0.0);
-            if (i > 0)
-                CK(cudaMemcpyAsync(c2.data(), h->dsc + 8, 2 * MAXP * sizeof(double), cudaMemcpyDeviceToHost,
-                                   h->stream));
-            const double hh = std::sqrt(dots_host(h, n, {fi}, fi)[0]);
+            pend = -1;
+            std::vector<double> c2(2 * MAXP + 2, 0.0);
+            CK(cudaMemcpyAsync(c2.data(), h->dsc + 8, (2 * MAXP + 2) * sizeof(double), cudaMemcpyDeviceToHost,
+                               h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            const double hh = std::sqrt(c2[2 * MAXP + (i & 1)]);
             for (int l = 0; l < i; ++l) S[l * MAXP + i] = c2[l] + c2[MAXP + l];
             if (hh <= tau * f0n[i]) {
                 bminres_event ev{};
@@ -1329,19 +1372,24 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
                 ev.ratio = f0n[i] > 0 ? hh / f0n[i] : 0.0;
                 h->events.push_back(ev);
                 S[i * MAXP + i] = 0.0;
+                // replaced by a random vector (C17), orthogonalised twice against f_1..f_{i-1} and
+                // normalised (deferred, as a kept column; no host read)
                 launch_rand(h, F + i, p, n, A->row_begin, o.seed, 0, (uint64_t)nrep0++);
-                if (i > 0)
-                    for (int pass = 0; pass < 2; ++pass) {
-                        launch_dots(h, n, prev, fi, h->dsc + 8);
-                        launch_axpy(h, n, prev, nullptr, h->dsc + 8, 1.0, fi, 1.0);
-                    }
-                const double rn = std::sqrt(dots_host(h, n, {fi}, fi)[0]);
-                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, fi, 1.0 / rn);
+                if (i > 0) {
+                    launch_colstep(h, F, n, p, i, 0, nullptr, i, false, -1, nullptr, d1);
+                    launch_colstep(h, F, n, p, i, i, d1, i, false, -1, nullptr, d2);
+                    launch_colstep(h, F, n, p, i, i, d2, 0, true, -1, nullptr, dn[i & 1]);
+                } else {
+                    launch_colstep(h, F, n, p, 0, 0, nullptr, 0, true, -1, nullptr, dn[0]);
+                }
+                pend = i;
             } else {
                 S[i * MAXP + i] = hh;
-                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, fi, 1.0 / hh);
+                pend = i;   // f_i / hh, applied by the next column's first pass (or below)
             }
         }
+        if (pend >= 0) launch_colstep(h, F, n, p, 0, 0, nullptr, 0, false, pend, dn[pend & 1], nullptr);
+        seg.mark("column path");
         // replacement pool (reading C18): drawn now, orthogonalised twice against U_p
         std::vector<Col> ucols;
         for (int l = 0; l < p; ++l) ucols.push_back(Col{F + l, p});
@@ -1377,6 +1425,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         init.status = 1;
         finished = true;
     }
+    seg.mark("pool+S");
     CK(cudaMemcpyAsync(h->st, &init, sizeof(DevState), cudaMemcpyHostToDevice, h->stream));
     halo_exchange(h, h->V[1], p, h->stream);   // U_1 rows the peers' first SpMM reads
     if (hist_cap) CK(cudaMemcpyAsync(h->hist, h0.data(), p * sizeof(double), cudaMemcpyHostToDevice, h->stream));
@@ -1396,7 +1445,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     // order, with an event pair around each (the kernels the product runs, timed one by one)
     const bool fused_expl = o.timing && h->kf.fused;
     if (a_async) CK(cudaStreamWaitEvent(h->stream, h->ev_a, 0));   // A staged before its first use
+    seg.mark("init state");
     if (graphs && !finished) build_graphs(h, sp, n);
+    seg.mark("graphs");
     CK(cudaEventRecord(e_loop0, h->stream));
     const long long nblocks = (maxit + p - 1) / p;
     const int GB = h->gblocks;               // block steps per graph
@@ -1487,6 +1538,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
     if (getenv("BMINRES_DEBUG_STATE")) debug_state(h, "exit");
     {
+        seg.mark("loop");
         TimeMark tm(h, PH_RESID);
         const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);   // (V slots are free now)
         spmm_plain(h, h->kf, sp.rowptr, sp.col, sp.val, Xe, h->M[0], n, h->stream, h->tpw);
