@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(256) k_axpy(AxpyArgs a) {
 //   1. if ncol >= 0: F(:,ncol) *= 1/sqrt(*nsrc)        (the previous column's deferred normalisation)
 //   2. if cin:      F(:,col) -= sum_{l<Kc} cin[l] F(:,l)  (one classical Gram-Schmidt pass)
 //   3. out[l] = F(:,l)^T F(:,col), l < Kd; if want_norm: out[Kd] = F(:,col)^T F(:,col)
+// With text != null the target vector is text[i * ts] (a vector outside the panel, e.g. a
+// replacement-pool vector) instead of F(:,col); col must then be 0.
 // Each thread owns whole rows (the row's P values in registers), so 1-3 need no ordering beyond
 // the row; the reductions are deterministic (per-thread, warp, CTA, then CTAs in order).
 struct ColStepArgs {
@@ -109,11 +111,13 @@ struct ColStepArgs {
     int nb;
     double* out;
     unsigned* cnt;
+    double* text;
+    long long ts;
 };
 
 // Lane layout: LP = next power of two >= P lanes per row (lane sub holds F(i, sub)), 32 / LP rows
 // per warp instruction, so each load is a contiguous, coalesced run of rows.
-template <int P>
+template <int P, bool TEXT>
 __global__ void __launch_bounds__(256, 4) k_colstep(ColStepArgs a) {
     constexpr int LP = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : P <= 16 ? 16 : 32;
     constexpr int RPW = 32 / LP;
@@ -149,13 +153,24 @@ __global__ void __launch_bounds__(256, 4) k_colstep(ColStepArgs a) {
                 x[u] = x[u] * inv;
                 if (ok) a.F[e] = x[u];
             }
-            double t = __shfl_sync(0xffffffffu, x[u], src);
+            double t;
+            long long row = 0;
+            if constexpr (TEXT) {
+                row = (e - sub) / P;
+                t = row < a.n ? a.text[row * a.ts] : 0.0;
+            } else {
+                t = __shfl_sync(0xffffffffu, x[u], src);
+            }
             if (upd) {
                 double sdot = c * x[u];
 #pragma unroll
                 for (int o = LP / 2; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
                 t = t - sdot;
-                if (sub == col && ok) a.F[e] = t;
+                if constexpr (TEXT) {
+                    if (sub == 0 && row < a.n) a.text[row * a.ts] = t;
+                } else {
+                    if (sub == col && ok) a.F[e] = t;
+                }
             }
             if (sub < Kd) acc = fma(x[u], t, acc);
             if (sub == col) accn = fma(t, t, accn);

@@ -496,11 +496,17 @@ struct SegTimer {
 
 // k_colstep (aux_kernels.cuh) for the compiled p; out gets Kd dots (+ the norm), allreduced
 void launch_colstep(bminres_ctx* h, double* F, long long n, int p, int col, int Kc, const double* cin, int Kd,
-                    bool want_norm, int ncol, const double* nsrc, double* out) {
-    ColStepArgs a{F, n, col, Kc, Kd, ncol, want_norm ? 1 : 0, cin, nsrc, h->part, 0, out, h->dcnt + 3};
+                    bool want_norm, int ncol, const double* nsrc, double* out, double* text = nullptr,
+                    long long ts = 1) {
+    ColStepArgs a{F, n, text ? 0 : col, Kc, Kd, ncol, want_norm ? 1 : 0, cin, nsrc, h->part, 0, out, h->dcnt + 3,
+                  text, ts};
     a.nb = grid_for(h, n, 256, std::min(NB_MAX, 4 * h->n_sm));   // one wave (4 CTAs per SM)
     switch (p) {
-#define CS(P) case P: k_colstep<P><<<a.nb, 256, 0, h->stream>>>(a); break;
+#define CS(P)                                                                           \
+    case P:                                                                             \
+        if (text) k_colstep<P, true><<<a.nb, 256, 0, h->stream>>>(a);                  \
+        else k_colstep<P, false><<<a.nb, 256, 0, h->stream>>>(a);                      \
+        break;
         CS(1) CS(2) CS(3) CS(4) CS(5) CS(6) CS(7) CS(8) CS(16) CS(32)
 #undef CS
         default: fail(h, BMINRES_EINVAL, "k_colstep: p not compiled");
@@ -1391,15 +1397,14 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         if (pend >= 0) launch_colstep(h, F, n, p, 0, 0, nullptr, 0, false, pend, dn[pend & 1], nullptr);
         seg.mark("column path");
         // replacement pool (reading C18): drawn now, orthogonalised twice against U_p
-        std::vector<Col> ucols;
-        for (int l = 0; l < p; ++l) ucols.push_back(Col{F + l, p});
         for (int qq = 0; qq < q; ++qq) {
-            Col r{h->pool + qq, std::max(q, 1)};
-            launch_rand(h, h->pool + qq, std::max(q, 1), n, A->row_begin, o.seed, 1, (uint64_t)qq);
-            for (int pass = 0; pass < 2; ++pass) {
-                launch_dots(h, n, ucols, r, h->dsc + 8);
-                launch_axpy(h, n, ucols, nullptr, h->dsc + 8, 1.0, r, 1.0);
-            }
+            double* r = h->pool + qq;
+            const long long rs = std::max(q, 1);
+            launch_rand(h, r, rs, n, A->row_begin, o.seed, 1, (uint64_t)qq);
+            // two classical Gram-Schmidt passes against U_p, one pass over the panel each
+            launch_colstep(h, F, n, p, 0, 0, nullptr, p, false, -1, nullptr, h->dsc + 8, r, rs);
+            launch_colstep(h, F, n, p, 0, p, h->dsc + 8, p, false, -1, nullptr, h->dsc + 8 + MAXP, r, rs);
+            launch_colstep(h, F, n, p, 0, p, h->dsc + 8 + MAXP, 0, false, -1, nullptr, nullptr, r, rs);
         }
     }
     // T = S, history[0], while-test (Alg. 2, reading C7)
