@@ -321,6 +321,20 @@ def test_host_pointers_full_size_bitwise():
     np.testing.assert_array_equal(ref1.history, r1.history)
 
 
+def test_host_pointers_with_x0_bitwise():
+    """Host A / B / X with X0 given (use_x0: the start block needs A, so A is staged on the solver
+    stream before it): bitwise the device-pointer path."""
+    from paper_1301_2102_b200 import Solver
+    P = synth.config(2)
+    X0 = synth.gaussian_rhs(P.B.shape[0], P.B.shape[1], seed=11) * 0.1
+    ref = gpu_solve(P.A, P.B, X0=X0, tol=0.0, maxit=40)
+    Xh = X0.copy()
+    with Solver(0, use_x0=True) as s:
+        r = s.solve(P.A, P.B, Xh, tol=0.0, maxit=40)
+    np.testing.assert_array_equal(ref.X, r.X)
+    np.testing.assert_array_equal(ref.history, r.history)
+
+
 def test_invalid_arguments():
     P = synth.config("1c")
     assert gpu_solve(P.A, np.ones((P.n, 9)), tol=1e-8, maxit=10).status_name == "EINVAL"  # p = 9 not compiled
