@@ -66,6 +66,161 @@ __global__ void __launch_bounds__(256) k_dots(DotArgs a) {
     if (threadIdx.x == 0) *a.cnt = 0u;
 }
 
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+    unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// The start block's column path in ONE cooperative launch (single rank): for each column the
+// same three passes as k_colstep (normalise the previous column + dots, subtract + dots,
+// subtract + norm), separated by grid barriers instead of kernel boundaries; the deflation
+// test and the replacement (k_rand's generator, C17) are decided on the device.  Every CTA
+// reduces the partials itself in one fixed order, so all CTAs hold the same (bitwise) values.
+// Outputs: S (p x p, ld MAXP), ev[m] = {ratio, kind} of step-0 events (col m+1, kind -1: none).
+struct StartArgs {
+    double* F;
+    long long n;
+    const double* f0n;   // ||F0(:,i)|| (device)
+    double tau;
+    unsigned long long seed;
+    long long row_begin;
+    double* part;        // nb x (P + 1) partials
+    double* S;           // out
+    double* ev;          // out: 2 x P (ratio, kind)
+};
+
+template <int P>
+__global__ void __launch_bounds__(256, 4) k_start_cgs(StartArgs a) {
+    constexpr int LP = P <= 1 ? 1 : P <= 2 ? 2 : P <= 4 ? 4 : P <= 8 ? 8 : P <= 16 ? 16 : 32;
+    constexpr int RPW = 32 / LP;
+    constexpr int NV = P + 1;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sred[8][LP + 1];
+    __shared__ double sv[2][NV];   // reduced values of the last pass (d: dots, then the norm)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane % LP, rsub = lane / LP;
+    const bool in = sub < P;
+    const int nb = gridDim.x;
+    const long long nw = (long long)nb * 8;
+    const long long stride = nw * RPW * P;
+    const long long e0 = ((long long)blockIdx.x * 8 + warp) * RPW * P + rsub * P + sub;
+    const long long ne = a.n * P;
+    unsigned long long nrep = 0;
+    int npass = 0;
+    // one pass: [normalise column ncol by inv] [col = rand] [col -= sum_{l<Kc} c_l F(:,l)];
+    // dots of F(:,l), l < Kd, with F(:,col) and its norm -> sv[slot] (every CTA)
+    auto pass = [&](int col, int ncol, double inv, bool rnd, unsigned long long key, int Kc, const double* cin,
+                    int Kd, int slot) {
+        const double c = (cin && sub < Kc) ? cin[sub] : 0.0;
+        const int src = rsub * LP + col;
+        double acc = 0.0, accn = 0.0;
+        constexpr int UNR = 8;
+        for (long long eb0 = e0; eb0 - sub - rsub * P < ne; eb0 += stride * UNR) {
+            double xs[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const long long eb = eb0 + u * stride;
+                xs[u] = (in && eb < ne) ? a.F[eb] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const long long eb = eb0 + u * stride;
+                const bool ok = in && eb < ne;
+                double x = xs[u];
+                if (sub == ncol) {
+                    x = x * inv;
+                    if (ok) a.F[eb] = x;
+                }
+                if (rnd && sub == col) {
+                    const long long row = (eb - sub) / P;
+                    const unsigned long long h = splitmix64(key ^ (unsigned long long)(a.row_begin + row));
+                    x = 2.0 * ((double)(h >> 11) * 0x1.0p-53) - 1.0;
+                    if (ok) a.F[eb] = x;
+                }
+                double t = __shfl_sync(0xffffffffu, x, src);
+                if (cin) {
+                    double sdot = c * x;
+#pragma unroll
+                    for (int o = LP / 2; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+                    t = t - sdot;
+                    if (sub == col && ok) a.F[eb] = t;
+                }
+                if (sub < Kd) acc = fma(x, t, acc);
+                if (sub == col) accn = fma(t, t, accn);
+            }
+        }
+#pragma unroll
+        for (int o = LP; o < 32; o <<= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            accn += __shfl_xor_sync(0xffffffffu, accn, o);
+        }
+        if (lane < LP) sred[warp][lane] = acc;
+        if (lane == col) sred[warp][LP] = accn;
+        __syncthreads();
+        double* part = a.part + (size_t)(npass & 1) * NV * nb;   // double-buffered: one barrier per pass
+        npass++;
+        for (int v = threadIdx.x; v <= Kd; v += blockDim.x) {
+            const int l = v < Kd ? v : LP;
+            double s = 0.0;
+            for (int w = 0; w < 8; ++w) s += sred[w][l];
+            part[(size_t)v * nb + blockIdx.x] = s;
+        }
+        grid.sync();
+        for (int v = warp; v <= Kd; v += 8) {
+            double s = 0.0;
+            for (int b = lane; b < nb; b += 32) s += __ldcg(part + (size_t)v * nb + b);
+            s = warp_sum(s);
+            if (lane == 0) sv[slot][v] = s;
+        }
+        __syncthreads();
+    };
+    __shared__ double d1[P], d2[P];
+    int pend = -1;
+    double pinv = 1.0;
+    for (int i = 0; i < P; ++i) {
+        pass(i, pend, pinv, false, 0ull, 0, nullptr, i, 0);
+        for (int l = threadIdx.x; l < i; l += blockDim.x) d1[l] = sv[0][l];
+        __syncthreads();
+        pass(i, -1, 1.0, false, 0ull, i, d1, i, 1);
+        for (int l = threadIdx.x; l < i; l += blockDim.x) d2[l] = sv[1][l];
+        __syncthreads();
+        pass(i, -1, 1.0, false, 0ull, i, d2, 0, 0);
+        const double hh = sqrt(sv[0][0]);
+        const double fn = a.f0n[i];
+        if (blockIdx.x == 0)
+            for (int l = threadIdx.x; l < i; l += blockDim.x) a.S[l * MAXP + i] = d1[l] + d2[l];
+        if (hh <= a.tau * fn) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.S[i * MAXP + i] = 0.0;
+                a.ev[2 * i] = fn > 0.0 ? hh / fn : 0.0;
+                a.ev[2 * i + 1] = hh <= 1e-12 * fn ? 0.0 : 1.0;
+            }
+            // replacement (C17, stream 0, event nrep), orthogonalised twice, normalised (deferred)
+            const unsigned long long key = splitmix64(a.seed ^ (0ull << 56) ^ (nrep << 32));
+            nrep++;
+            pass(i, -1, 1.0, true, key, 0, nullptr, i, 0);
+            __syncthreads();
+            for (int l = threadIdx.x; l < i; l += blockDim.x) d1[l] = sv[0][l];
+            __syncthreads();
+            pass(i, -1, 1.0, false, 0ull, i, d1, i, 1);
+            for (int l = threadIdx.x; l < i; l += blockDim.x) d2[l] = sv[1][l];
+            __syncthreads();
+            pass(i, -1, 1.0, false, 0ull, i, d2, 0, 0);
+        } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.S[i * MAXP + i] = hh;
+            a.ev[2 * i + 1] = -1.0;
+        }
+        pend = i;
+        pinv = 1.0 / sqrt(sv[0][0]);
+        __syncthreads();
+    }
+    // the last column's normalisation
+    for (long long eb = e0; eb - sub - rsub * P < ne; eb += stride)
+        if (in && eb < ne && sub == pend) a.F[eb] = a.F[eb] * pinv;
+}
+
 // t[i] = scale * (t[i] - sum_k c_k v_k[i]); c_k from cdev (times csign) if non-null else cval
 struct AxpyArgs {
     VecRef v[MAXREF];
@@ -207,12 +362,6 @@ __global__ void __launch_bounds__(256, 4) k_colstep(ColStepArgs a) {
     if (threadIdx.x == 0) *a.cnt = 0u;
 }
 
-__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
-    unsigned long long z = x + 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
 
 // random replacement vector (reading C17): integer hash, one exact scaling -> bitwise reproducible
 __global__ void k_rand(double* out, long long stride, long long n, long long row_begin, unsigned long long seed,

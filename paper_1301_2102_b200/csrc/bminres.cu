@@ -150,6 +150,8 @@ struct bminres_ctx {
     cudaStream_t side = nullptr;   // side branch during graph capture
     cudaStream_t cstream = nullptr;   // host-A staging copies, overlapped with the start block
     cudaEvent_t ev_a = nullptr;       // host A staged (recorded on cstream)
+    double* startbuf = nullptr;       // k_start_cgs: S, ||F0(:,i)||, events
+    bool coop_ok = false;             // cooperative launches supported
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     std::string err;
@@ -500,7 +502,8 @@ void launch_colstep(bminres_ctx* h, double* F, long long n, int p, int col, int 
                     long long ts = 1) {
     ColStepArgs a{F, n, text ? 0 : col, Kc, Kd, ncol, want_norm ? 1 : 0, cin, nsrc, h->part, 0, out, h->dcnt + 3,
                   text, ts};
-    a.nb = grid_for(h, n, 256, std::min(NB_MAX, 4 * h->n_sm));   // one wave (4 CTAs per SM)
+    static const int cps = getenv("BMINRES_COLSTEP_CPS") ? std::max(1, atoi(getenv("BMINRES_COLSTEP_CPS"))) : 4;
+    a.nb = grid_for(h, n, 256, std::min(NB_MAX, cps * h->n_sm));   // one wave (4 CTAs per SM)
     switch (p) {
 #define CS(P)                                                                           \
     case P:                                                                             \
@@ -514,6 +517,26 @@ void launch_colstep(bminres_ctx* h, double* F, long long n, int p, int col, int 
     check_launch(h, "k_colstep");
     const int nv = Kd + (want_norm ? 1 : 0);
     if (nv > 0) allred(h, out, nv, h->stream);
+}
+
+// k_start_cgs (aux_kernels.cuh): cooperative launch, one wave of co-resident CTAs
+void launch_start_cgs(bminres_ctx* h, double* F, long long n, int p, const double* f0n, double tau,
+                      unsigned long long seed, long long row_begin, double* S, double* ev) {
+    StartArgs sa{F, n, f0n, tau, seed, row_begin, h->part, S, ev};
+    void* args[] = {&sa};
+    const void* fn = nullptr;
+    switch (p) {
+#define SC(P) case P: fn = (const void*)k_start_cgs<P>; break;
+        SC(1) SC(2) SC(3) SC(4) SC(5) SC(6) SC(7) SC(8) SC(16) SC(32)
+#undef SC
+        default: fail(h, BMINRES_EINVAL, "k_start_cgs: p not compiled");
+    }
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0));
+    const int nb = std::max(1, std::min(NB_MAX, std::max(1, occ) * h->n_sm));
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(nb), dim3(256), args, 0, h->stream);
+    if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_start_cgs: ") + cudaGetErrorString(e));
+    h->launches++;
 }
 
 // host-visible dot products (synchronising)
@@ -1353,7 +1376,31 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         double* d2 = h->dsc + 8 + MAXP;
         double* dn[2] = {h->dsc + 8 + 2 * MAXP, h->dsc + 8 + 2 * MAXP + 1};   // ||f_i||^2 by parity
         int pend = -1;   // column whose normalisation (by 1/sqrt(*dn[pend & 1])) is pending
-        for (int i = 0; i < (fast ? 0 : p); ++i) {
+        const bool coop = !fast && !h->tp && h->coop_ok && !getenv("BMINRES_NO_COOP_START");
+        if (coop) {   // single rank: the whole column path in one cooperative launch
+            if (!h->startbuf) CK(cudaMalloc((void**)&h->startbuf, (MAXP * MAXP + 3 * MAXP) * sizeof(double)));
+            double* dS = h->startbuf;
+            double* dF0 = dS + MAXP * MAXP;
+            double* dEv = dF0 + MAXP;
+            h2d(h, dF0, f0n.data(), p * sizeof(double));
+            CK(cudaMemsetAsync(dS, 0, MAXP * MAXP * sizeof(double), h->stream));
+            launch_start_cgs(h, F, n, p, dF0, tau, o.seed, A->row_begin, dS, dEv);
+            std::vector<double> ev(2 * p);
+            CK(cudaMemcpyAsync(S.data(), dS, MAXP * MAXP * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(ev.data(), dEv, 2 * p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            for (int i = 0; i < p; ++i)
+                if (ev[2 * i + 1] >= 0.0) {
+                    bminres_event e{};
+                    e.j = 0;
+                    e.col = i + 1;
+                    e.kind = (int)ev[2 * i + 1];
+                    e.action = 1;
+                    e.ratio = ev[2 * i];
+                    h->events.push_back(e);
+                }
+        }
+        for (int i = 0; i < ((fast || coop) ? 0 : p); ++i) {
             const double* nsrc = pend >= 0 ? dn[pend & 1] : nullptr;
             if (i == 0) {
                 launch_colstep(h, F, n, p, 0, 0, nullptr, 0, true, -1, nullptr, dn[0]);
@@ -1652,6 +1699,9 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
     try {
         CK(cudaSetDevice(o.device));
         CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, o.device));
+        int coop = 0;
+        CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, o.device));
+        h->coop_ok = coop != 0;
         if (o.stream) {
             h->stream = (cudaStream_t)o.stream;
         } else {
@@ -1853,6 +1903,7 @@ void bminres_destroy(bminres_handle h) {
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->cstream) cudaStreamDestroy(h->cstream);
+    if (h->startbuf) cudaFree(h->startbuf);
     if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;

@@ -288,6 +288,21 @@ def test_config3_first_50(eps):
     assert_hist_close(r.history, ref.history)
 
 
+def test_start_column_path_variants(monkeypatch):
+    """The start block's column path runs as one cooperative launch on a single rank and as
+    per-pass k_colstep launches otherwise (row partitions): both against the oracle on config
+    3's dependent right-hand sides (8 step-0 replacements), and against each other."""
+    P = synth.config(3, eps=1e-10)
+    ref = oracle.solve(P.A, P.B, tol=P.tol, maxit=50)
+    r1 = gpu_solve(P.A, P.B, tol=P.tol, maxit=50)
+    monkeypatch.setenv("BMINRES_NO_COOP_START", "1")
+    r2 = gpu_solve(P.A, P.B, tol=P.tol, maxit=50)
+    for r in (r1, r2):
+        same_events(r.events, ref.events)
+        assert_hist_close(r.history, ref.history)
+    np.testing.assert_allclose(r1.X, r2.X, rtol=1e-9, atol=1e-12 * np.abs(r1.X).max())
+
+
 # ----------------------------------------------------------------------------- API properties
 
 
