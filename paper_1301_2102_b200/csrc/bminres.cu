@@ -142,6 +142,8 @@ struct Err {
 
 }  // namespace
 
+constexpr int GB_MAX = 25;   // block steps per graph, at most
+
 struct bminres_ctx {
     bminres_options opt{};
     int device = 0;
@@ -203,7 +205,8 @@ struct bminres_ctx {
     int nb1a = 0;
     double* AV = nullptr;
     bool pdl = true;   // programmatic dependent launch of the block-step kernels
-    int gblocks = 3;   // block steps per captured graph (fewer graph-boundary gaps; 3: +1.4% over 2 at config 2)
+    int gblocks = 3;   // block steps per captured graph (per solve: choose_gblocks)
+    bool gblocks_env = false;
     int prio_hi = 0;   // greatest stream priority (side branch)
     long long side_blocks = 0, slow_blocks = 0;
     Kfn kf{};
@@ -429,7 +432,10 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     };
     h->pdl = getenv("BMINRES_NO_PDL") == nullptr;
     h->xdefer = h->kf.fused && getenv("BMINRES_NO_XDEFER") == nullptr;
-    if (const char* gb = getenv("BMINRES_GRAPH_BLOCKS")) h->gblocks = std::max(1, std::min(6, atoi(gb)));
+    if (const char* gb = getenv("BMINRES_GRAPH_BLOCKS")) {
+        h->gblocks = std::max(1, std::min(GB_MAX, atoi(gb)));
+        h->gblocks_env = true;
+    }
     const char* ce = getenv("BMINRES_CLUSTER");
     h->csz = ce ? std::max(1, std::min(8, atoi(ce))) : 2;
     const char* oe = getenv("BMINRES_CTAS_PER_SM");
@@ -754,6 +760,25 @@ void launch_k4b(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n,
     K4bArgs a{h->V[sk], h->M[par], h->M[par ^ 1], sp.X, n, h->st, sk, h->tpw, par, force, record ? k : 0};
     h->kf.k4b<<<h->nb4, h->kf.nt4b, h->kf.smem4b, s>>>(a);
     check_launch(h, "k4b_update");
+}
+
+// Block steps per graph for a solve of nblocks block steps.  A graph boundary costs a stall:
+// each graph joins its last K3b, and the PDL overlap of K1's fused update with reduce2 is lost
+// across the boundary (~6 us at config 2; 3 -> 5 blocks per graph: 141.6k -> 143.7k it/s).
+// Blocks launched past the last one are wasted main-branch work (~9 boundaries' worth each),
+// so among 3..GB_MAX pick the count with the least boundaries + 9 x overshoot.
+int choose_gblocks(long long nblocks) {
+    int best = 3;
+    double bc = 1e300;
+    for (int g = 3; g <= GB_MAX; ++g) {
+        const long long graphs = (nblocks + g - 1) / g;
+        const double cost = (double)graphs + 9.0 * (double)(graphs * g - nblocks);
+        if (cost < bc) {
+            bc = cost;
+            best = g;
+        }
+    }
+    return best;
 }
 
 // Graph for side block s (s mod 6): main {reduce2 of block s, K1 + reduce1 + K2 of block s+1}
@@ -1498,10 +1523,11 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     const bool fused_expl = o.timing && h->kf.fused;
     if (a_async) CK(cudaStreamWaitEvent(h->stream, h->ev_a, 0));   // A staged before its first use
     seg.mark("init state");
+    const long long nblocks = (maxit + p - 1) / p;
+    if (!h->gblocks_env) h->gblocks = choose_gblocks(nblocks);
     if (graphs && !finished) build_graphs(h, sp, n);
     seg.mark("graphs");
     CK(cudaEventRecord(e_loop0, h->stream));
-    const long long nblocks = (maxit + p - 1) / p;
     const int GB = h->gblocks;               // block steps per graph
     const int LAG = std::max(2, 6 / GB);     // graphs in flight before the host polls
     std::vector<cudaEvent_t> lag_ev(LAG);
