@@ -1,2 +1,2 @@
-mkdir -p gpurun_out/lab1
-for c in 0 2 3 4 5 6; do timeout 300 scripts/micro/spmm_lab.bin $c 2>&1 | tee -a gpurun_out/lab1/lab.txt; done
+# scratch command file for gpurun (see scripts/gpu_check.sh for the full evidence run)
+bash scripts/gpu_check.sh run tests nofull
