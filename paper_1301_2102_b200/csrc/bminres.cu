@@ -154,6 +154,7 @@ struct bminres_ctx {
     cudaEvent_t ev_a = nullptr;       // host A staged (recorded on cstream)
     double* startbuf = nullptr;       // k_start_cgs: S, ||F0(:,i)||, events
     bool coop_ok = false;             // cooperative launches supported
+    DevState* hstate = nullptr;       // pinned host copy of the state (initial value, exit read)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     std::string err;
@@ -1307,7 +1308,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     }
 
     // ---- state init
-    static DevState init;
+    // the state's initial value, built in pinned host memory (one fast copy; also the exit copy)
+    if (!h->hstate) CK(cudaMallocHost((void**)&h->hstate, sizeof(DevState)));
+    DevState& init = *h->hstate;
     std::memset(&init, 0, sizeof(init));
     init.run_main = 1;
     init.k_main = 1;
@@ -1612,8 +1615,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     for (auto& e : lag_ev) cudaEventDestroy(e);
 
     // ---- exit: status, true residuals (K7), history, copy-back
-    DevState* fin = &init;   // reuse the static buffer
-    CK(cudaMemcpy(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    DevState* fin = &init;   // reuse the pinned buffer
+    CK(cudaMemcpyAsync(fin, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     if (getenv("BMINRES_DEBUG_STATE")) debug_state(h, "exit");
     {
         seg.mark("loop");
@@ -1930,6 +1934,7 @@ void bminres_destroy(bminres_handle h) {
     if (h->side) cudaStreamDestroy(h->side);
     if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->startbuf) cudaFree(h->startbuf);
+    if (h->hstate) cudaFreeHost(h->hstate);
     if (h->ev_a) cudaEventDestroy(h->ev_a);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
