@@ -1069,7 +1069,10 @@ bool fast_start(bminres_ctx* h, double* F, long long n, int p, std::vector<doubl
     upload_inverse(R1);
     h->kf.mat<<<g, 256, h->kf.smem_mat, h->stream>>>(F, h->gdev + MAXP * MAXP, U, n, p);
     check_launch(h, "k_materialize");
-    if (!host_chol(panel_gram(h, U, n, p), p, 0.5, R2)) return false;
+    if (!host_chol(panel_gram(h, U, n, p), p, 0.5, R2)) {
+        CK(cudaMemsetAsync(U, 0, (size_t)n * p * sizeof(double), h->stream));   // U_0 = 0 again
+        return false;
+    }
     upload_inverse(R2);
     h->kf.mat<<<g, 256, h->kf.smem_mat, h->stream>>>(U, h->gdev + MAXP * MAXP, F, n, p);
     check_launch(h, "k_materialize");
