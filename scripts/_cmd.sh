@@ -1,2 +1,1 @@
-# scratch command file for gpurun (see scripts/gpu_check.sh for the full evidence run)
-bash scripts/gpu_check.sh run tests nofull
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -k "converged_mid_graph" 2>&1 | tail -3

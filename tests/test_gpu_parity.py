@@ -319,6 +319,22 @@ def test_graphs_plain_and_host_pointers_bitwise():
     np.testing.assert_array_equal(r1.X, r3.X)
 
 
+def test_converged_mid_graph_bitwise():
+    """A solve that converges inside a graph (25 block steps per graph: the main branch runs on
+    past the stop until the host has synchronised): graphs give the plain launches' X, history
+    and counts bitwise, and the oracle's to the parity tolerance."""
+    P = synth.config("1c")
+    r1 = gpu_solve(P.A, P.B, tol=1e-6, maxit=4000, use_graphs=True)
+    r2 = gpu_solve(P.A, P.B, tol=1e-6, maxit=4000, use_graphs=False)
+    ref = oracle.solve(P.A, P.B, tol=1e-6, maxit=4000)
+    assert r1.status_name == "OK" and ref.status_name == "OK"
+    assert r1.iterations == r2.iterations
+    np.testing.assert_array_equal(r1.history, r2.history)
+    np.testing.assert_array_equal(r1.X, r2.X)
+    assert_counts_close(r1.iterations, ref.iterations)
+    assert_hist_close(r1.history, ref.history)
+
+
 def test_host_pointers_full_size_bitwise():
     """Host A / B / X at config 2's full size (A staged on its own stream beside the start block):
     bitwise the device-pointer path, also for a second solve on the same handle with a different
