@@ -627,11 +627,14 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
         cfg.numAttrs = 2;
     }
     // reduce2 triggers its dependent (K1(k+1) / K1a) right after its own wait: K1's fused update
-    // overlaps the reduction (+1.8% at config 2; reduce1 early: +0.3%, kept at exit)
+    // overlaps the reduction (+1.8% at config 2)
     // (not in split mode: its dependent K1a has no pre-wait work, and its early-resident CTAs would
     // take the SM slots K3b needs)
     static const int early2 = getenv("BMINRES_NO_EARLY_RED2") ? 0 : 1;
-    const int early = (which == 2 && !h->split) ? early2 : 0;
+    // reduce1 too: K2 launches during it and issues its first TMA stages (W, V_k: written by
+    // K1, which completed before reduce1's wait returned) -- config 2 145.8k -> 146.8k it/s
+    static const int early1 = getenv("BMINRES_NO_EARLY_RED1") ? 0 : 1;
+    const int early = h->split ? 0 : (which == 2 ? early2 : early1);
     cudaError_t e = (which == 2 && h->red2_fac)
                         ? cudaLaunchKernelEx(&cfg, h->kf.red2f, h->st, (int)(k & 1), early)
                         : cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, early);
