@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+# scratch command file for gpurun (see scripts/gpu_check.sh for the full evidence run)
+bash scripts/gpu_check.sh run tests nofull
