@@ -1,29 +1,37 @@
 #!/usr/bin/env python
 """bench.py — block-MINRES iterations/s on B200 (driver contract).
 
-A "step" is one bminres_solve call on the workload with a fixed iteration budget
-(--iters, default 2000 banded iterations = 250 block steps at p = 8): the start block
-(a0), then every row a1..a5 of the hot path once per block step.  The workload is
-BASELINE.json configs[1] (config 2: 3-D 7-point Laplacian 64^3 shifted by -3, p = 8,
-Gaussian B from seed 0), synthetic, fp64.
+Workload (default): BASELINE.json configs[3] -- config 4, the 3-D 7-point Laplacian on a 256^3
+grid shifted by -3 (n = 16.8M, nnz = 117M), p = 32 Gaussian right-hand sides from seed 0, fp64:
+the configuration BASELINE.json's metric ("... 1/2/4/8 B200") and the north star's targets are
+quoted on, and the largest one that fits one GPU.  A "step" is one bminres_solve call with a fixed
+budget of --iters banded iterations (default 1024 = 32 block steps at p = 32): the start block
+(row a0), then every row a1..a5 of the hot path once per block step.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
 
-`value`   = banded iterations of the solve / max-over-ranks device time (CUDA events).
-`e2e`     = the same metric through the C ABI with HOST buffers (A, B in; X out).
-`roofline`= the dominant kernel's algorithmic bytes per launch / its mean launch time
-            (CUDA events around every launch inside the timed region) vs MEASURED_PEAKS.
-`cpu_baseline` = the C oracle (tests' reference implementation) on a bounded sample.
-With N > 1 (torchrun) the ranks run ONE solve of the workload with the rows partitioned over
-them (halo exchange + allreduces over NCCL; strong scaling).  Testing
-aids: BENCH_BACKEND=gloo + BENCH_COMM=gloo run the same path with the host-callback transport
-(e.g. two ranks sharing one GPU).
+`value`      = banded iterations / max-over-ranks device time (CUDA events on the solver stream).
+`e2e`        = the same metric through the C ABI with HOST buffers (A, B in; X out per step).
+`roofline`   = the dominant kernel's algorithmic bytes per launch / its mean launch time (CUDA
+               events around every launch, timing mode) vs MEASURED_PEAKS.json.
+`step_roofline` = (CSR A + 10 panels) per block step / graph-mode time per block step.
+`cpu_baseline`  = the C oracle (the tests' reference implementation), one thread, on a bounded
+               sample of the same workload, run in a subprocess beside the GPU measurements.
+`secondary`  = config 2 (3-D 64^3, p = 8: BASELINE configs[1]) measured the same way (no e2e).
+`time_to_tol`= config 2 solved to tol 1e-8 (the north star's convergence gate at scale): iterations,
+               device time with and without one-time setup, true residuals, against the oracle's
+               count from tests/golden when present.
+With --gpus N > 1 the script re-executes itself under torch.distributed.run (one rank per GPU over
+NCCL) unless WORLD_SIZE is already set; the ranks run ONE solve with the rows partitioned (halo
+exchange + allreduces; strong scaling).  Testing aids: BENCH_BACKEND=gloo +
+BENCH_COMM=gloo run the same path with the host-callback transport (e.g. two ranks on one GPU).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,18 +43,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# algorithmic panel transfers per launch; K1 also streams CSR A
-# algorithmic panel transfers per launch.  The fused M/X update moves 5 panels on average: it
-# reads V_k, M_{k-2}, M_{k-1} and writes M_k every block, and reads + writes X every other block
-# (X updates deferred in pairs); the standalone K4b moves 6.
 # BASELINE.json's metric (the value is iterations/s; the achieved HBM GB/s against the roofline is
 # reported in "roofline" / "step_roofline")
 METRIC = "block-MINRES iterations/s and achieved HBM GB/s (fp64) vs roofline, 1/2/4/8 B200"
+# algorithmic panel transfers per launch; K1 also streams CSR A.  The fused M/X
+# update moves 5 panels on average: it reads V_k, M_{k-2}, M_{k-1} and writes M_k every block, and
+# reads + writes X every other block (X updates deferred in pairs); the standalone K4b moves 6.
 PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 8, "orth": 3, "update": 6,
                       # split mode (large panels): K1a reads V_k once (gathers) and writes AV; K1 then
                       # streams AV, V_k, V_{k-1} and writes W (+ the fused update)
                       "spmm_av": 2, "epilogue": 4, "epilogue_fused": 9}
 PHASE_READS_A = {"spmm", "spmm_fused", "spmm_av"}
+DEFAULT_ITERS = {"1": 2000, "1c": 2000, "2": 2000, "3": 2000, "4": 1024, "5": 1024}
 
 
 def load_peaks():
@@ -54,9 +62,21 @@ def load_peaks():
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_info() -> dict:
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
 
 
 class ClockSampler:
@@ -130,7 +150,8 @@ def max_over_ranks(x: float, world: int, device) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=device if os.environ.get("BENCH_BACKEND", "nccl") == "nccl"
+                     else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -141,68 +162,87 @@ def barrier(world):
         dist.barrier()
 
 
-def cpu_sample_iters(P, budget_s: float = 15.0) -> int:
-    """Iterations of the bounded oracle sample: ~budget_s of one-thread CPU work, from the oracle's
-    measured cost on config 2 (~0.8 ns per unit of nnz + 8 n p per iteration), 2 .. 400 (configs 4/5: the
-    oracle's start block alone is tens of seconds)."""
+# ----------------------------------------------------------------------------- the oracle (CPU baseline)
+
+ORACLE_SAMPLE = r"""
+import json, sys, time
+sys.path.insert(0, {root!r})
+import oracle, synth
+cfg = {cfg!r}
+P = synth.config(cfg if cfg == "1c" else int(cfg))
+oracle.lib()
+r = oracle.solve(P.A, P.B, tol=P.tol, maxit={iters}, tau=P.tau, pool_size=1, history=False)
+print(json.dumps({{"iterations": r.iterations, "start_s": r.start_s, "loop_s": r.loop_s, "name": P.name}}))
+"""
+
+
+def oracle_sample_iters(P, budget_s: float = 20.0) -> int:
+    """Iterations of the bounded oracle sample: ~budget_s of one-thread loop time, from the oracle's
+    measured cost on config 2 (26 ms per iteration: ~0.8 ns per unit of nnz/p + 8 n (2p+1) per
+    iteration), 2 .. 400."""
     units = float(P.A.nnz) + 8.0 * P.n * P.p
     est = budget_s / (0.82e-9 * units)
     return int(max(2, min(400, est)))
 
 
-def cpu_baseline(P, iters: int):
-    """The oracle as it stands, one thread, on the first `iters` iterations of the workload."""
-    import oracle
-    oracle.lib()
-    t0 = time.perf_counter()
-    r = oracle.solve(P.A, P.B, tol=P.tol, maxit=iters, tau=P.tau, pool_size=1)
-    dt = time.perf_counter() - t0
-    return {"value": r.iterations / dt, "unit": "iterations/s", "cores": 1, "kind": "oracle",
-            "sample": f"{P.name}: one oracle solve of {r.iterations} iterations (start block included), "
-                      f"{dt:.1f} s, 1 thread"}
+def start_oracle_sample(cfg: str, iters: int):
+    """The oracle as it stands, one thread, in a subprocess (it runs beside the GPU measurements on
+    another host core): one solve of `iters` iterations of the workload.  Its loop time (the start
+    block and the pool are timed separately) gives the per-iteration rate."""
+    code = ORACLE_SAMPLE.format(root=ROOT, cfg=cfg, iters=iters)
+    return subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+
+
+def finish_oracle_sample(proc, kind="oracle"):
+    out, err = proc.communicate()
+    if proc.returncode != 0:
+        return {"value": None, "unit": "iterations/s", "cores": 1, "kind": kind,
+                "sample": f"oracle sample failed: {err.strip().splitlines()[-1:] if err else proc.returncode}"}
+    d = json.loads(out.strip().splitlines()[-1])
+    value = d["iterations"] / d["loop_s"] if d["loop_s"] > 0 else None
+    return {"value": value, "unit": "iterations/s", "cores": 1, "kind": kind,
+            "sample": (f"{d['name']}: one oracle solve of {d['iterations']} banded iterations, one thread; value = "
+                       f"iterations / loop time ({d['loop_s']:.1f} s); its start block + pool took "
+                       f"{d['start_s']:.1f} s (not in the value)"),
+            "start_block_s": d["start_s"], "loop_s": d["loop_s"], "iterations": d["iterations"], **host_info()}
 
 
 def run_reference(args):
+    """The reference arm: the oracle (this tier has no reference code) on the same workload.  One
+    bounded sample: a solve of W + K banded iterations; value = iterations / loop time."""
     world, rank, local = dist_init()
     if rank != 0:
         return 0
-    P = problem(args.config)
-    import oracle
-    oracle.lib()
-    iters = args.ref_iters
-    for _ in range(args.warmup):
-        oracle.solve(P.A, P.B, tol=P.tol, maxit=max(2, iters // 8), tau=P.tau)
+    cfg = args.config
+    P = problem(cfg)
+    iters = max(2, args.warmup + args.steps) if args.ref_iters <= 0 else args.ref_iters
+    del P
     t0 = time.perf_counter()
-    total = 0
-    for _ in range(args.steps):
-        r = oracle.solve(P.A, P.B, tol=P.tol, maxit=iters, tau=P.tau, pool_size=1)
-        total += r.iterations
-    dt = time.perf_counter() - t0
-    value = total / dt
+    cpu = finish_oracle_sample(start_oracle_sample(cfg, iters))
+    wall = time.perf_counter() - t0
+    value = cpu["value"]
+    P = problem(cfg)
     line = {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": P.name, "n": P.n, "p": P.p, "iters_per_step": iters},
-            "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} oracle solves of {iters} iterations of {P.name}"},
+            "ms_per_step": 1e3 * cpu["loop_s"] / max(1, cpu["iterations"]) if value else None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": P.name, "n": P.n, "p": P.p, "nnz": P.A.nnz,
+                       "step": "one banded iteration of one oracle solve (W + K iterations in total)"},
+            "cpu_baseline": cpu, "wall_s": wall,
             "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_ours(args):
-    import torch
-    world, rank, local = dist_init()
-    local = local % max(1, torch.cuda.device_count())   # (ranks may share a GPU when testing)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    from paper_1301_2102_b200 import DeviceCsr, Solver
+# ----------------------------------------------------------------------------- our arm
 
-    P = problem(args.config)
+
+def measure(P, args, iters, world, rank, local, dev, *, e2e: bool, kernel_timing: bool):
+    """Device-timed solves of the workload (graphs, the product's launch mode), the per-kernel
+    roofline in timing mode, and optionally the end-to-end host-buffer solves."""
+    import torch
+    from paper_1301_2102_b200 import DeviceCsr, HostCsrRows, Solver
     n, p = P.n, P.p
-    # N > 1: one solve of the workload, rows partitioned over the ranks (halo exchange and
-    # allreduces over NCCL; DESIGN.md "Multi-GPU") -- strong scaling
     off = [n * q // world for q in range(world + 1)]
     r0, r1 = off[rank], off[rank + 1]
     A = DeviceCsr.from_host(P.A, dev) if world == 1 else DeviceCsr.rows_from_host(P.A, r0, r1, dev)
@@ -215,18 +255,18 @@ def run_ours(args):
         comm = TorchComm() if os.environ.get("BENCH_COMM", "nccl") == "gloo" else "nccl"
     n_loc = r1 - r0
     stream = torch.cuda.Stream(device=dev)
-    iters = args.iters
     peak, peak_kind = load_peaks()
     nnz_loc = int(P.A.indptr[r1]) - int(P.A.indptr[r0])
     abytes = 12.0 * nnz_loc + 4.0 * (n_loc + 1)   # this rank's CSR rows
     panel = 8.0 * n_loc * p
+    kw = dict(pool_size=1, record_history=False, stream=stream.cuda_stream, rank=rank, world=world, comm=comm,
+              plan_reuse=True)
 
     # ---- timed region: the product's launch mode (CUDA graphs, main/side branches overlapped)
-    solver = Solver(local, pool_size=1, use_graphs=not args.no_graphs, timing=False, record_history=False,
-                    stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
+    solver = Solver(local, use_graphs=not args.no_graphs, timing=False, **kw)
 
-    def step(s):
-        return s.solve(A, B, X, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
+    def step(s, Ain=A, Bin=B, Xin=X):
+        return s.solve(Ain, Bin, Xin, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
 
     for _ in range(args.warmup):
         step(solver)
@@ -254,15 +294,14 @@ def run_ours(args):
     value = total_iters / (ms_max / 1e3)   # iterations of the (one, partitioned) solve per second
     solver.close()
 
-    # ---- kernel-timing region: the same steps with a CUDA event pair around every kernel
-    # launch (explicit launches, kernels serialised on one stream), for the roofline
+    # ---- kernel-timing region: the same steps with a CUDA event pair around every kernel launch
+    # (explicit launches in the graph's order, serialised on the solver stream), for the roofline
     roof = None
-    if not args.no_kernel_timing:
-        st_t = Solver(local, pool_size=1, use_graphs=False, timing=True, record_history=False,
-                      stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
+    if kernel_timing:
+        st_t = Solver(local, use_graphs=False, timing=True, **kw)
         step(st_t)
         phase_ms, phase_n = {}, {}
-        for _ in range(args.steps):
+        for _ in range(max(1, min(args.steps, 3))):
             r = step(st_t)
             for k, v in r.stats["phase_ms"].items():
                 phase_ms[k] = phase_ms.get(k, 0.0) + v
@@ -292,23 +331,25 @@ def run_ours(args):
     # whole-step algorithmic roofline (CSR A + 10 panels per block step)
     blk_bytes = abytes + 10 * panel
     blocks = total_iters / p
-    step_roof = {"bytes_per_block_step": blk_bytes,
-                 "achieved_GBps": blk_bytes * blocks / (ms / 1e3) / 1e9}
+    step_roof = {"bytes_per_block_step": blk_bytes, "ms_per_block_step": ms_max / max(blocks, 1),
+                 "achieved_GBps": blk_bytes * blocks / (ms_max / 1e3) / 1e9,
+                 "note": "graph-mode device time of the whole solve (start block included) per block step"}
     step_roof["frac_of_measured"] = step_roof["achieved_GBps"] / peak
 
-    # end to end through the C ABI with host buffers (pinned A arrays, B and X)
-    e2e = None
-    if not args.no_e2e:
-        from paper_1301_2102_b200 import HostCsrRows
+    # ---- end to end through the C ABI with host buffers (pinned A arrays, B and X)
+    e2e_d = None
+    if e2e:
         Ah = HostCsrRows.from_host(P.A, 0, P.A.n) if world == 1 else HostCsrRows.from_host(P.A, r0, r1)
 
         def pinned(a):   # numpy view of a pinned copy (the library's H2D copies then run at DMA speed)
             return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         Ahost = HostCsrRows(Ah.n, pinned(Ah.indptr), pinned(Ah.indices), pinned(Ah.data), Ah.row_begin, Ah.n_global)
+        del Ah
         Bh = torch.from_numpy(Bh_full).pin_memory()
         Xh = torch.zeros_like(Bh).pin_memory()
-        s2 = Solver(local, pool_size=1, use_graphs=True, timing=False, record_history=False,
-                    stream=stream.cuda_stream, rank=rank, world=world, comm=comm)
+        del A, B, X, step   # (the device copies are not needed by the host-buffer solves)
+        torch.cuda.empty_cache()
+        s2 = Solver(local, use_graphs=True, timing=False, **kw)
         s2.solve(Ahost, Bh, Xh, tol=P.tol, maxit=iters, deflation_tol=P.tau, history=False)
         torch.cuda.synchronize()
         barrier(world)
@@ -320,35 +361,117 @@ def run_ours(args):
         dt = time.perf_counter() - t0
         dt = max_over_ranks(dt, world, dev)
         s2.close()
-        e2e = {"value": e_iters / dt, "unit": "iterations/s",
-               "h2d_bytes_per_step": int(abytes + panel), "d2h_bytes_per_step": int(panel)}
+        e2e_d = {"value": e_iters / dt, "unit": "iterations/s",
+                 "h2d_bytes_per_step": int(abytes + panel), "d2h_bytes_per_step": int(panel),
+                 "timing": "host wall clock around bminres_solve with pinned host A, B, X (copies inside)"}
+    torch.cuda.empty_cache()
+    return {"value": value, "ms": ms_max, "total_iters": total_iters, "launches": launches, "slow_blocks": slow,
+            "clocks": clk, "roofline": roof, "step_roofline": step_roof, "e2e": e2e_d, "peak": peak,
+            "abytes": abytes, "panel": panel, "n_loc": n_loc}
 
-    cpu = None
+
+def time_to_tol(cfg, local, dev):
+    """One solve of the config to its tol (maxit = the config's), cold (first call on a fresh handle:
+    workspace, graph capture) and warm (second call).  Device times from the library's CUDA events;
+    the cold call's host wall time includes the one-time setup."""
+    import torch
+    from paper_1301_2102_b200 import DeviceCsr, Solver
+    P = problem(cfg)
+    A = DeviceCsr.from_host(P.A, dev)
+    B = torch.from_numpy(P.B).to(dev)
+    out = {"workload": P.name, "tol": P.tol, "maxit": P.maxit}
+    with Solver(local, pool_size=1, record_history=False) as s:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = s.solve(A, B, tol=P.tol, maxit=P.maxit, deflation_tol=P.tau, history=False, raise_on_error=False)
+        cold = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r2 = s.solve(A, B, tol=P.tol, maxit=P.maxit, deflation_tol=P.tau, history=False, raise_on_error=False)
+        warm = time.perf_counter() - t0
+    out.update({"status": r2.status_name, "iterations": r2.iterations, "block_steps": r2.stats["block_steps"],
+                "slow_blocks": r2.stats["slow_blocks"], "events": len(r2.events),
+                "device_ms": r2.stats["solve_ms"], "loop_ms": r2.stats["loop_ms"],
+                "wall_s_cold_with_setup": cold, "wall_s_warm": warm,
+                "iterations_per_s": r2.iterations / (r2.stats["solve_ms"] / 1e3),
+                "max_true_res": max(r2.stats["true_res"]), "max_comp_res": max(r2.stats["comp_res"]),
+                "true_res_le_tol": bool(max(r2.stats["true_res"]) <= P.tol),
+                "cold_equals_warm_iterations": r.iterations == r2.iterations})
+    gpath = os.path.join(ROOT, "tests", "golden", f"{P.name}_tol.json")
+    if os.path.exists(gpath):
+        g = json.load(open(gpath))
+        out["oracle_iterations"] = g["iterations"]
+        out["oracle_status"] = g["status"]
+        out["count_rel_diff"] = (r2.iterations - g["iterations"]) / max(1, g["iterations"])
+        out["oracle_ms_per_iteration"] = g.get("ms_per_iteration")
+    return out
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_init()
+    local = local % max(1, torch.cuda.device_count())   # (ranks may share a GPU when testing)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    cfg = args.config
+    iters = args.iters if args.iters > 0 else DEFAULT_ITERS[cfg]
+    P = problem(cfg)
+    # the CPU baseline runs in its own process on another host core while the GPU is measured
+    cpu_proc = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(P, args.cpu_iters if args.cpu_iters > 0 else cpu_sample_iters(P))
+        cpu_proc = start_oracle_sample(cfg, args.cpu_iters if args.cpu_iters > 0 else oracle_sample_iters(P))
+    main = measure(P, args, iters, world, rank, local, dev, e2e=not args.no_e2e,
+                   kernel_timing=not args.no_kernel_timing)
+    n, p, name, nnz, tol, tau = P.n, P.p, P.name, P.A.nnz, P.tol, P.tau
+    del P
+
+    secondary = {}
+    if world == 1 and args.secondary:
+        for c in args.secondary.split(","):
+            if c and c != cfg:
+                Q = problem(c)
+                m = measure(Q, args, DEFAULT_ITERS[c], 1, 0, local, dev, e2e=False, kernel_timing=True)
+                secondary[Q.name] = {"value": m["value"], "unit": "iterations/s", "iters_per_step": DEFAULT_ITERS[c],
+                                     "n": Q.n, "p": Q.p, "ms_per_step": m["ms"] / args.steps,
+                                     "roofline": m["roofline"], "step_roofline": m["step_roofline"],
+                                     "gpu_launches": m["launches"], "clocks": m["clocks"]}
+                del Q
+    ttt = None
+    if world == 1 and args.time_to_tol:
+        ttt = time_to_tol(args.time_to_tol, local, dev)
+
+    cpu = finish_oracle_sample(cpu_proc) if cpu_proc else None
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "iterations/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        blk_bytes = main["abytes"] + 10 * main["panel"]
+        line = {"metric": METRIC, "value": main["value"], "unit": "iterations/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms"] / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
-                "config": {"workload": P.name, "n": n, "p": p, "nnz": P.A.nnz, "iters_per_step": iters,
-                           "tol": P.tol, "deflation_tol": P.tau, "pool_size": 1,
+                "config": {"workload": name, "n": n, "p": p, "nnz": nnz, "iters_per_step": iters,
+                           "tol": tol, "deflation_tol": tau, "pool_size": 1,
                            "l2": "inputs larger than L2 (working set per block step "
                                  f"{blk_bytes / 1e6:.0f} MB > 126 MB L2); no flush",
                            "parallelism": (f"row-partitioned x{world} (halo + allreduce over "
-                                           f"{'NCCL' if comm == 'nccl' else 'host callbacks, testing'})")
+                                           f"{'NCCL' if os.environ.get('BENCH_COMM', 'nccl') == 'nccl' else 'host callbacks, testing'})")
                            if world > 1 else "single GPU",
-                           "launch_mode": "plain launches" if (args.no_graphs or (world > 1 and comm != "nccl"))
-                           else "CUDA graphs (main/side branches)"},
-                "gpu_launches": launches, "slow_blocks": slow,
-                "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "hbm_peak_GBps": peak}
+                           "launch_mode": "plain launches" if (args.no_graphs or (world > 1 and os.environ.get(
+                               "BENCH_COMM", "nccl") != "nccl")) else "CUDA graphs (main/side branches)"},
+                "gpu_launches": main["launches"], "slow_blocks": main["slow_blocks"],
+                "roofline": main["roofline"], "step_roofline": main["step_roofline"], "cpu_baseline": cpu,
+                "e2e": main["e2e"], "clocks": main["clocks"], "hbm_peak_GBps": main["peak"],
+                "secondary": secondary or None, "time_to_tol": ttt}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
@@ -357,15 +480,24 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="2")
-    ap.add_argument("--iters", type=int, default=2000, help="banded iterations per step (maxit of one solve)")
+    ap.add_argument("--config", default="4")
+    ap.add_argument("--iters", type=int, default=0, help="banded iterations per step (0: 1024 for configs 4/5, "
+                                                          "2000 otherwise)")
+    ap.add_argument("--secondary", default="2", help="comma-separated configs measured after the main one (N = 1)")
+    ap.add_argument("--time-to-tol", default="2", help="config solved to tol at N = 1 ('' to skip)")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of CUDA graphs")
     ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel event region")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=0, help="oracle iterations of cpu_baseline (0: ~15 s sample)")
-    ap.add_argument("--ref-iters", type=int, default=40)
+    ap.add_argument("--cpu-iters", type=int, default=0, help="oracle iterations of cpu_baseline (0: ~20 s sample)")
+    ap.add_argument("--ref-iters", type=int, default=0, help="oracle iterations of --impl reference (0: W + K)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one rank per GPU: re-execute under torch.distributed.run (the driver's launch, made here)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

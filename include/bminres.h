@@ -18,7 +18,9 @@
  *    memory; the library detects which (cudaPointerGetAttributes) and, for host
  *    memory, stages the data through device buffers it owns, copying results
  *    back before returning.  The caller owns A, B, X; the library never frees
- *    them and keeps no pointer to them after a call returns.
+ *    them and keeps no pointer to them after a call returns (with
+ *    opt.plan_reuse = 1 it compares the col_idx pointer of the next call with
+ *    the previous one, never dereferencing it outside a call).
  *  - Calls are synchronous with respect to the host: they return after the work
  *    on the handle's stream is complete.  A handle is not re-entrant; distinct
  *    handles may be used from distinct threads.
@@ -80,7 +82,16 @@ typedef struct {
     int32_t split_spmm;      /* p in {8,16,32}: 0 auto (split when the n x p panel is >= 128 MB), 1 always,
                                 2 never.  Split: the SpMM A V_k runs alone at full occupancy (K1a) and K1
                                 streams its result; same arithmetic, bitwise */
-    int32_t reserved[6];
+    int32_t policy;          /* dependence policy: 0 = replace the dependent vector by a random one
+                                (the paper's choice; default); 1 = shrink the block size
+                                (BMINRES_EINVAL where not built) */
+    int32_t coeff_mode;      /* 0 = the paper's symmetric reuse h_{i,j} = h_{j,i} (default);
+                                other values: BMINRES_EINVAL (not built) */
+    int32_t plan_reuse;      /* world > 1: 0 = rebuild the halo plan on every solve (default; the library keeps
+                                nothing of the caller's CSR between calls); 1 = the caller promises that a
+                                solve with the same col_idx pointer, nnz, row_begin, n_loc and n passes the
+                                same column indices, and the plan of the previous solve is reused */
+    int32_t reserved[3];
 } bminres_options;
 
 /* One dependence event: candidate h_{j+p,j} <= gamma * ||A u_j||. */
@@ -128,8 +139,9 @@ int bminres_create(const bminres_options *opt, bminres_handle *out);
  * of DESIGN.md).  B: n_loc x p row-major (read only).  X: n_loc x p row-major
  * (output; input X_0 when opt.use_x0).  p in {1..8, 16, 32}; tol >= 0 finite;
  * maxit >= 0; deflation_tol >= 0 (the paper's gamma; reading C14:
- * relative to ||A u_j||).  Workspace (6 panels + pool) is allocated on the
- * first call for a given (n_loc, p) and reused.
+ * relative to ||A u_j||).  Workspace (5 panels, + 1 in split mode, + pool;
+ * bminres_workspace_bytes) is allocated on the first call for a given
+ * (n_loc, p) and reused.
  * Returns BMINRES_OK, BMINRES_MAXIT or an error code. */
 int bminres_solve(bminres_handle h, const bminres_csr *A, const double *B, double *X, int32_t p,
                   double tol, int64_t maxit, double deflation_tol);
@@ -158,7 +170,12 @@ int bminres_spmm(bminres_handle h, const bminres_csr *A, const double *X, double
 int bminres_random_vector(bminres_handle h, uint64_t seed, uint64_t stream, uint64_t event,
                           int64_t row_begin, int64_t n_loc, double *out, int64_t stride);
 
-/* Bytes of device workspace bminres_solve allocates for (n_loc, p, pool_size). */
+/* Upper bound on the device workspace bminres_solve allocates for (n_loc, p, pool_size) on one
+ * rank: 5 panels (V_{k-1}, V_k, V_{k+1}, M_{k-1}, M_k), the split-mode A V_k panel when the
+ * n_loc x p panel is >= 128 MB (p in {8,16,32}), the pool, 2 column-path scratch panels
+ * (allocated on the first breakdown only), partial-sum buffers, the history (<= 8 Mi doubles)
+ * and the state.  A row partition adds its halo rows to the three V panels; host-pointer
+ * calls add the staged copies of A, B and X. */
 size_t bminres_workspace_bytes(int64_t n_loc, int32_t p, int32_t pool_size);
 
 /* ---- Row-partitioned solves (world > 1) ----

@@ -48,7 +48,7 @@ class Config(C.Structure):
 class Result(C.Structure):
     _fields_ = [("status", C.c_int32), ("pad", C.c_int32), ("iterations", C.c_int64),
                 ("n_events", C.c_int64), ("true_res", C.c_double * MAX_P),
-                ("comp_res", C.c_double * MAX_P)]
+                ("comp_res", C.c_double * MAX_P), ("start_s", C.c_double), ("loop_s", C.c_double)]
 
 
 def build(force: bool = False) -> str:
@@ -99,6 +99,8 @@ class OracleResult:
     true_res: np.ndarray
     comp_res: np.ndarray
     dbg: dict = field(default_factory=dict)
+    start_s: float = 0.0           # wall time of the start block + pool (instrumentation)
+    loop_s: float = 0.0            # wall time of the iteration loop (instrumentation)
 
     @property
     def status_name(self) -> str:
@@ -140,7 +142,8 @@ def solve(A, B, *, tol=1e-8, maxit=100, tau=1e-8, seed=0, pool_size=1, X0=None,
         dbg = dict(U=dbg["U"].T.copy(), H=dbg["H"].T.copy(), R=dbg["R"].T.copy(), M=dbg["M"].T.copy(),
                    Z=dbg["Z"], S=dbg["S"])
     return OracleResult(int(res.status), it, hist[: it + 1].copy() if hist is not None else None, events, X,
-                        np.array(res.true_res[:p]), np.array(res.comp_res[:p]), dbg)
+                        np.array(res.true_res[:p]), np.array(res.comp_res[:p]), dbg, float(res.start_s),
+                        float(res.loop_s))
 
 
 def csr_block(A, X: np.ndarray) -> np.ndarray:

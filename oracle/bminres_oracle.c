@@ -36,11 +36,13 @@
  * invariants.  The replacement vectors' VALUES follow reading C17 (the paper
  * uses Matlab's mt19937ar): "parity unpinned" for those values.
  */
+#define _POSIX_C_SOURCE 199309L   /* clock_gettime (timing instrumentation) */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <float.h>
+#include <time.h>
 
 #define ORC_OK 0
 #define ORC_MAXIT 1
@@ -89,7 +91,15 @@ typedef struct {
     int64_t n_events;
     double true_res[ORC_MAX_P];   /* ||b_i - A x_i|| / ||b_i|| at exit */
     double comp_res[ORC_MAX_P];   /* ||T(:,i)|| / ||b_i|| at exit */
+    double start_s;               /* wall seconds: start block + pool (instrumentation only) */
+    double loop_s;                /* wall seconds: the iteration loop (instrumentation only) */
 } orc_result;
+
+static double wall_s(void) {   /* timing instrumentation; no part of the method */
+    struct timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return (double)t.tv_sec + 1e-9 * (double)t.tv_nsec;
+}
 
 /* ---------------- plain vector helpers (n-length loops) ---------------- */
 
@@ -245,6 +255,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
     int64_t nev = 0;
     int status = ORC_MAXIT;
     int64_t j = 0;
+    const double t_start = wall_s();
 
     /* ---- start: F0 = B - A X0 (X0 = 0 unless use_x0; Alg. 2, C6) ---- */
     for (int c = 0; c < p; ++c) {
@@ -317,6 +328,8 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
 
     int pool_exhausted = 0;
     int64_t iters = 0;                 /* completed iterations */
+    const double t_loop = wall_s();
+    res->start_s = t_loop - t_start;
     for (j = 1; status == ORC_MAXIT && j <= cfg->maxit; ++j) {
         const int m = (int)((j - 1) % p);          /* 0-based column within the block (C2) */
         /* block operator application every p iterations (Alg. 2, C2) */
@@ -463,6 +476,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
         if (mx < cfg->tol) { status = ORC_OK; break; }
         if (pool_exhausted) { status = ORC_EPOOL; break; }   /* C18 */
     }
+    res->loop_s = wall_s() - t_loop;
     res->iterations = iters;
     res->status = status;
     res->n_events = nev;

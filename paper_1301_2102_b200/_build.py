@@ -9,7 +9,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbminres.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("bminres.cu",)]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "step_kernels.cuh", "aux_kernels.cuh", "dmma_kernels.cuh")] + [
+# every header of csrc/ (a change to any of them rebuilds)
+DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + [
     os.path.join(ROOT, "include", "bminres.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

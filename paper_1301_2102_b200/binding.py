@@ -31,7 +31,8 @@ class Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("stream", C.c_void_p),
                 ("seed", C.c_uint64), ("pool_size", C.c_int32), ("use_x0", C.c_int32),
                 ("record_history", C.c_int32), ("use_graphs", C.c_int32), ("timing", C.c_int32),
-                ("split_spmm", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("split_spmm", C.c_int32), ("policy", C.c_int32), ("coeff_mode", C.c_int32),
+                ("plan_reuse", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class CsrStruct(C.Structure):
@@ -180,9 +181,33 @@ class HostCsrRows:
                    np.ascontiguousarray(A.data[k0:k1], dtype=np.float64), row_begin, int(A.n))
 
 
+def _dtype_name(x) -> str:
+    return str(x.dtype).replace("torch.", "")
+
+
+def _check_panel(x, what, shape=None):
+    """Row-major n x p fp64 panel (the layout every entry point takes)."""
+    if _dtype_name(x) != "float64":
+        raise BminresError(f"{what} must be float64, got {_dtype_name(x)}")
+    if len(x.shape) != 2:
+        raise BminresError(f"{what} must be 2-D (n x p), got shape {tuple(x.shape)}")
+    if shape is not None and tuple(int(d) for d in x.shape) != tuple(int(d) for d in shape):
+        raise BminresError(f"{what} has shape {tuple(x.shape)}, expected {tuple(shape)}")
+
+
+def _check_csr(A):
+    for nm, arr, want in (("row_ptr", A.row_ptr, "int32"), ("col_idx", A.col_idx, "int32"),
+                          ("values", A.values, "float64")):
+        if _dtype_name(arr) != want:
+            raise BminresError(f"DeviceCsr.{nm} must be {want}, got {_dtype_name(arr)}")
+    if int(A.row_ptr.numel()) != A.n + 1 or int(A.col_idx.numel()) != int(A.values.numel()):
+        raise BminresError("DeviceCsr: row_ptr must hold n+1 offsets and col_idx / values nnz entries")
+
+
 def _csr_struct(A) -> CsrStruct:
     s = CsrStruct()
     if isinstance(A, DeviceCsr):
+        _check_csr(A)
         s.n, s.nnz = (A.n_global if A.n_global is not None else A.n), A.nnz
         s.row_ptr, s.col_idx, s.values = _ptr(A.row_ptr), _ptr(A.col_idx), _ptr(A.values)
         s.row_begin, s.n_loc = A.row_begin, A.n
@@ -320,12 +345,14 @@ class Solver:
 
     def __init__(self, device: int = 0, *, pool_size: int = 1, seed: int = 0, use_graphs: bool = True,
                  timing: bool = False, record_history: bool = True, use_x0: bool = False, stream=None,
-                 rank: int = 0, world: int = 1, comm=None, split_spmm: int = 0):
+                 rank: int = 0, world: int = 1, comm=None, split_spmm: int = 0, policy: int = 0,
+                 plan_reuse: bool = False):
         L = lib()
         o = Options()
         L.bminres_default_options(C.byref(o))
         o.device, o.pool_size, o.seed = device, pool_size, seed
         o.split_spmm = split_spmm
+        o.policy, o.plan_reuse = policy, int(plan_reuse)
         o.use_graphs, o.timing, o.record_history, o.use_x0 = int(use_graphs), int(timing), int(record_history), int(use_x0)
         o.stream = stream
         o.rank, o.world = rank, world
@@ -383,7 +410,11 @@ class Solver:
                 X = torch.zeros_like(B)
             else:
                 X = np.zeros_like(B)
+        _check_panel(B, "B")
+        _check_panel(X, "X", B.shape)
         s = _csr_struct(A)
+        if int(B.shape[0]) != s.n_loc:
+            raise BminresError(f"B has {int(B.shape[0])} rows, A holds {s.n_loc}")
         rc = L.bminres_solve(self._h, C.byref(s), _ptr(B), _ptr(X), p, float(tol), int(maxit), float(deflation_tol))
         if rc < 0 and raise_on_error:
             raise BminresError(f"bminres_solve: {STATUS.get(rc, rc)}: {self.last_error()}")
@@ -417,6 +448,8 @@ class Solver:
         import torch
         if Y is None:
             Y = torch.empty_like(X)
+        _check_panel(X, "X")
+        _check_panel(Y, "Y", (A.n, X.shape[1]))
         s = _csr_struct(A)
         rc = lib().bminres_spmm(self._h, C.byref(s), _ptr(X), _ptr(Y), int(X.shape[1]))
         if rc != 0:

@@ -176,7 +176,7 @@ struct bminres_ctx {
     HostFlags* hf = nullptr;      // host pointer (mapped)
     HostFlags* hf_dev = nullptr;  // device alias
     double* hist = nullptr;
-    long long hist_cap = 0;
+    size_t hist_elems = 0;   // capacity of hist in doubles (rows x p of any earlier solve)
     // staged inputs (host-pointer calls)
     int* a_rowptr = nullptr;
     int* a_col = nullptr;
@@ -1052,10 +1052,12 @@ bool host_chol(const std::vector<double>& G, int p, double keep, std::vector<dou
 // above the deflation threshold tau^2 (C13); otherwise the caller runs the column-by-column MGS2
 // path, which decides step-0 deflation exactly as the oracle does.  In exact arithmetic S and U
 // are those of the Gram-Schmidt QR (R with positive diagonal is unique).
-bool fast_start(bminres_ctx* h, double* F, long long n, int p, std::vector<double>& S) {
+bool fast_start(bminres_ctx* h, double* F, long long n, int p, double tau, std::vector<double>& S) {
     if (getenv("BMINRES_NO_FAST_START")) return false;
     std::vector<double> R1, R2;
-    if (!host_chol(panel_gram(h, F, n, p), p, 1e-4, R1)) return false;
+    // pivot m = ||f_m - proj||^2, G_mm = ||f_m||^2 = ||F0(:,m)||^2: a pivot <= tau^2 G_mm is exactly the
+    // oracle's step-0 test ||f_m|| <= tau ||F0(:,m)|| (C13), so such a block takes the column path
+    if (!host_chol(panel_gram(h, F, n, p), p, std::max(1e-4, tau * tau), R1)) return false;
     auto upload_inverse = [&](const std::vector<double>& R) {   // R^{-1} (upper), ld MAXP
         std::vector<double> Ri((size_t)MAXP * MAXP, 0.0);
         for (int l = 0; l < p; ++l)
@@ -1105,7 +1107,8 @@ void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, i
     const void* key[5] = {A->col_idx, (const void*)(intptr_t)A->nnz, (const void*)(intptr_t)A->row_begin,
                           (const void*)(intptr_t)A->n_loc, (const void*)(intptr_t)A->n};
     std::string err;
-    if (!(h->d_lcol && std::equal(key, key + 5, h->plan_key))) {
+    // the plan is rebuilt on every solve unless the caller opted into reuse (header: plan_reuse)
+    if (!(h->opt.plan_reuse && h->d_lcol && std::equal(key, key + 5, h->plan_key))) {
         // offsets of every rank: all-to-all of (row_begin, n_loc)
         std::vector<long long> snd(2 * world), rcv(2 * world), one(world, 2);
         for (int q = 0; q < world; ++q) {
@@ -1308,9 +1311,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
 
     // ---- history buffer
     long long hist_cap = o.record_history ? std::min<long long>(maxit + 1, std::max<long long>(1, (8ll << 20) / p)) : 0;
-    if (hist_cap > h->hist_cap) {
+    if ((size_t)hist_cap * p > h->hist_elems) {   // (capacity in doubles: p may change between solves)
         dalloc(h, &h->hist, (size_t)hist_cap * p);
-        h->hist_cap = hist_cap;
+        h->hist_elems = (size_t)hist_cap * p;
     }
 
     // ---- state init
@@ -1402,7 +1405,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // column can deflate
         long long nrep0 = 0;
         seg.mark("stage+norms");
-        const bool fast = fast_start(h, F, n, p, S);
+        const bool fast = fast_start(h, F, n, p, tau, S);
         seg.mark(fast ? "fast_start" : "fast_fail");
         // Column path: per column one pass per CGS step over the panel (k_colstep: 1 -- normalise
         // the previous column, dots; 2 -- subtract, dots; 3 -- subtract, norm) and one host read
@@ -1729,6 +1732,14 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
         g_create_err = "split_spmm must be 0 (auto), 1 (always) or 2 (never)";
         return BMINRES_EINVAL;
     }
+    if (o.policy != 0) {
+        g_create_err = "policy: only 0 (replacement, P:690-729) is built";
+        return BMINRES_EINVAL;
+    }
+    if (o.coeff_mode != 0) {
+        g_create_err = "coeff_mode: only 0 (symmetric reuse, P:270-272) is built";
+        return BMINRES_EINVAL;
+    }
     auto* h = new bminres_ctx();
     h->opt = o;
     h->device = o.device;
@@ -1846,8 +1857,20 @@ int bminres_random_vector(bminres_handle h, uint64_t seed, uint64_t stream, uint
 }
 
 size_t bminres_workspace_bytes(int64_t n_loc, int32_t p, int32_t pool_size) {
-    return sizeof(double) * ((size_t)n_loc * p * 5 + (size_t)n_loc * std::max(pool_size, 1)) +
-           sizeof(double) * (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8) + sizeof(DevState);
+    // the allocations of ensure_workspace / do_solve (single rank; a row partition adds n_halo rows
+    // to each V slot), as an upper bound: V[3], M[2] and the pool (each with 32 doubles of slack),
+    // the split-mode AV panel (same rule as ensure_workspace), the partial-sum buffers, the history
+    // at its cap (8 Mi doubles), the two column-path scratch panels (allocated on the first
+    // breakdown only), the small buffers and the state
+    const size_t panel = (size_t)n_loc * p + 32;
+    Kfn f;
+    const bool split = kfn_for(p, &f, pool_size) && f.k1pre != nullptr && (double)n_loc * p * 8.0 >= 128e6;
+    const size_t part = (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP + MAXREF + 8) +
+                        (size_t)NB_MAX * (MAXP * MAXP + MAXP) + 2 * (size_t)NB_MAX * (MAXP * MAXP + MAXQ * MAXP);
+    const size_t hist = std::min<size_t>((size_t)8 << 20, (size_t)std::max(p, 1) * ((8ull << 20) / std::max(p, 1)));
+    size_t d = 5 * panel + (split ? panel : 0) + (size_t)n_loc * std::max(pool_size, 1) + 32 + part + hist +
+               2 * panel + (MAXREF + 64) + 2 * MAXP * MAXP + (MAXP * MAXP + 3 * MAXP);
+    return sizeof(double) * d + 16 * sizeof(unsigned) + sizeof(DevState);
 }
 
 int bminres_get_unique_id(uint8_t out[128]) {

@@ -93,6 +93,9 @@ def problem(name):
     if name == "lap3d12p8":
         A = synth.laplacian_3d(12, shift=2.5)
         return synth.Problem("lap3d12p8", A, synth.gaussian_rhs(A.n, 8, seed=1), 1e-10, 4000)
+    if name == "dep2d":   # config 3's recipe (B = [G, G C + eps N], eps = 0) on a small grid: step-0 events
+        A = synth.laplacian_2d(20, shift=2.5)
+        return synth.Problem("dep2d", A, synth.dependent_rhs(A.n, 4, 0.0, seed=0), 1e-10, 4000)
     raise ValueError(name)
 
 
@@ -108,7 +111,8 @@ def solve_worker(rank, world, port, outdir, name, maxit):
     with Solver(0, rank=rank, world=world, comm=TorchComm()) as s:
         r = s.solve(A, B, tol=P.tol, maxit=maxit, deflation_tol=P.tau)
         X = r.X.cpu().numpy()
+    ev = np.array([[e["j"], e["col"], e["kind"], e["action"]] for e in r.events], dtype=np.int64).reshape(-1, 4)
     np.savez(os.path.join(outdir, f"solve{rank}.npz"), X=X, hist=r.history, it=r.iterations, status=r.status,
-             true_res=np.array(r.stats["true_res"]))
+             true_res=np.array(r.stats["true_res"]), events=ev)
     dist.barrier()
     dist.destroy_process_group()

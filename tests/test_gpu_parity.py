@@ -497,3 +497,117 @@ def test_full_size_config_closed_form_and_invariants(cfg):
     h = r.history
     assert np.all(h[1:] <= h[:-1] * (1 + 1e-12) + 1e-15), "residual histories must not increase (P3)"
     np.testing.assert_allclose(r.stats["comp_res"], r.stats["true_res"], rtol=0, atol=1e-8)
+
+
+# ----------------------------------------------------------------------------- round-2 parity gaps
+
+
+def _golden(name):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)
+    with open(path) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_config_first_50_vs_oracle(cfg):
+    """Configs 4 (3-D 256^3, p = 32) and 5 (unstructured n = 4.19M, p = 16) at full size and in the
+    bench's launch configuration (graphs, split mode): the first 50 iterations' residual histories
+    to 1e-9 and the events against the oracle's (tests/golden/*_first50.json, written by
+    scripts/make_golden.py from oracle.solve only)."""
+    P = synth.config(cfg)
+    g = _golden(f"{P.name}_first50.json")
+    assert g["n"] == P.n and g["p"] == P.p and g["nnz"] == P.A.nnz
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=50, deflation_tol=P.tau)
+    assert r.iterations == g["iterations"] == 50 and r.status == g["status"]
+    assert_hist_close(r.history, np.array(g["history"]))
+    same_events(r.events, g["events"])
+    np.testing.assert_allclose(r.stats["true_res"], g["true_res"], rtol=1e-8)
+
+
+def test_singular_r_closed_form():
+    """ESINGULAR_R (reading C23): b_1 = the null vector 1 of a 16 x 16 grid graph Laplacian, so
+    A u_1 = 0 exactly, the j = 1 candidate is an exact dependence and R_1 is singular: GPU and oracle
+    both stop with ESINGULAR_R at j = 1 with X = 0 and the same event."""
+    from tests.test_oracle_pins import grid_graph_laplacian
+    A = grid_graph_laplacian(16)
+    rng = np.random.default_rng(1)
+    B = np.concatenate([np.ones((A.n, 1)), rng.standard_normal((A.n, 2))], axis=1)
+    ref = oracle.solve(A, B, tol=1e-8, maxit=50, pool_size=1)
+    assert ref.status_name == "ESINGULAR_R"
+    r = gpu_solve(A, B, tol=1e-8, maxit=50)
+    assert r.status_name == "ESINGULAR_R", r.status_name
+    assert r.iterations == ref.iterations
+    same_events(r.events, ref.events)
+    np.testing.assert_array_equal(r.X, 0.0)
+
+
+@pytest.mark.parametrize("use_graphs", [True, False])
+def test_replacement_runs_vs_oracle(use_graphs):
+    """Runs WITH replacements (the oracle side is pinned by test_lsq_after_* in
+    test_oracle_pins.py): Fig. 3's B = [e_1, A e_1] and config 3's recipe at eps = 0 on a small
+    grid -- events, 50-iteration histories and X against the oracle."""
+    A = synth.laplacian_2d(12, shift=2.0)
+    e1 = np.zeros(A.n)
+    e1[0] = 1.0
+    D = synth.csr_to_dense(A)
+    cases = [(A, np.stack([e1, D @ e1], axis=1)),
+             (synth.laplacian_2d(14, shift=2.5), synth.dependent_rhs(14 * 14, 3, 0.0, seed=0))]
+    for Ai, Bi in cases:
+        ref = oracle.solve(Ai, Bi, tol=0.0, maxit=60, pool_size=1)
+        r = gpu_solve(Ai, Bi, tol=0.0, maxit=60, use_graphs=use_graphs)
+        same_events(r.events, ref.events)
+        assert r.iterations == ref.iterations
+        assert_hist_close(r.history, ref.history)
+        np.testing.assert_allclose(r.X, ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+
+
+def test_handle_reuse_across_block_sizes():
+    """One handle reused for p = 4, then p = 8 and p = 32 at the same maxit (the history buffer is
+    sized in doubles, not rows): each solve equals a fresh handle's and the oracle's history."""
+    torch = _torch()
+    from paper_1301_2102_b200 import DeviceCsr, Solver
+    A = synth.laplacian_3d(12, shift=2.5)
+    dA = DeviceCsr.from_host(A, "cuda:0")
+    with Solver(0) as s:
+        for p in (4, 8, 32, 4):
+            B = synth.gaussian_rhs(A.n, p, seed=p)
+            r = s.solve(dA, torch.from_numpy(B).to("cuda:0"), tol=0.0, maxit=64)
+            ref = oracle.solve(A, B, tol=0.0, maxit=64)
+            assert r.iterations == 64
+            assert_hist_close(r.history, ref.history)
+            np.testing.assert_allclose(r.X.cpu().numpy(), ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+
+
+def test_binding_rejects_wrong_dtypes_and_shapes(solver):
+    """The binding validates what the C ABI cannot: dtypes, 2-D shapes and matching row counts."""
+    torch = _torch()
+    from paper_1301_2102_b200 import BminresError, DeviceCsr
+    A = synth.laplacian_2d(8, shift=1.0)
+    dA = DeviceCsr.from_host(A, "cuda:0")
+    B = torch.zeros((A.n, 2), dtype=torch.float64, device="cuda:0")
+    with pytest.raises(BminresError):
+        solver.solve(dA, B.float())
+    with pytest.raises(BminresError):
+        solver.solve(dA, B[:-1])
+    with pytest.raises(BminresError):
+        solver.solve(dA, B, torch.zeros((A.n, 3), dtype=torch.float64, device="cuda:0"))
+    bad = DeviceCsr(dA.n, dA.row_ptr.long(), dA.col_idx, dA.values)
+    with pytest.raises(BminresError):
+        solver.solve(bad, B)
+
+
+def test_start_block_large_deflation_tol():
+    """A start column whose projection residual ratio (~0.03) lies between the CholQR2 fast path's
+    own 1e-2 guard and a large deflation_tol (0.05) is a step-0 event (C13) on the GPU exactly as in
+    the oracle (the fast path tests tau^2 against the Cholesky pivots)."""
+    A = synth.laplacian_2d(20, shift=2.5)
+    rng = np.random.default_rng(4)
+    g = rng.standard_normal((A.n, 2))
+    B = np.concatenate([g, g[:, :1] + 0.03 * rng.standard_normal((A.n, 1)), rng.standard_normal((A.n, 1))], axis=1)
+    ref = oracle.solve(A, B, tol=0.0, maxit=40, tau=0.05, pool_size=1)
+    assert [(e["j"], e["col"]) for e in ref.events][:1] == [(0, 3)]
+    r = gpu_solve(A, B, tol=0.0, maxit=40, deflation_tol=0.05)
+    same_events(r.events, ref.events)
+    assert_hist_close(r.history, ref.history, rtol=1e-8)

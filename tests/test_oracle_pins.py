@@ -482,3 +482,83 @@ def test_config1_singular_floor():
     assert r.status_name == "MAXIT"
     assert np.all(r.history >= floor * (1 - 1e-6))
     np.testing.assert_allclose(r.history[1100], floor, rtol=1e-4)
+
+
+# ----------------------------------------------------------------------------- P1 / P4 after replacements
+
+
+def _lsq_over_own_basis(A, B, maxit, *, pool_size=1):
+    """P1 on runs WITH replacement events: the replaced basis still satisfies the Lanczos relation
+    (h_{j+p,j} := 0, exact dependence), so x_j must still minimise ||b_i - A x|| over
+    R(U_j) -- here U_j is the oracle's own basis (dbg_U), the minimiser found by dense least squares."""
+    D = dense(A)
+    r = oracle.solve(A, B, tol=0.0, maxit=maxit, pool_size=pool_size, debug_iters=maxit)
+    U = r.dbg["U"]
+    beta = np.linalg.norm(B, axis=0)
+    for j in range(1, maxit + 1):
+        rj = oracle.solve(A, B, tol=0.0, maxit=j, pool_size=pool_size)
+        res, Xls = lsq_residuals(D, B, U, j)
+        big = res > 1e-12 * beta
+        np.testing.assert_allclose(rj.history[j][big] * beta[big], res[big], rtol=1e-8)
+        # P4: the computed residual is the true residual
+        assert np.all(np.abs(rj.comp_res - rj.true_res) <= 1e-9 * np.maximum(1.0, rj.true_res))
+        if j in (1, maxit // 2, maxit):
+            np.testing.assert_allclose(rj.X, Xls, rtol=1e-7, atol=1e-8 * max(1.0, np.abs(Xls).max()))
+    return r
+
+
+def test_lsq_after_replacement_fig3():
+    """Fig. 3's B = [e_1, A e_1]: column 1's candidate at j = 1 is exactly dependent
+    and replaced by a random vector; every later iterate is still the least-squares minimiser over
+    the (replaced) basis, and computed = true residual."""
+    A = synth.laplacian_2d(12, shift=2.0)
+    D = dense(A)
+    e1 = np.zeros(A.n)
+    e1[0] = 1.0
+    B = np.stack([e1, D @ e1], axis=1)
+    r = _lsq_over_own_basis(A, B, 30)
+    assert [(e["j"], e["col"], e["action"]) for e in r.events] == [(1, 1, 1)]
+
+
+def test_lsq_after_step0_replacement_config3_recipe():
+    """Config 3's recipe B = [G, G C + eps N] at eps = 0 on a small grid: the last p/2 start columns
+    deflate at step 0 (eqn.init-QR, reading C13) and are replaced; the iterates remain the
+    least-squares minimisers over the oracle's basis at every j."""
+    A = synth.laplacian_2d(14, shift=2.5)
+    B = synth.dependent_rhs(A.n, 3, 0.0, seed=0)
+    r = _lsq_over_own_basis(A, B, 36)
+    assert [(e["j"], e["col"]) for e in r.events] == [(0, 4), (0, 5), (0, 6)]
+
+
+# ----------------------------------------------------------------------------- ESINGULAR_R closed form
+
+
+def grid_graph_laplacian(m):
+    """Neumann graph Laplacian of an m x m grid: integer entries, A 1 = 0 exactly in fp64."""
+    n = m * m
+    D = np.zeros((n, n))
+    for y in range(m):
+        for x in range(m):
+            i = y * m + x
+            for dx, dy in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+                if 0 <= x + dx < m and 0 <= y + dy < m:
+                    D[i, (y + dy) * m + x + dx] = -1.0
+                    D[i, i] += 1.0
+    return synth.dense_to_csr(D)
+
+
+def test_singular_r_closed_form():
+    """r_11 = 0 exactly: b_1 = the null vector 1 of a graph Laplacian (m = 16, so u_1 = 1/16 and
+    A u_1 = 0 in exact fp64).  The candidate of j = 1 is w = 0 (omega = 0: an exact dependence,
+    replaced), the Hessenberg column h_1 is zero, so R_1 is singular and the solve stops with
+    ESINGULAR_R at j = 1 (reading C23; x cannot be updated)."""
+    A = grid_graph_laplacian(16)
+    D = dense(A)
+    assert np.all(D @ np.full(A.n, 1 / 16) == 0.0)
+    rng = np.random.default_rng(1)
+    B = np.concatenate([np.ones((A.n, 1)), rng.standard_normal((A.n, 2))], axis=1)
+    r = oracle.solve(A, B, tol=1e-8, maxit=50, pool_size=1)
+    assert r.status_name == "ESINGULAR_R"
+    assert r.events and r.events[0]["j"] == 1 and r.events[0]["col"] == 1 and r.events[0]["kind"] == 0
+    assert r.iterations == 0
+    np.testing.assert_array_equal(r.X, 0.0)

@@ -117,6 +117,33 @@ def test_two_rank_solve_matches_single_rank(tmp_path, name, maxit):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name,maxit", [("1c", 120), ("lap3d12p8", 160), ("dep2d", 200)])
+def test_two_rank_solve_matches_oracle(tmp_path, name, maxit):
+    """Row a6 against the ORACLE (not the single-rank GPU solve): the 2-rank partitioned solve
+    (halo exchange + allreduces, replicated small QR) gives the oracle's residual history to 1e-9
+    over the first 50 iterations, its iteration count and status, its dependence events (dep2d:
+    step-0 replacements of columns 5-8) and its X."""
+    import oracle
+    from tests._dist_workers import problem, solve_worker
+    _spawn(solve_worker, 2, str(tmp_path), name, maxit)
+    parts = [np.load(tmp_path / f"solve{r}.npz") for r in range(2)]
+    P = problem(name)
+    ref = oracle.solve(P.A, P.B, tol=P.tol, maxit=maxit, tau=P.tau, pool_size=1)
+    ref_ev = [[e["j"], e["col"], e["kind"], e["action"]] for e in ref.events]
+    if name == "dep2d":
+        assert [e[:2] for e in ref_ev] == [[0, 5], [0, 6], [0, 7], [0, 8]]
+    for d in parts:
+        assert int(d["it"]) == ref.iterations and int(d["status"]) == ref.status
+        k = min(51, len(ref.history))
+        h, hr = d["hist"][:k], ref.history[:k]
+        assert np.all(np.abs(h - hr) <= 1e-9 * np.abs(hr) + 1e-14), np.max(np.abs(h - hr) / np.abs(hr))
+        assert d["events"].tolist() == ref_ev
+        np.testing.assert_allclose(d["true_res"], ref.true_res, rtol=1e-6, atol=1e-13)
+    X = np.vstack([parts[0]["X"], parts[1]["X"]])
+    np.testing.assert_allclose(X, ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("p", [4, 8])
 def test_nccl_transport_world1_bitwise(p):
     """The partition path with the NCCL transport (allreduce / exchange captured in the graphs) at
