@@ -52,7 +52,10 @@ METRIC = "block-MINRES iterations/s and achieved HBM GB/s (fp64) vs roofline, 1/
 PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 8, "orth": 3, "update": 6,
                       # split mode (large panels): K1a reads V_k once (gathers) and writes AV; K1 then
                       # streams AV, V_k, V_{k-1} and writes W (+ the fused update)
-                      "spmm_av": 2, "epilogue": 4, "epilogue_fused": 9}
+                      "spmm_av": 2, "epilogue": 4, "epilogue_fused": 9,
+                      # split mode, p >= 16: the update as its own kernel (V_{k-2}, M_{k-4}, M_{k-3} read,
+                      # M_{k-2} written, X read + written every other block: 5 on average)
+                      "update_main": 5}
 PHASE_READS_A = {"spmm", "spmm_fused", "spmm_av"}
 DEFAULT_ITERS = {"1": 2000, "1c": 2000, "2": 2000, "3": 2000, "4": 1024, "5": 1024}
 
@@ -320,7 +323,7 @@ def measure(P, args, iters, world, rank, local, dev, *, e2e: bool, kernel_timing
             except Exception:
                 traffic = None
         step_ms = sum(phase_ms[k] for k in ("spmm", "spmm_fused", "orth", "smallqr", "update", "reduce", "spmm_av",
-                                            "epilogue", "epilogue_fused") if k in phase_ms)
+                                            "epilogue", "epilogue_fused", "update_main") if k in phase_ms)
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "bytes_per_launch": bytes_launch, "mean_launch_us": per_launch_ms * 1e3,
@@ -426,7 +429,7 @@ def run_ours(args):
     del P
 
     secondary = {}
-    if world == 1 and args.secondary:
+    if world == 1 and args.secondary and args.secondary != "none":
         for c in args.secondary.split(","):
             if c and c != cfg:
                 Q = problem(c)
@@ -437,7 +440,7 @@ def run_ours(args):
                                      "gpu_launches": m["launches"], "clocks": m["clocks"]}
                 del Q
     ttt = None
-    if world == 1 and args.time_to_tol:
+    if world == 1 and args.time_to_tol and args.time_to_tol != "none":
         ttt = time_to_tol(args.time_to_tol, local, dev)
 
     cpu = finish_oracle_sample(cpu_proc) if cpu_proc else None
@@ -483,8 +486,8 @@ def main():
     ap.add_argument("--config", default="4")
     ap.add_argument("--iters", type=int, default=0, help="banded iterations per step (0: 1024 for configs 4/5, "
                                                           "2000 otherwise)")
-    ap.add_argument("--secondary", default="2", help="comma-separated configs measured after the main one (N = 1)")
-    ap.add_argument("--time-to-tol", default="2", help="config solved to tol at N = 1 ('' to skip)")
+    ap.add_argument("--secondary", default="2", help="comma-separated configs measured after the main one (N = 1; 'none' to skip)")
+    ap.add_argument("--time-to-tol", default="2", help="config solved to tol at N = 1 ('none' to skip)")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of CUDA graphs")
     ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel event region")
     ap.add_argument("--no-e2e", action="store_true")

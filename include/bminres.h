@@ -104,10 +104,12 @@ typedef struct {
     double ratio;    /* h / omega */
 } bminres_event;
 
-#define BMINRES_NPHASE 13  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
+#define BMINRES_NPHASE 14  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
                               reduce (k_reduce), spmm_fused (K1 with the M/X update of block k-2),
                               split mode (large panels): spmm_av (K1a, A V_k alone), epilogue (K1 streaming
-                              A V_k), epilogue_fused (the same with the M/X update of block k-2) */
+                              A V_k), epilogue_fused (the same with the M/X update of block k-2),
+                              update_main (split mode, p >= 16: the M/X update of block k-2 as its own
+                              kernel before K1a(k)) */
 
 typedef struct {
     int32_t status;           /* return code of the last solve */

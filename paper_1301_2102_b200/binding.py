@@ -15,9 +15,9 @@ import numpy as np
 from . import _build
 
 MAX_P = 32
-NPHASE = 13
+NPHASE = 14
 PHASES = ["spmm", "orth", "smallqr", "update", "slowpath", "start", "resid", "other", "reduce", "spmm_fused",
-          "spmm_av", "epilogue", "epilogue_fused"]
+          "spmm_av", "epilogue", "epilogue_fused", "update_main"]
 STATUS = {0: "OK", 1: "MAXIT", -1: "EINVAL", -2: "ECUDA", -3: "ENCCL", -4: "ENOMEM", -5: "EPOOL",
           -6: "ESINGULAR_R"}
 SUPPORTED_P = (1, 2, 3, 4, 5, 6, 7, 8, 16, 32)

@@ -33,7 +33,7 @@ using namespace bmr;
 namespace {
 
 enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER, PH_REDUCE,
-             PH_SPMM_FUSED, PH_SPMM_AV, PH_EPI, PH_EPI_FUSED };
+             PH_SPMM_FUSED, PH_SPMM_AV, PH_EPI, PH_EPI_FUSED, PH_UPD_MAIN };
 
 struct Retained {
     double* v;
@@ -46,6 +46,8 @@ struct Kfn {  // per-p kernel table
     void (*k1a)(K1Args);     // split mode: the SpMM alone (null: no split kernels for this p)
     void (*k1pre)(K1Args);   // split mode: K1 streaming A V_k
     size_t smem1pre;
+    void (*k1u)(K1Args);     // split mode, p >= 16: the M/X update of block k-2 as its own kernel
+    size_t smem1u;
     // start block / exit residual: Gram, V R^{-1}, plain SpMM (DMMA / K1a versions for p = 8, 16, 32)
     void (*red2f)(DevState*, int, int);   // reduce2 + factorisation for the DMMA K1 (null: k_reduce)
     void (*gram)(const double*, long long, int, double*, int, double*, unsigned*);
@@ -66,6 +68,8 @@ Kfn make_kfn(int q) {
     f.k1a = nullptr;
     f.k1pre = nullptr;
     f.smem1pre = 0;
+    f.k1u = nullptr;
+    f.smem1u = 0;
     f.red2f = nullptr;
     f.gram = k_gram;
     f.mat = k_materialize;
@@ -92,6 +96,10 @@ Kfn make_kfn(int q) {
             if constexpr (P <= 8) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
             else if constexpr (P <= 16) f.red2f = k_red2f_t<P, DM<P>::FR, DM<P>::NC>;
             f.smem1pre = K1DSmem<P, true>::bytes;
+            if constexpr (P >= 16) {
+                f.k1u = k1u_update<P>;
+                f.smem1u = UpdB<P>::bytes;
+            }
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
             f.nt2 = K2DSmem<P>::WARPS * 32;
@@ -201,6 +209,7 @@ struct bminres_ctx {
     int nb1 = 0, nb2 = 0, nb4 = 0, tpw = 4, csz = 2;
     // split mode: K1a (SpMM alone, full occupancy) -> AV, then K1<P, true>
     bool split = false;
+    bool upd_sep = false;    // split mode: the M/X update of block k-2 runs as k1u_update before K1a(k)
     bool red2_fac = false;   // reduce2 factors the new block once (k_red2f)
     bool xdefer = false;   // fused updates defer X in pairs
     int nb1a = 0;
@@ -390,6 +399,8 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         const bool can = h->kf.k1pre != nullptr;
         const int mode = se ? (atoi(se) != 0 ? 1 : 2) : h->opt.split_spmm;
         h->split = can && (mode == 1 || (mode == 0 && (double)n * p * 8.0 >= 128e6));
+        // the update as its own kernel (k1u_update) in split mode where it is compiled
+        h->upd_sep = h->split && h->kf.k1u != nullptr && getenv("BMINRES_FUSED_UPD") == nullptr;
         if (h->split) {
             dalloc(h, &h->AV, panel);
         } else if (h->AV) {
@@ -683,6 +694,26 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
              par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X, nullptr, h->xdefer ? 1 : 0};
+    if (h->split && h->upd_sep && fuse) {
+        // the M/X update of block k-2 (row a5) on this stream before K1a(k): its V_{k-2} rows are
+        // overwritten by K1(k)'s W; K1a and K1 wait for it (PDL)
+        TimeMark tm(h, PH_UPD_MAIN);
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+        cfg.gridDim = dim3(h->n_sm);
+        cfg.blockDim = dim3(UPD_THREADS);
+        cfg.dynamicSmemBytes = h->kf.smem1u;
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k1u, a);
+        if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k1u_update: ") + cudaGetErrorString(e));
+        h->launches++;
+        a.fuse = 0;
+        fuse = 0;
+    }
     if (h->split) {
         // K1a: AV = A V_k (PDL after reduce2 / K2), then K1 streams AV
         K1Args aa = a;
@@ -1585,7 +1616,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // same graphs (their collectives match).
         for (long long s = b; s <= nblocks && graphs; s += GB) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
-            h->launches += GB * ((h->kf.fused ? 5 : 6) + (h->split ? 1 : 0));
+            h->launches += GB * ((h->kf.fused ? 5 : 6) + (h->split ? 1 : 0) + (h->upd_sep ? 1 : 0));
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -1772,6 +1803,9 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
             if (f.k1pre)
                 CK(cudaFuncSetAttribute((const void*)f.k1pre, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)f.smem1pre));
+            if (f.k1u)
+                CK(cudaFuncSetAttribute((const void*)f.k1u, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)f.smem1u));
             CK(cudaFuncSetAttribute((const void*)f.k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem2));
             CK(cudaFuncSetAttribute((const void*)f.k3b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
             CK(cudaFuncSetAttribute((const void*)f.k4b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4b));

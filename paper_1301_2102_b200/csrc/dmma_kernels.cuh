@@ -51,6 +51,18 @@ __device__ __forceinline__ void stage_tile(double* dst, const double* src, long 
     }
 }
 
+// cp.async one TRU x P tile (rows base.., zero-fill past n) into smem rows of stride P + 4
+template <int P, int TRU = 16>
+__device__ __forceinline__ void stage_rows(double* dst, const double* src, long long base, long long n, int lane) {
+    constexpr int RS = P + 4, CPR = P / 2;
+    for (int c = lane; c < TRU * CPR; c += 32) {
+        const int r = c / CPR, q = c % CPR;
+        const long long i = base + r;
+        const bool ok = i < n;
+        cp_async16(dst + r * RS + 2 * q, src + (ok ? i : 0) * P + 2 * q, ok);
+    }
+}
+
 // ------------------------------------------------------------------ M/X update on DMMA (row a5)
 //
 // M_k = V_k (Tr_k R_kk^{-1}) - M_{k-2} R_{k-2,k}R_kk^{-1} - M_{k-1} R_{k-1,k}R_kk^{-1}
@@ -253,11 +265,15 @@ __device__ __forceinline__ void frag_acc_t(double* sAcc, int ld, int m0, int n0,
 
 template <int P>
 struct K2DSmem {
-    static constexpr int WARPS = P >= 16 ? 8 : 4;   // large p: more warps to hide the DMMA chains
-    static constexpr int NS = P >= 32 ? 2 : NSTAGE;  // cp.async stages (shared-memory budget)
+    // rows per warp tile: 16 (two 8-row DMMA chunks share every B fragment; the k-chunks run
+    // outermost so every A fragment feeds NC DMMAs -- at p = 32 the 8-row version was bound by
+    // shared-memory bandwidth, two LDS.64 per DMMA)
+    static constexpr int TR = 16, MC = TR / 8, RS = DM<P>::RS, TILE = TR * RS;
+    static constexpr int WARPS = P >= 32 ? 4 : (P >= 16 ? 8 : 4);
+    static constexpr int NS = P >= 16 ? 2 : NSTAGE;   // cp.async stages (shared-memory budget)
     static constexpr int RSQ = 12;                        // pool tile row stride (8 columns + pad)
-    static constexpr int TQ = DM<P>::TR * RSQ;
-    static constexpr int STG = 2 * DM<P>::TILE + TQ;         // one stage of one warp
+    static constexpr int TQ = TR * RSQ;
+    static constexpr int STG = 2 * TILE + TQ;         // one stage of one warp
     // slot-major: stage s of warp w at pipe + (s * WARPS + w) * STG
     static constexpr int pipe = WARPS * NS * STG;
     static constexpr int LD = P + 1;
@@ -273,7 +289,8 @@ template <int P>
 __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
     using D = DM<P>;
     using S = K2DSmem<P>;
-    constexpr int WARPS = S::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR, RSQ = S::RSQ;
+    constexpr int WARPS = S::WARPS, TR = S::TR, MC = S::MC, RS = S::RS, KC = D::KC, NC = D::NC, FR = D::FR;
+    constexpr int RSQ = S::RSQ, TILE = S::TILE;
     DevState* st = a.st;
     if (!st->run_main) {
         k2_stopped(st);
@@ -298,14 +315,13 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
         if (t < ntiles) {
             double* sl = wb + slot * WARPS * S::STG;
             const long long base = t * TR;
-            stage_tile<P>(sl, a.W, base, a.n, lane);
-            stage_tile<P>(sl + D::TILE, a.V, base, a.n, lane);
+            stage_rows<P, TR>(sl, a.W, base, a.n, lane);
+            stage_rows<P, TR>(sl + TILE, a.V, base, a.n, lane);
             for (int c = lane; c < TR * MAXQ; c += 32) {
                 const int r = c / MAXQ, q = c % MAXQ;
                 const long long i = base + r;
                 const bool ok = i < a.n && q < Q;
-                if (q < Q || true)
-                    cp_async8(sl + 2 * D::TILE + r * RSQ + q, a.pool + (ok ? i * qc + qf + q : 0), ok);
+                cp_async8(sl + 2 * TILE + r * RSQ + q, a.pool + (ok ? i * qc + qf + q : 0), ok);
             }
         }
         cp_commit();
@@ -360,37 +376,59 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
         __syncwarp();
         double* sl = wb + (int)(it % S::NS) * WARPS * S::STG;
         double* tW = sl;
-        const double* tV = sl + D::TILE;
-        double* tR = sl + 2 * D::TILE;
+        const double* tV = sl + TILE;
+        double* tR = sl + 2 * TILE;
         const long long base = (t0 + it * ts) * TR;
+        // pool r_q -= U_k coef_{k-1}(:,q) = V_k F(:,q) and W' = W - U_k G_s = W - V_k (Tr_k G_s),
+        // k-chunks outermost (each output accumulates over kc in increasing order)
+        double c[MC][NC][2], cq[MC][2];
 #pragma unroll
-        for (int mc = 0; mc < TR / 8; ++mc) {
+        for (int mc = 0; mc < MC; ++mc) {
+            cq[mc][0] = tR[(mc * 8 + fr) * RSQ + 2 * fc];
+            cq[mc][1] = tR[(mc * 8 + fr) * RSQ + 2 * fc + 1];
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                c[mc][nc][0] = tW[(mc * 8 + fr) * RS + nc * 8 + 2 * fc];
+                c[mc][nc][1] = tW[(mc * 8 + fr) * RS + nc * 8 + 2 * fc + 1];
+            }
+        }
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+            double aV[MC];
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc) aV[mc] = tV[(mc * 8 + fr) * RS + kc * 4 + fc];
+            if (Q > 0) {
+                const double bq = fF[kc * 32 + lane];
+#pragma unroll
+                for (int mc = 0; mc < MC; ++mc) dmma(cq[mc][0], cq[mc][1], aV[mc], bq);
+            }
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const double be = fE[(kc * NC + nc) * 32 + lane];
+#pragma unroll
+                for (int mc = 0; mc < MC; ++mc) dmma(c[mc][nc][0], c[mc][nc][1], aV[mc], be);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int mc = 0; mc < MC; ++mc) {
             const int r0 = mc * 8;
             const long long row = base + r0 + fr;
             const bool rok = row < a.n;
             if (Q > 0) {
-                // pool r_q -= U_k coef_{k-1}(:,q) = V_k F(:,q)
-                double c0 = tR[(r0 + fr) * RSQ + 2 * fc], c1 = tR[(r0 + fr) * RSQ + 2 * fc + 1];
-#pragma unroll
-                for (int kc = 0; kc < KC; ++kc) dmma(c0, c1, tV[(r0 + fr) * RS + kc * 4 + fc], fF[kc * 32 + lane]);
-                tR[(r0 + fr) * RSQ + 2 * fc] = c0;
-                tR[(r0 + fr) * RSQ + 2 * fc + 1] = c1;
+                tR[(r0 + fr) * RSQ + 2 * fc] = cq[mc][0];
+                tR[(r0 + fr) * RSQ + 2 * fc + 1] = cq[mc][1];
                 if (rok) {
-                    if (2 * fc < Q) a.pool[row * qc + qf + 2 * fc] = c0;
-                    if (2 * fc + 1 < Q) a.pool[row * qc + qf + 2 * fc + 1] = c1;
+                    if (2 * fc < Q) a.pool[row * qc + qf + 2 * fc] = cq[mc][0];
+                    if (2 * fc + 1 < Q) a.pool[row * qc + qf + 2 * fc + 1] = cq[mc][1];
                 }
             }
-            // W' = W - U_k G_s = W - V_k (Tr_k G_s)
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 const int col = nc * 8 + 2 * fc;
-                double c0 = tW[(r0 + fr) * RS + col], c1 = tW[(r0 + fr) * RS + col + 1];
-#pragma unroll
-                for (int kc = 0; kc < KC; ++kc)
-                    dmma(c0, c1, tV[(r0 + fr) * RS + kc * 4 + fc], fE[(kc * NC + nc) * 32 + lane]);
-                tW[(r0 + fr) * RS + col] = c0;
-                tW[(r0 + fr) * RS + col + 1] = c1;
-                if (rok) *reinterpret_cast<double2*>(a.W + row * P + col) = make_double2(c0, c1);
+                tW[(r0 + fr) * RS + col] = c[mc][nc][0];
+                tW[(r0 + fr) * RS + col + 1] = c[mc][nc][1];
+                if (rok) *reinterpret_cast<double2*>(a.W + row * P + col) = make_double2(c[mc][nc][0], c[mc][nc][1]);
             }
         }
         __syncwarp();
@@ -576,6 +614,182 @@ __global__ void __launch_bounds__(256) k_materialize_dmma(const double* V, const
 }
 template <int P>
 constexpr size_t mat_dmma_smem() { return sizeof(double) * (DM<P>::FR + 8 * 2 * DM<P>::TILE); }
+
+// ------------------------------------------------------------------ the M/X update as its own kernel
+//
+// Row a5 (eqn.search-dir-comp, eqn.approx-update) for large panels (split mode,
+// p in {16, 32}): the update of block k-2 on the main stream right before K1a(k) (its V_{k-2} rows
+// are overwritten by K1(k)'s W).  Same arithmetic as dmma_update -- for every output the DMMAs
+// accumulate in the same order ([Tr R^{-1}], -B2, -B1 per k-chunk; then Z_{k-1}, then Z_k) -- so the
+// results are bitwise those of the fused update.  The difference is register blocking: a warp
+// owns TRU = 16 rows (two 8-row DMMA chunks) and walks the k-chunks outermost, so each A fragment
+// feeds NC DMMAs and each B fragment (a p x p factor in fragment order) two, instead of one each
+// (at p = 32 the fused update was bound by shared-memory bandwidth: 2 LDS.64 per DMMA).
+template <int P>
+struct UpdB {
+    static constexpr int WARPS = 8;
+    static constexpr int TRU = 16;
+    static constexpr int MC = TRU / 8;
+    static constexpr int NS = P >= 32 ? 1 : 2;     // cp.async stages per warp (shared-memory budget)
+    static constexpr int RS = P + 4;
+    static constexpr int TILE = TRU * RS;
+    static constexpr int SLOT = 4 * TILE;          // V_b, M_{b-2} (-> M_b), M_{b-1}, X
+    static constexpr size_t bytes = sizeof(double) * (5 * P * P + WARPS * NS * SLOT);
+};
+
+
+constexpr int UPD_THREADS = 256;
+template <int P>
+__global__ void __launch_bounds__(UPD_THREADS, 1) k1u_update(K1Args a) {
+    static_assert(UpdB<P>::WARPS * 32 == UPD_THREADS, "k1u_update block size");
+    using U = UpdB<P>;
+    using D = DM<P>;
+    constexpr int WARPS = U::WARPS, TRU = U::TRU, MC = U::MC, NS = U::NS, RS = U::RS, TILE = U::TILE;
+    constexpr int KC = D::KC, NC = D::NC, FR = D::FR;
+    DevState* st = a.st;
+    pdl_wait();   // (reduce2 of block k-1 has completed; K1a(k) and K1(k) wait for this grid)
+    const long long k = st->k_main, b = k - 2;
+    // the same condition as K1's fused update (uniform over CTAs; see k1_dmma)
+    if (!(b >= st->k_upd_min && b < st->k_side && b < st->stop_side_at)) return;
+    unsigned long long* tr = trace_begin(st, TR_K4B);
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->upd_last = b;
+    const int xm = a.xdefer ? (((b - st->k_upd_min) & 1) ? 2 : 1) : 0;
+    const bool with_x = xm != 1;
+    K4bArgs u{a.Y, a.Mk2, a.Mk1, a.Xs, a.n, st, (a.sk + 1) % 3, 0, a.par, 1, b, xm, b};
+    extern __shared__ __align__(16) double dynu[];
+    UpdF<P> f{dynu, dynu + FR, dynu + 2 * FR, dynu + 3 * FR, dynu + 4 * FR};
+    double* pipe = dynu + 5 * FR;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fc = lane & 3;
+    double* wb = pipe + warp * NS * U::SLOT;
+    const long long ntiles = (a.n + TRU - 1) / TRU;
+    const long long tw = (long long)blockIdx.x * WARPS + warp, ts = (long long)gridDim.x * WARPS;
+    auto issue = [&](long long it) {
+        const long long t = tw + it * ts;
+        if (t < ntiles) {
+            double* sl = wb + (int)(it % NS) * U::SLOT;
+            const long long base = t * TRU;
+            stage_rows<P, TRU>(sl, u.U, base, a.n, lane);
+            stage_rows<P, TRU>(sl + TILE, u.M2, base, a.n, lane);
+            stage_rows<P, TRU>(sl + 2 * TILE, u.M1, base, a.n, lane);
+            if (with_x) stage_rows<P, TRU>(sl + 3 * TILE, u.X, base, a.n, lane);
+        }
+        cp_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < NS - 1; ++s) issue(s);
+    upd_setup<P>(u, f, threadIdx.x, blockDim.x);
+    __syncthreads();
+    for (long long it = 0; tw + it * ts < ntiles; ++it) {
+        if (NS > 1) {
+            issue(it + NS - 1);
+            cp_wait<NS - 1>();
+        } else {
+            issue(it);
+            cp_wait<0>();
+        }
+        __syncwarp();
+        double* sl = wb + (int)(it % NS) * U::SLOT;
+        const double* tV = sl;
+        double* tM2 = sl + TILE;
+        const double* tM1 = sl + 2 * TILE;
+        const double* tX = sl + 3 * TILE;
+        const long long base = (tw + it * ts) * TRU;
+        // M_b = V_b (Tr_b R^{-1}) - M_{b-2} B2 - M_{b-1} B1, k-chunks outermost
+        double mk[MC][NC][2];
+#pragma unroll
+        for (int mc = 0; mc < MC; ++mc)
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) mk[mc][nc][0] = mk[mc][nc][1] = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+            double aV[MC], a2[MC], a1[MC];
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc) {
+                const int ai = (mc * 8 + fr) * RS + kc * 4 + fc;
+                aV[mc] = tV[ai];
+                a2[mc] = tM2[ai];
+                a1[mc] = tM1[ai];
+            }
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const int bi = (kc * NC + nc) * 32 + lane;
+                const bool tri = kc <= 2 * nc + 1;   // Tr_b R^{-1} is upper triangular
+                const double bA = tri ? f.fA[bi] : 0.0, b2 = f.fB2[bi], b1 = f.fB1[bi];
+#pragma unroll
+                for (int mc = 0; mc < MC; ++mc) {
+                    if (tri) dmma(mk[mc][nc][0], mk[mc][nc][1], aV[mc], bA);
+                    dmma(mk[mc][nc][0], mk[mc][nc][1], a2[mc], b2);
+                    dmma(mk[mc][nc][0], mk[mc][nc][1], a1[mc], b1);
+                }
+            }
+        }
+        __syncwarp();
+        // M_b overwrites M_{b-2} (in the tile and in HBM)
+#pragma unroll
+        for (int mc = 0; mc < MC; ++mc) {
+            const long long row = base + mc * 8 + fr;
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                const int col = nc * 8 + 2 * fc;
+                tM2[(mc * 8 + fr) * RS + col] = mk[mc][nc][0];
+                tM2[(mc * 8 + fr) * RS + col + 1] = mk[mc][nc][1];
+                if (row < a.n) *reinterpret_cast<double2*>(u.M2 + row * P + col) = make_double2(mk[mc][nc][0], mk[mc][nc][1]);
+            }
+        }
+        __syncwarp();
+        if (with_x) {
+            // X += M_{b-1} Z_{b-1} (deferred, xm = 2), then X += M_b Z_b
+            double x[MC][NC][2];
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc)
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    const int col = nc * 8 + 2 * fc;
+                    x[mc][nc][0] = tX[(mc * 8 + fr) * RS + col];
+                    x[mc][nc][1] = tX[(mc * 8 + fr) * RS + col + 1];
+                }
+            if (xm == 2) {
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc) {
+                    double a1[MC];
+#pragma unroll
+                    for (int mc = 0; mc < MC; ++mc) a1[mc] = tM1[(mc * 8 + fr) * RS + kc * 4 + fc];
+#pragma unroll
+                    for (int nc = 0; nc < NC; ++nc) {
+                        const double bz = f.fZp[(kc * NC + nc) * 32 + lane];
+#pragma unroll
+                        for (int mc = 0; mc < MC; ++mc) dmma(x[mc][nc][0], x[mc][nc][1], a1[mc], bz);
+                    }
+                }
+            }
+#pragma unroll
+            for (int kc = 0; kc < KC; ++kc) {
+                double a2[MC];
+#pragma unroll
+                for (int mc = 0; mc < MC; ++mc) a2[mc] = tM2[(mc * 8 + fr) * RS + kc * 4 + fc];
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    const double bz = f.fZ[(kc * NC + nc) * 32 + lane];
+#pragma unroll
+                    for (int mc = 0; mc < MC; ++mc) dmma(x[mc][nc][0], x[mc][nc][1], a2[mc], bz);
+                }
+            }
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc) {
+                const long long row = base + mc * 8 + fr;
+                if (row < a.n)
+#pragma unroll
+                    for (int nc = 0; nc < NC; ++nc)
+                        *reinterpret_cast<double2*>(u.X + row * P + nc * 8 + 2 * fc) =
+                            make_double2(x[mc][nc][0], x[mc][nc][1]);
+            }
+        }
+        __syncwarp();
+    }
+    cp_wait<0>();
+    trace_pt(tr, 5);
+}
 
 // ------------------------------------------------------------------ K1a: the SpMM alone (split mode)
 //

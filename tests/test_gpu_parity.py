@@ -128,6 +128,9 @@ def test_split_mode_bitwise(p):
         if kw.get("timing"):
             assert r.stats["phase_launches"]["spmm_av"] > 0
             assert r.stats["phase_launches"]["spmm_fused"] == 0
+            # p >= 16: the M/X update runs as its own register-blocked kernel (k1u_update), bitwise
+            # the fused update of the other mode
+            assert (r.stats["phase_launches"]["update_main"] > 0) == (p >= 16)
 
 
 @pytest.mark.parametrize("p,maxit", [(8, 120), (8, 128), (16, 144), (32, 160)])
