@@ -222,6 +222,13 @@ int bminres_set_comm_callbacks(bminres_handle h, const bminres_comm_callbacks *c
 int bminres_halo_plan(int32_t world, int32_t rank, const int64_t *offsets, int64_t nnz, const int32_t *col_idx,
                       int32_t *local_col, int64_t *halo_rows, int64_t *n_halo, int64_t *halo_count);
 
+/* Interior rows of a partition (host only): the longest run [*lo, *hi) of this rank's rows whose
+ * remapped columns (local_col from bminres_halo_plan; < n_loc = own row) are all local, i.e. whose
+ * SpMM rows need no halo row.  In split mode the solver runs these rows' SpMM while the halo of
+ * the next basis block is exchanged (overlap), then the rows [0, lo) and [hi, n_loc).
+ * row_ptr: n_loc+1 offsets into local_col.  lo = hi = 0 when no row is interior. */
+int bminres_interior_rows(int64_t n_loc, const int32_t *row_ptr, const int32_t *local_col, int64_t *lo, int64_t *hi);
+
 /* Message of the last error on this handle (or the last create error if h is NULL). */
 const char *bminres_last_error(bminres_handle h);
 

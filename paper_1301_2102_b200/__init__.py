@@ -4,7 +4,7 @@ The product is ``libbminres.so`` (C ABI, include/bminres.h; CUDA sm_100a kernels
 ``csrc/``).  This package only builds it (``_build``) and binds it (``binding``).
 """
 from .binding import (BminresError, DeviceCsr, HostCsrRows, Solver, SolveResult, STATUS, SUPPORTED_P, TorchComm,  # noqa: F401
-                      halo_plan, lib, nccl_unique_id, workspace_bytes)
+                      halo_plan, interior_rows, lib, nccl_unique_id, workspace_bytes)
 
 __all__ = ["BminresError", "DeviceCsr", "HostCsrRows", "Solver", "SolveResult", "STATUS", "SUPPORTED_P", "TorchComm", "halo_plan",
-           "lib", "nccl_unique_id", "workspace_bytes"]
+           "interior_rows", "lib", "nccl_unique_id", "workspace_bytes"]

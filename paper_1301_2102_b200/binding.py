@@ -96,6 +96,8 @@ def lib():
         L.bminres_set_comm_callbacks.argtypes = [C.c_void_p, C.POINTER(CommCallbacks)]
         L.bminres_halo_plan.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
+        L.bminres_interior_rows.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int64)]
         L.bminres_last_error.argtypes = [C.c_void_p]
         L.bminres_last_error.restype = C.c_char_p
         L.bminres_destroy.argtypes = [C.c_void_p]
@@ -107,7 +109,7 @@ def lib():
 EXPORTED = ["bminres_default_options", "bminres_create", "bminres_solve", "bminres_stats", "bminres_get_history",
             "bminres_get_events", "bminres_spmm", "bminres_random_vector", "bminres_workspace_bytes",
             "bminres_get_unique_id", "bminres_init_nccl", "bminres_set_comm_callbacks", "bminres_halo_plan",
-            "bminres_last_error", "bminres_destroy"]
+            "bminres_interior_rows", "bminres_last_error", "bminres_destroy"]
 
 
 def _ptr(x):
@@ -245,6 +247,19 @@ def halo_plan(world: int, rank: int, offsets, col_idx):
     if rc != 0:
         raise BminresError(f"bminres_halo_plan: {STATUS.get(rc, rc)}")
     return local[:len(col)], rows[:nh.value], cnt
+
+
+def interior_rows(row_ptr, local_col):
+    """bminres_interior_rows (host only): the longest run [lo, hi) of rows with only local columns."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    lc = np.ascontiguousarray(local_col, dtype=np.int32)
+    if lc.size == 0:
+        lc = np.zeros(1, dtype=np.int32)
+    lo, hi = C.c_int64(), C.c_int64()
+    rc = lib().bminres_interior_rows(len(rp) - 1, rp.ctypes.data, lc.ctypes.data, C.byref(lo), C.byref(hi))
+    if rc != 0:
+        raise BminresError(f"bminres_interior_rows: {STATUS.get(rc, rc)}")
+    return lo.value, hi.value
 
 
 @dataclass

@@ -50,6 +50,7 @@ struct Kfn {  // per-p kernel table
     size_t smem1u;
     // start block / exit residual: Gram, V R^{-1}, plain SpMM (DMMA / K1a versions for p = 8, 16, 32)
     void (*red2f)(DevState*, int, int);   // reduce2 + factorisation for the DMMA K1 (null: k_reduce)
+    void (*fac2)(DevState*, int);         // row partition: the factorisation after the allreduce
     void (*gram)(const double*, long long, int, double*, int, double*, unsigned*);
     void (*mat)(const double*, const double*, double*, long long, int);
     size_t smem_gram, smem_mat;
@@ -71,6 +72,7 @@ Kfn make_kfn(int q) {
     f.k1u = nullptr;
     f.smem1u = 0;
     f.red2f = nullptr;
+    f.fac2 = nullptr;
     f.gram = k_gram;
     f.mat = k_materialize;
     f.smem_gram = f.smem_mat = 0;
@@ -95,6 +97,7 @@ Kfn make_kfn(int q) {
             // (p = 8: the one-cluster variant, 136k vs 134k it/s; p = 16: the ticketed one, 106k vs 103k)
             if constexpr (P <= 8) f.red2f = k_red2f<P, DM<P>::FR, DM<P>::NC>;
             else if constexpr (P <= 16) f.red2f = k_red2f_t<P, DM<P>::FR, DM<P>::NC>;
+            if constexpr (P <= 16) f.fac2 = k_fac2<P, DM<P>::FR, DM<P>::NC>;
             f.smem1pre = K1DSmem<P, true>::bytes;
             if constexpr (P >= 16) {
                 f.k1u = k1u_update<P>;
@@ -159,6 +162,8 @@ struct bminres_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // side branch during graph capture
     cudaStream_t cstream = nullptr;   // host-A staging copies, overlapped with the start block
+    cudaStream_t ustream = nullptr;   // split mode: the M/X update (k1u_update) beside K1a
+    cudaEvent_t ev_u0 = nullptr, ev_u1 = nullptr;
     cudaEvent_t ev_a = nullptr;       // host A staged (recorded on cstream)
     double* startbuf = nullptr;       // k_start_cgs: S, ||F0(:,i)||, events
     bool coop_ok = false;             // cooperative launches supported
@@ -195,6 +200,7 @@ struct bminres_ctx {
     size_t bx_cap = 0, xx_cap = 0;
     // graphs
     cudaGraphExec_t gexec[6] = {};
+    long long graph_launches = 0;   // kernels captured in one graph
     const void* gkey[8] = {};
     // per-solve
     std::vector<Retained> retained;
@@ -233,6 +239,12 @@ struct bminres_ctx {
     double* d_sendbuf = nullptr;
     size_t lcol_cap = 0, send_cap = 0, sendbuf_cap = 0;
     std::vector<long long> sc_d, rc_d;     // halo counts in doubles (rows x p) per peer
+    // halo overlap (split mode): rows [int_lo, int_hi) reference no halo row, so K1a runs them while
+    // the exchange of V_{k+1} is in flight on hstream
+    long long int_lo = 0, int_hi = 0;
+    bool overlap = false, halo_pending = false;
+    cudaStream_t hstream = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     int world() const { return opt.world; }
 };
 
@@ -628,7 +640,9 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (which == 2 && h->red2_fac && P <= 8) {   // k_red2f: one cluster of RF_CL CTAs
+    // row partition: the totals are summed by k_reduce, allreduced, then factored by k_fac2
+    const bool fac_after = which == 2 && h->red2_fac && h->tp;
+    if (which == 2 && h->red2_fac && !h->tp && P <= 8) {   // k_red2f: one cluster of RF_CL CTAs
         at[1].id = cudaLaunchAttributeClusterDimension;
         at[1].val.clusterDim.x = RF_CL;
         at[1].val.clusterDim.y = 1;
@@ -646,14 +660,25 @@ void launch_reduce(bminres_ctx* h, cudaStream_t s, int which, long long k) {
     // K1, which completed before reduce1's wait returned) -- config 2 145.8k -> 146.8k it/s
     static const int early1 = getenv("BMINRES_NO_EARLY_RED1") ? 0 : 1;
     const int early = h->split ? 0 : (which == 2 ? early2 : early1);
-    cudaError_t e = (which == 2 && h->red2_fac)
+    cudaError_t e = (which == 2 && h->red2_fac && !fac_after)
                         ? cudaLaunchKernelEx(&cfg, h->kf.red2f, h->st, (int)(k & 1), early)
-                        : cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, early);
+                        : cudaLaunchKernelEx(&cfg, k_reduce, h->st, which, (int)(k & 1), P, fac_after ? 0 : early);
     if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_reduce: ") + cudaGetErrorString(e));
     h->launches++;
     if (h->tp) {   // the totals over all ranks (K3b then runs replicated)
         double* tot = which == 1 ? h->st->red1 : h->st->red2[k & 1];
         allred(h, tot, which == 1 ? P * P + P : P * P + MAXQ * P, s);
+    }
+    if (fac_after) {   // every rank factors the bitwise-identical totals once (K1's prologue loads them)
+        cudaLaunchConfig_t fc{};
+        fc.gridDim = dim3(1);
+        fc.blockDim = dim3(256);
+        fc.stream = s;
+        fc.attrs = at;
+        fc.numAttrs = 1;   // (PDL after the allreduce)
+        cudaError_t e2 = cudaLaunchKernelEx(&fc, h->kf.fac2, h->st, (int)(k & 1));
+        if (e2 != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k_fac2: ") + cudaGetErrorString(e2));
+        h->launches++;
     }
 }
 
@@ -671,6 +696,36 @@ void halo_exchange(bminres_ctx* h, double* V, int p, cudaStream_t s) {
     if (!h->tp->exchange(h->d_sendbuf, h->sc_d.data(), V + h->plan.n_loc * p, h->rc_d.data(), s, err))
         fail(h, BMINRES_ENCCL, err);
 }
+// The exchange of V_{k+1} after K2(k), overlapped (split mode with an interior): the rows are
+// packed on s, the transport runs on hstream; K1a(k+1) processes the interior rows meanwhile and
+// waits for ev_halo before the boundary rows (launch_k1).  halo_join makes s wait for a pending
+// exchange (every other consumer of the halo, graph ends, the end of the block loop).
+void halo_exchange_async(bminres_ctx* h, double* V, int p, cudaStream_t s) {
+    if (!h->tp) return;
+    if (!h->overlap) {
+        halo_exchange(h, V, p, s);
+        return;
+    }
+    TimeMark tm(h, PH_OTHER);
+    const long long ns = (long long)h->plan.send_rows.size();
+    if (ns > 0) {
+        k_pack_rows<<<grid_for(h, ns * p, 256, 4 * h->n_sm), 256, 0, s>>>(V, h->d_send_rows, ns, p, h->d_sendbuf);
+        check_launch(h, "k_pack_rows");
+    }
+    CK(cudaEventRecord(h->ev_pack, s));
+    CK(cudaStreamWaitEvent(h->hstream, h->ev_pack, 0));
+    std::string err;
+    if (!h->tp->exchange(h->d_sendbuf, h->sc_d.data(), V + h->plan.n_loc * p, h->rc_d.data(), h->hstream, err))
+        fail(h, BMINRES_ENCCL, err);
+    CK(cudaEventRecord(h->ev_halo, h->hstream));
+    h->halo_pending = true;
+}
+void halo_join(bminres_ctx* h, cudaStream_t s) {
+    if (!h->halo_pending) return;
+    CK(cudaStreamWaitEvent(s, h->ev_halo, 0));
+    h->halo_pending = false;
+}
+
 // Y = A X alone (start block with X0, exit residual, bminres_spmm): the full-occupancy K1a kernel
 // for p in {8, 16, 32}, else the plain variant of the generic K1.  Both sum each row in CSR order
 // with fma from 0 (bitwise the same A X as the block steps' SpMM).
@@ -694,23 +749,40 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
              par, sk, h->tpw, fuse, h->M[par], h->M[par ^ 1], sp.X, nullptr, h->xdefer ? 1 : 0};
+    // the M/X update of block k-2 (row a5): its V_{k-2} rows are overwritten by K1(k)'s W, so it runs
+    // on this stream before K1a(k) (PDL).  BMINRES_UPD_BRANCH (experiment): on its own high-priority
+    // branch beside K1a(k) (independent data), joined before K1(k) -- measured no faster at config 4
+    // (2.10k vs 2.10k it/s; the pair is bound by HBM and the power cap together)
+    bool upd_branch = false;
     if (h->split && h->upd_sep && fuse) {
-        // the M/X update of block k-2 (row a5) on this stream before K1a(k): its V_{k-2} rows are
-        // overwritten by K1(k)'s W; K1a and K1 wait for it (PDL)
-        TimeMark tm(h, PH_UPD_MAIN);
-        cudaLaunchConfig_t cfg{};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
-        cfg.gridDim = dim3(h->n_sm);
-        cfg.blockDim = dim3(UPD_THREADS);
-        cfg.dynamicSmemBytes = h->kf.smem1u;
-        cfg.stream = s;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k1u, a);
-        if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k1u_update: ") + cudaGetErrorString(e));
-        h->launches++;
+        static const bool branch = getenv("BMINRES_UPD_BRANCH") != nullptr;
+        upd_branch = !h->opt.timing && branch;
+        cudaStream_t us = s;
+        if (upd_branch) {
+            CK(cudaEventRecord(h->ev_u0, s));
+            CK(cudaStreamWaitEvent(h->ustream, h->ev_u0, 0));
+            us = h->ustream;
+        }
+        cudaStream_t keep = h->stream;
+        h->stream = us;
+        {
+            TimeMark tm(h, PH_UPD_MAIN);
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = (h->pdl && !upd_branch) ? 1 : 0;
+            cfg.gridDim = dim3(h->n_sm - 1);   // (one SM left for K3b: the two do not fit one SM together)
+            cfg.blockDim = dim3(UPD_THREADS);
+            cfg.dynamicSmemBytes = h->kf.smem1u;
+            cfg.stream = us;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k1u, a);
+            if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k1u_update: ") + cudaGetErrorString(e));
+            h->launches++;
+        }
+        h->stream = keep;
+        if (upd_branch) CK(cudaEventRecord(h->ev_u1, us));
         a.fuse = 0;
         fuse = 0;
     }
@@ -720,9 +792,12 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
         aa.Vprev = nullptr;
         aa.Y = h->AV;
         aa.fuse = 0;
+        // (BMINRES_K1A_DYN, experiment: chunks in order from st->k1a_ctr -- for K1a beside the update
+        // branch; alone it measured slower, 3.09 vs 2.63 ms at config 4)
+        aa.dyn = getenv("BMINRES_K1A_DYN") ? 1 : 0;
         cudaStream_t keep = h->stream;
         h->stream = s;
-        {
+        auto k1a_launch = [&](const K1Args& args) {
             TimeMark tm(h, PH_SPMM_AV);
             cudaLaunchConfig_t cfg{};
             cudaLaunchAttribute at[1];
@@ -734,11 +809,30 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
             cfg.stream = s;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k1a, aa);
+            cudaError_t e = cudaLaunchKernelEx(&cfg, h->kf.k1a, args);
             if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k1a_spmm: ") + cudaGetErrorString(e));
             h->launches++;
+        };
+        if (h->halo_pending) {
+            // row partition: the interior rows while V_k's halo is in flight, then the boundary
+            // rows [0, int_lo) and [int_hi, n) once it has landed
+            K1Args ai = aa;
+            ai.r0 = h->int_lo;
+            ai.nrows = h->int_hi - h->int_lo;
+            k1a_launch(ai);
+            halo_join(h, s);
+            K1Args ab = aa;
+            ab.r0 = 0;
+            ab.nrows = h->int_lo + (n - h->int_hi);
+            ab.gap_at = h->int_lo;
+            ab.gap = h->int_hi - h->int_lo;
+            if (ab.dyn) ab.dyn = 2;
+            if (ab.nrows > 0) k1a_launch(ab);
+        } else {
+            k1a_launch(aa);
         }
         a.AV = h->AV;
+        if (upd_branch) CK(cudaStreamWaitEvent(s, h->ev_u1, 0));   // the update read V_{k-2}
         {
             TimeMark tm(h, fuse ? PH_EPI_FUSED : PH_EPI);
             launch_cluster(h, h->kf.k1pre, h->nb1, h->kf.nt1, h->kf.smem1pre, a, "k1_dmma(split)");
@@ -747,6 +841,7 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
         launch_reduce(h, s, 1, k);
         return;
     }
+    halo_join(h, s);
     {
         TimeMark tm(h, fuse ? PH_SPMM_FUSED : PH_SPMM);
         cudaStream_t keep = h->stream;
@@ -767,7 +862,7 @@ void launch_k2(bminres_ctx* h, cudaStream_t s, long long n, long long k, bool wi
         launch_cluster(h, h->kf.k2, h->nb2, h->kf.nt2, h->kf.smem2, a, "k2_orth");
         h->stream = keep;
     }
-    halo_exchange(h, h->V[(sk + 1) % 3], h->p_ws, s);   // V_{k+1} rows the peers' SpMM reads
+    halo_exchange_async(h, h->V[(sk + 1) % 3], h->p_ws, s);   // V_{k+1} rows the peers' SpMM reads
     if (with_reduce) launch_reduce(h, s, 2, k);
 }
 // side branch of block k: M_k -> M[k%2] (over M_{k-2}), M_{k-1} = M[(k+1)%2]
@@ -847,7 +942,9 @@ void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
             CK(cudaEventRecord(h->ev_join, h->side));
         }
         CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+        halo_join(h, h->stream);   // (a graph ends with no exchange in flight)
         CK(cudaStreamEndCapture(h->stream, &g));
+        h->graph_launches = h->launches - saved;   // kernels per graph (the same for every residue)
         h->launches = saved;
         CK(cudaGraphInstantiate(&h->gexec[q], g, 0));
         cudaGraphDestroy(g);
@@ -888,6 +985,7 @@ T get_state(bminres_ctx* h, size_t offset) {
 // Tr_{b+1} = I, DevState.Ck[par] = C_b and the pool coefficients of block b are zero (the
 // pool was updated here, column by column).
 void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, long long maxit) {
+    halo_join(h, h->stream);   // (the exchange of the candidates' halo, replaced below)
     TimeMark tm(h, PH_SLOW);
     const int par = (int)(b & 1);
     const long long j0 = GET_STATE(h, j_done) + 1;
@@ -1133,7 +1231,7 @@ bool retained_live(bminres_ctx* h, long long jfirst) {
 
 // Build (or reuse) the halo plan of this rank's CSR rows: offsets of all ranks, remote columns by
 // owner, the lists the peers read from this rank (exchanged), the remapped column indices.
-void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, int p) {
+void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* rowptr_dev, const int* col_dev, int p) {
     const int world = h->opt.world, rank = h->opt.rank;
     const void* key[5] = {A->col_idx, (const void*)(intptr_t)A->nnz, (const void*)(intptr_t)A->row_begin,
                           (const void*)(intptr_t)A->n_loc, (const void*)(intptr_t)A->n};
@@ -1154,8 +1252,11 @@ void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, i
             off[q + 1] = off[q] + rcv[2 * q + 1];
         }
         if (off[world] != A->n) fail(h, BMINRES_EINVAL, "the ranks' rows do not cover 0..n-1");
-        std::vector<int> col(std::max<long long>(A->nnz, 1));
-        CK(cudaMemcpy(col.data(), col_dev, A->nnz * sizeof(int), cudaMemcpyDeviceToHost));
+        std::vector<int> col(std::max<long long>(A->nnz, 1)), rp(A->n_loc + 1);
+        // (stream-ordered: a host CSR is staged on h->stream just before)
+        CK(cudaMemcpyAsync(col.data(), col_dev, A->nnz * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(rp.data(), rowptr_dev, (A->n_loc + 1) * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
         HaloPlan& pl = h->plan;
         if (!build_halo_plan(world, rank, off.data(), A->nnz, col.data(), pl))
             fail(h, BMINRES_EINVAL, "column index outside [0, n)");
@@ -1185,6 +1286,10 @@ void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, i
             h->send_cap = std::max<long long>(ns, 1);
         }
         h2d(h, h->d_send_rows, pl.send_rows.data(), ns * sizeof(long long));
+        long long lo = 0, hi = 0;
+        interior_rows(A->n_loc, rp.data(), pl.local_col.data(), &lo, &hi);
+        h->int_lo = lo;
+        h->int_hi = hi;
         std::copy(key, key + 5, h->plan_key);
     }
     const long long ns = (long long)h->plan.send_rows.size();
@@ -1205,6 +1310,7 @@ void setup_partition(bminres_ctx* h, const bminres_csr* A, const int* col_dev, i
 // into the scratch slot Vs, the halo exchanged, and the SpMM gathers from Vs.
 const double* extended_input(bminres_ctx* h, const double* X, long long n, int p, double* Vs) {
     if (!h->tp) return X;
+    halo_join(h, h->stream);
     CK(cudaMemcpyAsync(Vs, X, (size_t)n * p * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
     halo_exchange(h, Vs, p, h->stream);
     return Vs;
@@ -1332,12 +1438,17 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         }
     }
     if (h->tp) {   // (a transport at world = 1 runs the same path with an empty halo)
-        setup_partition(h, A, sp.col, p);   // halo plan; the SpMM reads the remapped columns
+        setup_partition(h, A, sp.rowptr, sp.col, p);   // halo plan; the SpMM reads the remapped columns
         sp.col = h->d_lcol;
     } else {
         h->n_ext = n;
     }
     ensure_workspace(h, n, p, q);
+    // row partition, split mode: overlap the exchange with K1a's interior rows when they are at least
+    // a quarter of the rows (z-slabs of config 4: all but the first and last planes; config 5's
+    // long-range entries leave no interior at G > 1)
+    h->overlap = h->tp && h->split && (h->int_hi - h->int_lo) * 4 >= n && getenv("BMINRES_NO_HALO_OVERLAP") == nullptr;
+    h->halo_pending = false;
     const double* B = Bin;
 
     // ---- history buffer
@@ -1373,9 +1484,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     init.part2[1] = h->part2[1];
     init.ncl1 = h->nb1 / h->csz;
     init.ncl2 = h->nb2 / h->csz;
-    // reduce2 factors the new block once (single rank: a partition's totals are allreduced after
-    // the reduce kernel, so each rank's K1 factors them itself)
-    h->red2_fac = h->kf.red2f && !h->tp && !getenv("BMINRES_NO_RED2F");
+    // reduce2 factors the new block once (a row partition: k_fac2 after the allreduce of the totals)
+    h->red2_fac = h->kf.red2f && !getenv("BMINRES_NO_RED2F");
     init.red2_fac = h->red2_fac ? 1 : 0;
     init.fac_bad = 0;
     init.given_blk = -1;
@@ -1608,6 +1718,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         }
         // pipelined graphs: side block s with main block s+1 (fused: K1(s+1) applies the
         // update of block s-1; updates of blocks < b were applied explicitly)
+        halo_join(h, h->stream);   // (the graphs' first K1 does not wait for an exchange launched before them)
         if (h->kf.fused) SET_STATE(h, k_upd_min, b);
         long long launched = 0;
         // The host stops launching on a stop / breakdown seen in a graph it has synchronised
@@ -1616,7 +1727,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         // same graphs (their collectives match).
         for (long long s = b; s <= nblocks && graphs; s += GB) {
             CK(cudaGraphLaunch(h->gexec[s % 6], h->stream));
-            h->launches += GB * ((h->kf.fused ? 5 : 6) + (h->split ? 1 : 0) + (h->upd_sep ? 1 : 0));
+            h->launches += h->graph_launches;
             CK(cudaEventRecord(lag_ev[launched % LAG], h->stream));
             launched++;
             if (launched >= LAG) {
@@ -1650,6 +1761,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         }
         main_ahead = true;
     }
+    halo_join(h, h->stream);
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaEventRecord(e_loop1, h->stream));
     for (auto& e : lag_ev) cudaEventDestroy(e);
@@ -1792,6 +1904,12 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
         CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
         h->prio_hi = prio_hi;
         CK(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, prio_hi));
+        CK(cudaStreamCreateWithPriority(&h->ustream, cudaStreamNonBlocking, prio_hi));
+        CK(cudaStreamCreateWithPriority(&h->hstream, cudaStreamNonBlocking, prio_hi));
+        CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_u0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_u1, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
         // large dynamic shared memory for the p = 32 kernels
@@ -1966,6 +2084,15 @@ int bminres_halo_plan(int32_t world, int32_t rank, const int64_t* offsets, int64
     return BMINRES_OK;
 }
 
+int bminres_interior_rows(int64_t n_loc, const int32_t* row_ptr, const int32_t* local_col, int64_t* lo, int64_t* hi) {
+    if (n_loc < 0 || !row_ptr || (n_loc > 0 && row_ptr[n_loc] > 0 && !local_col) || !lo || !hi) return BMINRES_EINVAL;
+    long long l = 0, u = 0;
+    interior_rows(n_loc, row_ptr, local_col, &l, &u);
+    *lo = l;
+    *hi = u;
+    return BMINRES_OK;
+}
+
 const char* bminres_last_error(bminres_handle h) {
     if (!h) return g_create_err.c_str();
     return h->err.c_str();
@@ -1995,6 +2122,12 @@ void bminres_destroy(bminres_handle h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->ustream) cudaStreamDestroy(h->ustream);
+    if (h->hstream) cudaStreamDestroy(h->hstream);
+    if (h->ev_pack) cudaEventDestroy(h->ev_pack);
+    if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+    if (h->ev_u0) cudaEventDestroy(h->ev_u0);
+    if (h->ev_u1) cudaEventDestroy(h->ev_u1);
     if (h->cstream) cudaStreamDestroy(h->cstream);
     if (h->startbuf) cudaFree(h->startbuf);
     if (h->hstate) cudaFreeHost(h->hstate);

@@ -77,6 +77,27 @@ inline bool build_halo_plan(int world, int rank, const long long* offsets, long 
     return true;
 }
 
+// The longest run of rows [lo, hi) whose columns are all local (remapped index < n_loc): the
+// interior, whose SpMM rows need no halo row.  (lo = hi = 0 when there is none.)
+inline void interior_rows(long long n_loc, const int* row_ptr, const int* local_col, long long* lo, long long* hi) {
+    long long best_lo = 0, best = 0, cur = 0;
+    for (long long i = 0; i < n_loc; ++i) {
+        bool in = true;
+        for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+            if (local_col[e] >= n_loc) {
+                in = false;
+                break;
+            }
+        cur = in ? cur + 1 : 0;
+        if (cur > best) {
+            best = cur;
+            best_lo = i - cur + 1;
+        }
+    }
+    *lo = best_lo;
+    *hi = best_lo + best;
+}
+
 // ------------------------------------------------------------------ transports
 
 struct Transport {
@@ -152,6 +173,13 @@ struct NcclTransport : Transport {
     long long* dbuf = nullptr;   // device staging of the plan lists
     size_t dcap = 0;
     bool init(const unsigned char id[128], int rank_, int world_, std::string& err) {
+        // The allreduces' summation order must be fixed (bitwise reproducible runs,
+        // and every rank's replicated small QR depends on it): pin the ring algorithm and the LL
+        // protocol (the allreduced buffers are <= 9 KB, where LL is also the fastest) unless the
+        // caller set them.  (NCCL_PROTO applies to collectives only; the halo send/recv keep
+        // NCCL's own point-to-point protocol choice.)
+        setenv("NCCL_ALGO", "Ring", 0);
+        setenv("NCCL_PROTO", "LL", 0);
         NcclApi& a = nccl_api();
         if (!a.load(err)) return false;
         rank = rank_;

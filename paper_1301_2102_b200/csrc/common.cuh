@@ -82,6 +82,9 @@ struct DevState {
     long long hist_cap;
     double tol, tau;
     unsigned cnt1, cnt2, cnt3, cnt4;   // tickets (cnt2: k_red2f's last CTA)
+    // K1a chunk counters (split mode, dynamic chunk order; [1]: the boundary launch of a row
+    // partition), reset by K1(k) -- which runs after K1a(k) completes -- for K1a(k+1)
+    unsigned long long k1a_ctr[2];
     // k_red2f (single rank): reduce2's last CTA factors the new block once -- C_k, Tr_{k+1},
     // coef_k in the state, and K1(k+1)'s fragments of Tr_{k+1} and -(Tr_k C_k^T) below; fac_bad:
     // breakdown / cancellation of the block (published as by K1's own prologue)
@@ -564,6 +567,50 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
     return true;
 }
 
+// The factorisation of block k's new candidates from reduce2's totals in sm[0 .. P*P + q*P):
+// factor_block (Cholesky of W'^T W', the breakdown / cancellation tests), C_k,
+// Tr_{k+1} = C_k^{-1}, coef_k, D = Tr_k C_k^T, and K1(k+1)'s fragments of Tr_{k+1} and -D.
+// k = k_main - 1 (K2(k) advanced k_main).  All threads of one CTA.
+template <int P, int FRN, int NCF>
+__device__ void red2_factor(DevState* st, int par, double* sm, unsigned long long* tr) {
+    const int Q = st->q_live;
+    double* sRed = sm;                           // totals (P*P + MAXQ*P)
+    double* sC = sRed + P * P + MAXQ * P;
+    double* sCi = sC + P * P;
+    double* sTp = sCi + P * P;
+    double* sCo = sTp + P * P;
+    double* sOm = sCo + P * MAXQ;
+    double* sD = sOm + P;
+    const long long k = st->k_main - 1;
+    const int sk1 = (int)((k + 1) % 3), sk = (int)(k % 3);
+    for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
+    load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
+    __syncthreads();
+    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo);
+    if (bad) {
+        if (threadIdx.x == 0) {
+            st->fac_bad = 1;
+            publish_breakdown(st, k);
+        }
+        trace_pt(tr, 5);
+        return;
+    }
+    store_pp<P>(st->Ck[par], sC);
+    store_pp<P>(st->Tr[sk1], sCi);
+    for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[par][t] = sCo[t];
+    smm_nn<P>(sTp, sC, sD, true);                // D = Tr_k C_k^T
+    __syncthreads();
+    // fragment order of the DMMA K1 (to_frag: 4 x 8 blocks, KC = P/4 k-chunks, NCF = P/8 n-chunks)
+    for (int t = threadIdx.x; t < FRN; t += blockDim.x) {
+        const int blk = t / 32, l = t % 32, kc = blk / NCF, nc = blk % NCF;
+        const int r = kc * 4 + l % 4, c = nc * 8 + l / 4;
+        st->fT[t] = sCi[r * P + c];
+        st->fD[t] = -sD[r * P + c];
+    }
+    if (threadIdx.x == 0) st->fac_bad = 0;
+    trace_pt(tr, 5);
+}
+
 // reduce2 with the factorisation (red2_fac, single rank): the totals of K2(k)'s partials as
 // k_reduce computes them (same order), then the last CTA to finish (ticket) factors the new block
 // exactly as K1(k+1)'s prologue would -- factor_block on the totals, C_k, Tr_{k+1} = C_k^{-1},
@@ -610,42 +657,8 @@ __global__ void __launch_bounds__(256) k_red2f_t(DevState* st, int par, int earl
     if (!s_last) return;
     __threadfence();
     if (threadIdx.x == 0) st->cnt2 = 0u;
-    double* sRed = sm;                           // totals (P*P + MAXQ*P)
-    double* sC = sRed + P * P + MAXQ * P;
-    double* sCi = sC + P * P;
-    double* sTp = sCi + P * P;
-    double* sCo = sTp + P * P;
-    double* sOm = sCo + P * MAXQ;
-    double* sD = sOm + P;
-    const long long k = st->k_main - 1;
-    const int sk1 = (int)((k + 1) % 3), sk = (int)(k % 3);
-    for (int t = threadIdx.x; t < E; t += blockDim.x) sRed[t] = __ldcg(st->red2[par] + t);
-    for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
-    load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
-    __syncthreads();
-    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo);
-    if (bad) {
-        if (threadIdx.x == 0) {
-            st->fac_bad = 1;
-            publish_breakdown(st, k);
-        }
-        trace_pt(tr, 5);
-        return;
-    }
-    store_pp<P>(st->Ck[par], sC);
-    store_pp<P>(st->Tr[sk1], sCi);
-    for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[par][t] = sCo[t];
-    smm_nn<P>(sTp, sC, sD, true);                // D = Tr_k C_k^T
-    __syncthreads();
-    // fragment order of the DMMA K1 (to_frag: 4 x 8 blocks, KC = P/4 k-chunks, NCF = P/8 n-chunks)
-    for (int t = threadIdx.x; t < FRN; t += blockDim.x) {
-        const int blk = t / 32, l = t % 32, kc = blk / NCF, nc = blk % NCF;
-        const int r = kc * 4 + l % 4, c = nc * 8 + l / 4;
-        st->fT[t] = sCi[r * P + c];
-        st->fD[t] = -sD[r * P + c];
-    }
-    if (threadIdx.x == 0) st->fac_bad = 0;
-    trace_pt(tr, 5);
+    for (int t = threadIdx.x; t < E; t += blockDim.x) sm[t] = __ldcg(st->red2[par] + t);
+    red2_factor<P, FRN, NCF>(st, par, sm, tr);
 }
 
 // One thread-block cluster of RF_CL CTAs x RF_W warps: each warp sums its entries (k_reduce's
@@ -691,42 +704,22 @@ __global__ void __launch_bounds__(rf_warps<P>() * 32) k_red2f(DevState* st, int 
     }
     cl.sync();
     if (cl.block_rank() != 0) return;   // (the leader reads only its own shared memory)
-    double* sRed = sm;                           // totals (P*P + MAXQ*P)
-    double* sC = sRed + P * P + MAXQ * P;
-    double* sCi = sC + P * P;
-    double* sTp = sCi + P * P;
-    double* sCo = sTp + P * P;
-    double* sOm = sCo + P * MAXQ;
-    double* sD = sOm + P;
-    const long long k = st->k_main - 1;
-    const int sk1 = (int)((k + 1) % 3), sk = (int)(k % 3);
-    for (int t = threadIdx.x; t < E; t += blockDim.x) st->red2[par][t] = sRed[t];   // (K3b(k) reads them)
-    for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
-    load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
-    __syncthreads();
-    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo);
-    if (bad) {
-        if (threadIdx.x == 0) {
-            st->fac_bad = 1;
-            publish_breakdown(st, k);
-        }
-        trace_pt(tr, 5);
-        return;
-    }
-    store_pp<P>(st->Ck[par], sC);
-    store_pp<P>(st->Tr[sk1], sCi);
-    for (int t = threadIdx.x; t < P * MAXQ; t += blockDim.x) st->coef[par][t] = sCo[t];
-    smm_nn<P>(sTp, sC, sD, true);                // D = Tr_k C_k^T
-    __syncthreads();
-    // fragment order of the DMMA K1 (to_frag: 4 x 8 blocks, KC = P/4 k-chunks, NCF = P/8 n-chunks)
-    for (int t = threadIdx.x; t < FRN; t += blockDim.x) {
-        const int blk = t / 32, l = t % 32, kc = blk / NCF, nc = blk % NCF;
-        const int r = kc * 4 + l % 4, c = nc * 8 + l / 4;
-        st->fT[t] = sCi[r * P + c];
-        st->fD[t] = -sD[r * P + c];
-    }
-    if (threadIdx.x == 0) st->fac_bad = 0;
-    trace_pt(tr, 5);
+    for (int t = threadIdx.x; t < E; t += blockDim.x) st->red2[par][t] = sm[t];   // (K3b(k) reads them)
+    red2_factor<P, FRN, NCF>(st, par, sm, tr);
+}
+
+// Factor-only reduce2 tail for a row partition: the totals were summed by k_reduce and allreduced
+// over the ranks (bitwise identical on every rank), so every rank factors them once here -- one
+// CTA, the same code as k_red2f's -- and K1(k+1)'s prologue only loads the fragments.
+template <int P, int FRN, int NCF>
+__global__ void __launch_bounds__(256) k_fac2(DevState* st, int par) {
+    unsigned long long* tr = trace_begin(st, TR_RED2);
+    pdl_wait();
+    if (!st->run_main) return;
+    __shared__ double sm[P * P + MAXQ * P + 3 * P * P + P * MAXQ + P + 2 * P * P];
+    const int E = P * P + st->q_live * P;
+    for (int t = threadIdx.x; t < E; t += blockDim.x) sm[t] = __ldcg(st->red2[par] + t);
+    red2_factor<P, FRN, NCF>(st, par, sm, tr);
 }
 
 // K2 prologue, block k: G = Tr_k^T (V_k^T W) from K1's partials, om2; CTA 0 publishes G, om2 for

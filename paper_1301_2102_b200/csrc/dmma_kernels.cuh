@@ -848,13 +848,35 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
     const int sub = lane % LP, rsub = lane / LP;
     const bool act = sub < LANES;
     const int c0 = sub * VEC;
-    const long long ngroups = (a.n + RPW - 1) / RPW;
+    // rows: all n, or (row partition, halo overlap) the interior range / the boundary rows around it
+    const long long nr = a.nrows >= 0 ? a.nrows : a.n;
+    const long long ngroups = (nr + RPW - 1) / RPW;
     const long long chunk = (long long)nw * KU;
-    long long cidx = blockIdx.x;
+    // chunk order: static round robin over the CTAs, or (dyn) taken in increasing order from a
+    // counter by whichever CTA is resident -- all resident CTAs then sweep the rows together even
+    // when some become resident late (K1a running beside the update kernel), so the far stencil
+    // neighbours (z planes) stay in L2
+    __shared__ long long s_chunk;
+    unsigned long long* ctr = (st && a.dyn) ? st->k1a_ctr + (a.dyn - 1) : nullptr;
+    auto next_chunk = [&](long long cur) -> long long {
+        if (!ctr) return cur < 0 ? (long long)blockIdx.x : cur + gridDim.x;
+        __syncthreads();   // every warp is done with the current chunk's s_chunk
+        if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(ctr, 1ull);
+        __syncthreads();
+        return s_chunk;
+    };
+    long long cidx = next_chunk(-1);
     int cpos = warp;
-    for (long long g = cidx * chunk + cpos; g < ngroups;) {
-        const long long i = g * RPW + rsub;
-        const bool live = act && i < a.n;
+    for (long long g = cidx * chunk + cpos; g < ngroups || (ctr && cidx * chunk < ngroups);) {
+        if (g >= ngroups) {   // (dyn: this warp has no group in the chunk's tail; the others may)
+            cpos = warp;
+            cidx = next_chunk(cidx);
+            g = cidx * chunk + cpos;
+            continue;
+        }
+        const long long v = g * RPW + rsub;
+        const long long i = a.r0 + v + ((a.gap_at >= 0 && v >= a.gap_at) ? a.gap : 0);
+        const bool live = act && v < nr;
         const int r0 = live ? __ldg(a.rowptr + i) : 0;
         const int r1 = live ? __ldg(a.rowptr + i + 1) : 0;
         double acc[VEC];
@@ -898,7 +920,7 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
         cpos += nw;
         if (cpos >= chunk) {
             cpos = warp;
-            cidx += gridDim.x;
+            cidx = next_chunk(cidx);
         }
         g = cidx * chunk + cpos;
     }
@@ -1185,6 +1207,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             cp_commit();
         };
         pdl_wait();   // A V_k (k1a) and, through it, red2 of block k-1 are complete
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->k1a_ctr[0] = st->k1a_ctr[1] = 0ull;   // for K1a(k+1)
         trace_pt(tr, 2);
 #pragma unroll
         for (int s = 0; s < NSP; ++s) stage3(s);   // the first tiles stream in during the prologue

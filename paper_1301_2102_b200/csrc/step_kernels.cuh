@@ -49,6 +49,10 @@ struct K1Args {
     // split mode (k1_dmma<P, true>): A V_k was computed by k1a_spmm into AV; K1 stages its rows
     const double* AV;
     int xdefer;           // fused update: X updates deferred in pairs
+    // K1a only (row partitions, halo overlap): the rows processed are r0 + v (+ gap once v >= gap_at)
+    // for v < nrows; nrows < 0: all n rows
+    long long r0 = 0, nrows = -1, gap_at = -1, gap = 0;
+    int dyn = 0;          // K1a: CTA chunks taken from st->k1a_ctr[dyn - 1] in order (0: static round robin)
 };
 
 template <int P>

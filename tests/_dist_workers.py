@@ -93,6 +93,9 @@ def problem(name):
     if name == "lap3d12p8":
         A = synth.laplacian_3d(12, shift=2.5)
         return synth.Problem("lap3d12p8", A, synth.gaussian_rhs(A.n, 8, seed=1), 1e-10, 4000)
+    if name == "slab16":   # z-slabs of a 3-D Laplacian with p = 16, solved in split mode (halo overlap)
+        A = synth.laplacian_3d(12, 12, 16, shift=2.5)
+        return synth.Problem("slab16", A, synth.gaussian_rhs(A.n, 16, seed=3), 1e-10, 4000)
     if name == "dep2d":   # config 3's recipe (B = [G, G C + eps N], eps = 0) on a small grid: step-0 events
         A = synth.laplacian_2d(20, shift=2.5)
         return synth.Problem("dep2d", A, synth.dependent_rhs(A.n, 4, 0.0, seed=0), 1e-10, 4000)
@@ -108,7 +111,8 @@ def solve_worker(rank, world, port, outdir, name, maxit):
     off = _split(P.n, world)
     A = DeviceCsr.rows_from_host(P.A, off[rank], off[rank + 1], "cuda:0")
     B = torch.from_numpy(np.ascontiguousarray(P.B[off[rank]:off[rank + 1]])).to("cuda:0")
-    with Solver(0, rank=rank, world=world, comm=TorchComm()) as s:
+    # slab16: split mode (K1a alone, its interior rows overlapping the halo exchange; the update kernel)
+    with Solver(0, rank=rank, world=world, comm=TorchComm(), split_spmm=1 if name == "slab16" else 0) as s:
         r = s.solve(A, B, tol=P.tol, maxit=maxit, deflation_tol=P.tau)
         X = r.X.cpu().numpy()
     ev = np.array([[e["j"], e["col"], e["kind"], e["action"]] for e in r.events], dtype=np.int64).reshape(-1, 4)

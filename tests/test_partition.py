@@ -42,6 +42,33 @@ def _local_spmm(A, off, rank, local, halo_rows, X):
     return Y
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_interior_rows_of_z_slabs(world):
+    """The overlap's interior (bminres_interior_rows): for z-slabs of a 3-D 7-point stencil
+    (nx x ny planes, lexicographic, z slowest) a rank's interior is its slab minus its first plane
+    (unless it is rank 0) and its last plane (unless it is the last rank) -- the closed form of the
+    rows with no neighbour in another slab; a random matrix has (almost) none."""
+    from paper_1301_2102_b200 import halo_plan, interior_rows
+    nx, ny, nz = 6, 5, 4 * world
+    A = synth.laplacian_3d(nx, ny, nz, shift=1.3)
+    plane = nx * ny
+    off = [plane * (nz * q // world) for q in range(world + 1)]
+    ip = np.asarray(A.indptr, dtype=np.int64)
+    for r in range(world):
+        k0, k1 = ip[off[r]], ip[off[r + 1]]
+        local, _, _ = halo_plan(world, r, off, A.indices[k0:k1])
+        lo, hi = interior_rows((ip[off[r]:off[r + 1] + 1] - k0).astype(np.int32), local)
+        n_loc = off[r + 1] - off[r]
+        assert (lo, hi) == ((plane if r > 0 else 0), (n_loc - plane if r < world - 1 else n_loc))
+    B = synth.random_sym_sparse(60, 0.3, seed=2)
+    off = [0, 30, 60]
+    ip = np.asarray(B.indptr, dtype=np.int64)
+    local, _, _ = halo_plan(2, 0, off, B.indices[:ip[30]])
+    lo, hi = interior_rows(ip[:31].astype(np.int32), local)
+    rows_ok = [all(local[e] < 30 for e in range(ip[i], ip[i + 1])) for i in range(30)]
+    assert hi - lo == max((len(run) for run in "".join("1" if x else "0" for x in rows_ok).split("0")), default=0)
+
+
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("kind", ["lap3d", "random"])
 def test_halo_plan_reproduces_global_product(world, kind):
@@ -117,12 +144,14 @@ def test_two_rank_solve_matches_single_rank(tmp_path, name, maxit):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,maxit", [("1c", 120), ("lap3d12p8", 160), ("dep2d", 200)])
+@pytest.mark.parametrize("name,maxit", [("1c", 120), ("lap3d12p8", 160), ("dep2d", 200), ("slab16", 192)])
 def test_two_rank_solve_matches_oracle(tmp_path, name, maxit):
     """Row a6 against the ORACLE (not the single-rank GPU solve): the 2-rank partitioned solve
-    (halo exchange + allreduces, replicated small QR) gives the oracle's residual history to 1e-9
-    over the first 50 iterations, its iteration count and status, its dependence events (dep2d:
-    step-0 replacements of columns 5-8) and its X."""
+    (halo exchange + allreduces, replicated small QR, the block factored once per rank after the
+    allreduce) gives the oracle's residual history to 1e-9 over the first 50 iterations, its
+    iteration count and status, its dependence events (dep2d: step-0 replacements of columns 5-8)
+    and its X.  slab16: z-slabs in split mode -- K1a's interior rows run before the halo lands, the
+    boundary rows after it."""
     import oracle
     from tests._dist_workers import problem, solve_worker
     _spawn(solve_worker, 2, str(tmp_path), name, maxit)

@@ -1,0 +1,101 @@
+"""Row f4: the block-vs-sequential study inputs (CPU pins) and the GPU study solves
+against the oracle (-m gpu).
+
+The study's "sequential MINRES" is p independent p = 1 solves; block MINRES with p = 1 is MINRES
+(pinned against SciPy in test_oracle_pins.py::test_p1_is_scalar_minres).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import studies
+
+
+# ----------------------------------------------------------------------------- inputs (CPU)
+
+
+def test_model_matrix_is_the_papers_operator():
+    """A = -L - 200 I, L = h^-2 (I (+) T + T (+) I), T = tridiag(1,-2,1), built as
+    Kronecker sums here and compared entry by entry; 13 negative eigenvalues at N = 200 (indefinite)."""
+    N = 12
+    h = 1.0 / (N - 1)
+    T = np.diag(-2.0 * np.ones(N)) + np.diag(np.ones(N - 1), 1) + np.diag(np.ones(N - 1), -1)
+    L = (np.kron(np.eye(N), T) + np.kron(T, np.eye(N))) / h ** 2
+    np.testing.assert_allclose(synth.csr_to_dense(studies.model_matrix(N)), -L - 200 * np.eye(N * N), rtol=1e-15)
+    lam, _, _ = studies.eigenpairs(200)
+    assert (lam < 0).sum() == 13 and np.all(np.diff(np.abs(lam)) >= 0)
+
+
+def test_analytic_eigenvectors():
+    """q_{kl} are orthonormal eigenvectors of A with the stated eigenvalues (ordered by |lambda|)."""
+    N = 14
+    A = synth.csr_to_dense(studies.model_matrix(N))
+    lam, k, l = studies.eigenpairs(N)
+    Q = np.stack([studies.eigvec_combination(N, k[i:i + 1], l[i:i + 1], np.ones(1)) for i in range(N * N)], axis=1)
+    np.testing.assert_allclose(Q.T @ Q, np.eye(N * N), atol=1e-12)
+    np.testing.assert_allclose(A @ Q, Q * lam[None, :], atol=1e-9 * np.abs(lam).max())
+    ref = np.sort(np.abs(np.linalg.eigvalsh(A)))
+    np.testing.assert_allclose(np.abs(lam), ref, rtol=1e-10)
+
+
+@pytest.mark.parametrize("kind", ["small", "large"])
+def test_eigmix_pairs_share_exactly_2m_components(kind):
+    """eqn.smalleigsRHS / eqn.largeeigsRHS: b_1 and b_2 have components on 2m common eigenvectors
+    (m = 0: orthogonal), and lie in the stated eigen-subspaces."""
+    N, band = 12, 6
+    lam, k, l = studies.eigenpairs(N)
+    Q = np.stack([studies.eigvec_combination(N, k[i:i + 1], l[i:i + 1], np.ones(1)) for i in range(N * N)], axis=1)
+    for m in (0, 1, 3):
+        B = studies.eigmix_pair(N, m, kind, seed=m, band=band)
+        c1, c2 = Q.T @ B[:, 0], Q.T @ B[:, 1]
+        common = (np.abs(c1) > 1e-12) & (np.abs(c2) > 1e-12)
+        assert common.sum() == 2 * m
+        if m == 0:
+            assert abs(B[:, 0] @ B[:, 1]) < 1e-10
+        n = N * N
+        s1 = set(np.flatnonzero(np.abs(c1) > 1e-12))
+        if kind == "small":
+            assert s1 == set(range(band + m))
+        else:
+            assert s1 == set(range(2 * band)) | set(range(n - 2 * band, n - 2 * band + m))
+
+
+def test_fig2_and_fig4_rhs():
+    B = studies.fig2_rhs(10, 4)
+    assert np.all(B[:, 0] == 1) and np.all(B[:3, 1:] == np.eye(3)) and np.all(B[3:, 1:] == 0)
+    p1, p2 = studies.fig4_pairs(5)
+    assert p1[0, 0] == 1 and np.all(p1[:, 1] == 1) and p2[1, 1] == 1 and p2[:, 1].sum() == 1
+
+
+# ----------------------------------------------------------------------------- GPU studies vs the oracle
+
+
+@pytest.mark.gpu
+def test_study_counts_match_oracle():
+    """The study's block and sequential iteration counts on a small grid (N = 24) equal the
+    oracle's within the north star's +-2% (or +-2): Fig. 2 RHS (p = 4), both Fig. 4 pairs, and one
+    eigen-mix pair of each kind -- solved through the batched runner of scripts/study_block_vs_seq.py."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "study", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                              "study_block_vs_seq.py"))
+    study = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(study)
+    N = 24
+    A = studies.model_matrix(N)
+    run = study.Runner(A, threads=3, tol=1e-8, maxit=20000)
+    cases = [studies.fig2_rhs(A.n, 4), *studies.fig4_pairs(A.n),
+             studies.eigmix_pair(N, 2, "small", seed=5, band=12), studies.eigmix_pair(N, 10, "large", seed=6, band=12)]
+    try:
+        for B in cases:
+            blk, seq = run.block_and_sequential(B)
+            ref = oracle.solve(A, B, tol=1e-8, maxit=20000)
+            assert abs(blk["iterations"] - ref.iterations) <= max(2, 0.02 * ref.iterations), (blk, ref.iterations)
+            assert blk["status"] == ref.status_name
+            for c, s in enumerate(seq):
+                rc = oracle.solve(A, B[:, c:c + 1], tol=1e-8, maxit=20000)
+                assert abs(s["iterations"] - rc.iterations) <= max(2, 0.02 * rc.iterations), (c, s, rc.iterations)
+    finally:
+        run.close()
