@@ -36,7 +36,7 @@ class Event(C.Structure):
 
 
 class Config(C.Structure):
-    _fields_ = [("p", C.c_int32), ("pool_size", C.c_int32), ("use_x0", C.c_int32), ("pad", C.c_int32),
+    _fields_ = [("p", C.c_int32), ("pool_size", C.c_int32), ("use_x0", C.c_int32), ("policy", C.c_int32),
                 ("tol", C.c_double), ("tau", C.c_double), ("maxit", C.c_int64), ("seed", C.c_uint64),
                 ("history", C.c_void_p), ("history_cap", C.c_int64),
                 ("events", C.c_void_p), ("events_cap", C.c_int64),
@@ -108,8 +108,9 @@ class OracleResult:
 
 
 def solve(A, B, *, tol=1e-8, maxit=100, tau=1e-8, seed=0, pool_size=1, X0=None,
-          history=True, events_cap=4096, debug_iters=0) -> OracleResult:
-    """Run the oracle.  A: synth.Csr; B: n×p float64 (row-major)."""
+          history=True, events_cap=4096, debug_iters=0, policy=0) -> OracleResult:
+    """Run the oracle.  A: synth.Csr; B: n×p float64 (row-major).  policy: 0 replacement
+    (P:690-729), 1 block-size reduction "shrink"."""
     B = np.ascontiguousarray(B, dtype=np.float64)
     n, p = B.shape
     indptr = np.ascontiguousarray(A.indptr, dtype=np.int32)
@@ -117,7 +118,7 @@ def solve(A, B, *, tol=1e-8, maxit=100, tau=1e-8, seed=0, pool_size=1, X0=None,
     data = np.ascontiguousarray(A.data, dtype=np.float64)
     X = np.zeros((n, p)) if X0 is None else np.array(X0, dtype=np.float64, order="C", copy=True)
     cfg = Config()
-    cfg.p, cfg.pool_size, cfg.use_x0 = p, pool_size, int(X0 is not None)
+    cfg.p, cfg.pool_size, cfg.use_x0, cfg.policy = p, pool_size, int(X0 is not None), int(policy)
     cfg.tol, cfg.tau, cfg.maxit, cfg.seed = tol, tau, maxit, seed
     hist = np.zeros((maxit + 1, p)) if history else None
     if hist is not None:

@@ -57,7 +57,8 @@ typedef struct {
     int64_t j;      /* iteration at which the candidate was rejected (0 = start block) */
     int32_t col;    /* 1-based: block column ((j-1) mod p)+1, or RHS column at j = 0 */
     int32_t kind;   /* 0 = exact (h <= 1e-12*omega), 1 = near (C15) */
-    int32_t action; /* 1 = replaced, 2 = replaced + retained, 3 = pool exhausted */
+    int32_t action; /* 1 = replaced, 2 = replaced + retained, 3 = pool exhausted,
+                       4 = removed (shrink policy), 5 = removed + retained */
     int32_t pad;
     double ratio;   /* h / omega */
 } orc_event;
@@ -66,7 +67,7 @@ typedef struct {
     int32_t p;
     int32_t pool_size;
     int32_t use_x0;
-    int32_t pad;
+    int32_t policy;         /* 0 = replacement, 1 = block-size reduction "shrink" */
     double tol;
     double tau;             /* deflation tolerance (the paper's gamma) */
     int64_t maxit;
@@ -235,6 +236,10 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
     retained_t *ret = calloc((size_t)(pool_cap + W2 + 4), sizeof(retained_t));
     int64_t n_ret = 0, ret_cap = pool_cap + W2 + 4;
     double *Vref = calloc((size_t)(W2 * (p + 1)), sizeof(double));
+    /* shrink policy: absent[i % W2] = 1 when u_i was removed (u_i = 0, not in the basis);
+       indices keep their numbering */
+    unsigned char *absent = calloc((size_t)W2, 1);
+    const int shrink = cfg->policy == 1;
     double *tauref = calloc((size_t)W2, sizeof(double));
     double *hl = calloc((size_t)(HR * p), sizeof(double));   /* hl[i%HR][t-1] = h_{i+t,i} */
     double *hcol = calloc((size_t)(2 * p + 1), sizeof(double));
@@ -245,7 +250,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
     double ycol[ORC_MAX_P + 1];
     double z[ORC_MAX_P];
     if (!Ubuf || !Mbuf || !Wblk || !w || !mj || !F || !pool || !ret || !Vref || !tauref || !hl ||
-        !hcol || !work) {
+        !hcol || !work || !absent) {
         res->status = ORC_ENOMEM;
         goto done;
     }
@@ -286,7 +291,14 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
                 S[l * p + i] += s;
             }
         double h = nrm2(n, ui);
-        if (h <= tau * fn0) {
+        if (h <= tau * fn0 && shrink) {
+            /* shrink: the dependent start column is removed, u_i = 0 */
+            double ratio = fn0 > 0.0 ? h / fn0 : 0.0;
+            record_event(cfg, &nev, 0, i + 1, h <= 1e-12 * fn0 ? 0 : 1, 4, ratio);
+            S[i * p + i] = 0.0;
+            memset(ui, 0, sizeof(double) * (size_t)n);
+            absent[(i + 1) % W2] = 1;
+        } else if (h <= tau * fn0) {
             double ratio = fn0 > 0.0 ? h / fn0 : 0.0;
             record_event(cfg, &nev, 0, i + 1, h <= 1e-12 * fn0 ? 0 : 1, 1, ratio);
             S[i * p + i] = 0.0;
@@ -335,6 +347,36 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
         /* block operator application every p iterations (Alg. 2, C2) */
         if (m == 0)
             for (int c = 0; c < p; ++c) csr_matvec(n, indptr, indices, data, U(j + c), Wblk + (int64_t)c * n);
+        /* shrink: the basis is exhausted once every index of the window j .. j+p-1 is removed */
+        if (shrink) {
+            int live = 0;
+            for (int64_t i = j; i <= j + p - 1; ++i) live += !absent[i % W2];
+            if (!live) break;
+        }
+        if (shrink && absent[j % W2]) {
+            /* u_j was removed: column j of \bar H is deleted -- A u_j = 0, so
+               u_{j+p} = 0 is removed too, h_{.,j} = 0; no reflector (identity), R column
+               j and m_j are zero, z_j is the tail's first row (zero: the removed row of Z) */
+            for (int q = 0; q <= 2 * p; ++q) hcol[q] = 0.0;
+            for (int t = 1; t <= p; ++t) hl[(j % HR) * p + (t - 1)] = 0.0;
+            double *unew0 = U(j + p);
+            memset(unew0, 0, sizeof(double) * (size_t)n);
+            absent[(j + p) % W2] = 1;
+            if (dcap > 0 && j <= dcap && cfg->dbg_U) memset(cfg->dbg_U + (j + p - 1) * n, 0, sizeof(double) * (size_t)n);
+            double *vj0 = Vref + (j % W2) * (p + 1);
+            for (int q = 0; q <= p; ++q) vj0[q] = q == 0 ? 1.0 : 0.0;
+            tauref[j % W2] = 0.0;
+            for (int c = 0; c < p; ++c) {
+                z[c] = T[c];
+                for (int r = 0; r < p - 1; ++r) T[r * p + c] = T[(r + 1) * p + c];
+                T[(p - 1) * p + c] = 0.0;
+            }
+            memset(MV(j), 0, sizeof(double) * (size_t)n);
+            for (int64_t i = 0; i < n; ++i)
+                for (int c = 0; c < p; ++c) X[i * p + c] += 0.0 * z[c];
+            if (dcap > 0 && j <= dcap && cfg->dbg_Z) memcpy(cfg->dbg_Z + (j - 1) * p, z, sizeof(double) * (size_t)p);
+            goto residuals;
+        }
         memcpy(w, Wblk + (int64_t)m * n, sizeof(double) * (size_t)n);
         const double omega = nrm2(n, w);           /* raw candidate norm ||A u_j|| (C14) */
 
@@ -358,6 +400,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
         double h = nrm2(n, w);
         double hjp;
         double *unew = U(j + p);
+        absent[(j + p) % W2] = 0;
         if (h <= tau * omega) {
             /* breakdown: candidate dependent */
             int kind = h <= 1e-12 * omega ? 0 : 1;
@@ -378,7 +421,12 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
                 n_ret++;
                 action = 2;
             }
-            if (pool_next < pool_cap) {
+            if (shrink) {
+                /* block-size reduction: u_{j+p} = 0 is not added to the basis */
+                memset(unew, 0, sizeof(double) * (size_t)n);
+                absent[(j + p) % W2] = 1;
+                action = kind == 1 ? 5 : 4;
+            } else if (pool_next < pool_cap) {
                 /* replacement: pool vector, already orthogonal to u_1..u_{j+p-1}
                    (P:718-721); orthogonalised twice more against retained + window, normalised */
                 double *r = pool + pool_next * n;
@@ -464,6 +512,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
         }
 
         /* ---- computed residuals (eqn.comp-resid) and the stop test (C7) ---- */
+    residuals:;
         double mx = 0.0;
         for (int c = 0; c < p; ++c) {
             double s = 0.0;
@@ -499,7 +548,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
 done:
     if (ret) for (int64_t q = 0; q < n_ret; ++q) free(ret[q].vec);
     free(Ubuf); free(Mbuf); free(Wblk); free(w); free(mj); free(F); free(pool); free(ret);
-    free(Vref); free(tauref); free(hl); free(hcol); free(work);
+    free(Vref); free(tauref); free(hl); free(hcol); free(work); free(absent);
 #undef U
 #undef MV
     return res->status;

@@ -1,0 +1,24 @@
+"""K3b (small banded QR) phase times from the device tracer: prologue (factor), the serial chain
+(warp 0: phase A reflectors + phase B), the stores.  usage: python scripts/trace_k3b.py P [launch]"""
+import os, sys, tempfile
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+p = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+launch = sys.argv[2] if len(sys.argv) > 2 else "20"
+f = os.path.join(tempfile.gettempdir(), "bmr_trace_k3b.bin")
+os.environ["BMINRES_TRACE"] = launch
+os.environ["BMINRES_TRACE_FILE"] = f
+import torch, synth
+from paper_1301_2102_b200 import DeviceCsr, Solver
+A = synth.laplacian_3d(40, shift=3.0)
+B = synth.gaussian_rhs(A.n, p, seed=1)
+dA, dB = DeviceCsr.from_host(A, "cuda:0"), torch.from_numpy(B).to("cuda:0")
+res = []
+for graphs in (False, True):
+    with Solver(0, pool_size=1, record_history=False, use_graphs=graphs) as s:
+        s.solve(dA, dB, tol=0.0, maxit=40 * p, history=False)
+    t = np.fromfile(f, dtype=np.uint64).reshape(7, 1024, -1).astype(np.int64)
+    x = t[4, 0]
+    d = np.diff(x[[0, 2, 3, 5]]) / 1e3
+    print(f"p={p} graphs={graphs}: K3b prologue+load {d[0]:.1f} us, serial chain {d[1]:.1f} us, stores {d[2]:.1f} us, "
+          f"total {(x[5]-x[0])/1e3:.1f} us")

@@ -562,3 +562,112 @@ def test_singular_r_closed_form():
     assert r.events and r.events[0]["j"] == 1 and r.events[0]["col"] == 1 and r.events[0]["kind"] == 0
     assert r.iterations == 0
     np.testing.assert_array_equal(r.X, 0.0)
+
+
+# ----------------------------------------------------------------------------- f1: block-size reduction ("shrink")
+
+
+def _shrink_example():
+    """p = 2, B = [b, A^3 b] on a random integer symmetric matrix: A u_5 is exactly dependent (the
+    first dependent candidate of B = [b, A^t b] is at j = 2t - 1, P8) -- the paper's example of
+    P:601-611 (dependence at column 5, p = 2)."""
+    rng = np.random.default_rng(7)
+    n = 12
+    M = rng.integers(-3, 4, (n, n))
+    M = np.triu(M, 1)
+    M = M + M.T
+    M[np.diag_indices(n)] = rng.integers(-4, 5, n)
+    b = rng.integers(-2, 3, n).astype(float)
+    B = np.stack([b, M @ M @ M @ b], axis=1).astype(float)
+    return synth.dense_to_csr(M.astype(float)), M.astype(float), B
+
+
+def test_shrink_patterns_of_the_paper():
+    """Shrink policy: u_7 = 0 is removed, hence u_9 = u_11 = 0; columns 7, 9
+    and rows 7, 9, 11 of H_10 vanish and the compacted H~_10 has exactly the printed pattern
+    (eqn.H10-dep); A U~_10 = U~_12 H~_10; R~_10 is the QR factor of H~_10 (dense
+    brute force), with the bold zero r_{5,10} of eqn.R10-dep.  Reading C25: the printed
+    bold zero r_{2,6} is not a structural zero (reflector 2 spans rows 2..4 and h_{4,6} = h_{6,4} > 0);
+    brute force gives a nonzero entry, which the oracle reproduces."""
+    A, M, B = _shrink_example()
+    r = oracle.solve(A, B, tol=0.0, maxit=10, pool_size=1, policy=1, debug_iters=10)
+    assert [(e["j"], e["col"], e["kind"], e["action"]) for e in r.events] == [(5, 1, 0, 4)]
+    H, R, U = r.dbg["H"], r.dbg["R"], r.dbg["U"]
+    assert np.all(H[[6, 8, 10], :] == 0) and np.all(H[:, [6, 8]] == 0)
+    assert np.all(U[:, [6, 8, 10]] == 0)
+    rows = [0, 1, 2, 3, 4, 5, 7, 9, 11]      # u_1..u_6, u_8, u_10, u_12
+    cols = [0, 1, 2, 3, 4, 5, 7, 9]           # columns 1..6, 8, 10
+    Ht = H[np.ix_(rows, cols)]
+    printed = np.array([  # eqn.H10-dep, nonzero pattern
+        [1, 1, 1, 0, 0, 0, 0, 0],
+        [1, 1, 1, 1, 0, 0, 0, 0],
+        [1, 1, 1, 1, 1, 0, 0, 0],
+        [0, 1, 1, 1, 1, 1, 0, 0],
+        [0, 0, 1, 1, 1, 1, 0, 0],
+        [0, 0, 0, 1, 1, 1, 1, 0],
+        [0, 0, 0, 0, 0, 1, 1, 1],
+        [0, 0, 0, 0, 0, 0, 1, 1],
+        [0, 0, 0, 0, 0, 0, 0, 1]])
+    np.testing.assert_array_equal(np.abs(Ht) > 1e-10, printed.astype(bool))
+    np.testing.assert_allclose(M @ U[:, cols], U[:, rows] @ Ht, atol=1e-12 * np.abs(M).sum())
+    Rt = R[np.ix_(cols, cols)]
+    _, Rd = np.linalg.qr(Ht)
+    np.testing.assert_allclose(np.abs(Rt), np.abs(Rd), rtol=1e-10, atol=1e-12)
+    assert abs(Rt[4, 7]) < 1e-12                                  # bold zero r_{5,10}
+    assert abs(Rt[1, 5]) > 1e-3                                   # r_{2,6}: reading C25
+    assert np.all(R[:, [6, 8]] == 0) and np.all(R[[6, 8], :] == 0)
+
+
+def test_shrink_bandwidth_drops_in_two_stages():
+    """removing one dependent vector reduces the bandwidth of the compacted H~ by one at
+    column i (= 5, the dependent candidate: h_{7,5} = 0) and by a second one at column i + p (= 7,
+    u_7 removed: column deleted), two vectors fewer in the Lanczos window from then on."""
+    A, M, B = _shrink_example()
+    r = oracle.solve(A, B, tol=0.0, maxit=10, pool_size=1, policy=1, debug_iters=10)
+    H = r.dbg["H"]
+    present = [i for i in range(12) if i not in (6, 8, 10)]
+    width = []
+    for c in range(10):
+        if c in (6, 8):
+            continue
+        nz = [present.index(i) for i in present if abs(H[i, c]) > 1e-10]
+        width.append(max(nz) - min(nz))   # sub- plus superdiagonals of compact column c
+    # compact columns 4, 5, 6, 8, 10: the full width 2p = 4 drops to 3 at column 5 (h_{7,5} = 0)
+    # and to 2 at column 8 (u_7 removed: no h_{7,8}) -- two vectors fewer, in two stages
+    assert width[3:] == [4, 3, 3, 2, 2], width
+
+
+@pytest.mark.parametrize("case", ["fig3", "p2_dependent"])
+def test_shrink_iterates_are_least_squares_over_the_compact_basis(case):
+    """P1 for the shrink policy: x_j minimises ||b_i - A x|| over the span of the non-removed basis
+    vectors among u_1..u_j (the compacted basis), every j; computed = true residual (P4)."""
+    if case == "fig3":
+        A = synth.laplacian_2d(10, shift=2.0)
+        D = dense(A)
+        e1 = np.zeros(A.n)
+        e1[0] = 1.0
+        B = np.stack([e1, D @ e1], axis=1)
+    else:
+        A, D, B = _shrink_example()
+    jmax = 10 if case == "p2_dependent" else 30
+    r = oracle.solve(A, B, tol=0.0, maxit=jmax, pool_size=1, policy=1, debug_iters=jmax)
+    assert r.events and all(e["action"] == 4 for e in r.events)
+    U = r.dbg["U"]
+    beta = np.linalg.norm(B, axis=0)
+    for j in range(1, r.iterations + 1):
+        rj = oracle.solve(A, B, tol=0.0, maxit=j, pool_size=1, policy=1)
+        Q = U[:, :j][:, np.linalg.norm(U[:, :j], axis=0) > 0]
+        res, Xls = lsq_residuals(D, B, Q, Q.shape[1])
+        big = res > 1e-10 * beta
+        np.testing.assert_allclose(rj.history[j][big] * beta[big], res[big], rtol=1e-7)
+        assert np.all(np.abs(rj.comp_res - rj.true_res) <= 1e-9 * np.maximum(1.0, rj.true_res))
+
+
+def test_shrink_step0_removal():
+    """Shrink at step 0 (reading C13 under P:582-636): a dependent start column is removed (u_i = 0,
+    S_ii = 0), not replaced; the other columns converge as if the block were smaller."""
+    A = synth.laplacian_2d(14, shift=2.5)
+    B = synth.dependent_rhs(A.n, 3, 0.0, seed=0)
+    r = oracle.solve(A, B, tol=1e-10, maxit=2000, pool_size=1, policy=1)
+    assert [(e["j"], e["col"], e["action"]) for e in r.events][:3] == [(0, 4, 4), (0, 5, 4), (0, 6, 4)]
+    assert r.status_name == "OK" and r.true_res.max() < 1e-9

