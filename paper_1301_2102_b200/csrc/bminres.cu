@@ -1335,7 +1335,7 @@ void debug_state(bminres_ctx* h, const char* tag) {
             d.k_main, d.j_done, d.given_blk, d.side_go, d.stop_after);
     pm("G1", d.G[1], p, MAXP, p); pm("Ck0", d.Ck[0], p, MAXP, p); pm("Ck1", d.Ck[1], p, MAXP, p); pm("CprevS", d.CprevS, p, MAXP, p);
     pm("T", d.T, p, MAXP, p); pm("res", d.res, 1, p, p);
-    pm("ring", d.rv, 2 * p + 1, MAXP + 1, p + 1); pm("rtau", d.rtau, 1, 2 * p + 1, 2 * p + 1);
+    pm("Qacc[0]", d.Qacc[0], 2 * p, 2 * MAXP, 2 * p); pm("Qacc[1]", d.Qacc[1], 2 * p, 2 * MAXP, 2 * p);
 }
 
 int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xin, int p, double tol, long long maxit,

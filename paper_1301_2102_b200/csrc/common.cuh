@@ -115,8 +115,9 @@ struct DevState {
     double B2[2][MAXP * MAXP];     // R_{k-2,k} R_kk^{-1}
     long long k_upd_min;           // fused updates (K1(k) applies block k-2's) only for blocks >= this
     long long upd_last;            // last block whose M/X update was applied
-    double rv[(2 * MAXP + 1) * (MAXP + 1)];   // Householder ring, slot = i mod (2p+1)
-    double rtau[2 * MAXP + 1];
+    // accumulated Householder: Qacc[b & 1] = H_{bp} ... H_{(b-1)p+1}
+    // restricted to the block's 2p rows (b-1)p+1 .. (b+1)p, row-major with ld 2 MAXP
+    double Qacc[2][(2 * MAXP) * (2 * MAXP)];
     double beta[MAXP];             // ||b_i||
     double res[MAXP];              // latest computed relative residuals
     double* hist;                  // (hist_cap) x p computed relative residuals, or null

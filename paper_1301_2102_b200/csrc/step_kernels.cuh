@@ -462,7 +462,10 @@ struct K3Smem {
     static constexpr int LD = P + 1, W2 = 2 * P + 1;
     static constexpr int nA = P * LD;
     static constexpr int nH = 4 * P * LD;
-    static constexpr int nV = W2 * (P + 2);
+    // accumulated Householder (f2): one 2p x 2p block matrix (ld 2p+1), this block's p reflectors
+    // (v: p+1, tau), a 2p x p product scratch
+    static constexpr int LDQ = 2 * P + 1;
+    static constexpr int nV = 2 * P * LDQ + P * (P + 2) + 2 * P * P;
     static constexpr int rest = nH + nV + 4 * P + P * P;
     static constexpr int scr = 8 * P * P + 2 * MAXQ * P + P + 8;   // prologue scratch (reuses sH..)
     static constexpr int doubles = 6 * nA + (rest > scr ? rest : scr);
@@ -472,7 +475,7 @@ struct K3Smem {
 template <int P>
 __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     using S = K3Smem<P>;
-    constexpr int W2 = S::W2, LD = S::LD;
+    constexpr int LD = S::LD;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long* tr = trace_begin(st, TR_K3B);
     __shared__ long long s_k, s_jd, s_maxit, s_hcap;
@@ -500,8 +503,10 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     double* sG = sI + S::nA;      // G (K1)
     double* sCp = sG + S::nA;     // C_{k-1}
     double* sH = sCp + S::nA;     // the block's p Hessenberg columns, global-row frame (4p rows)
-    double* sV = sH + S::nH;      // reflector ring: v (p+1) + tau per slot
-    double* sHn = sV + S::nV;     // ||h_j||
+    double* sQ = sH + S::nH;                   // an accumulated block reflector Q_b (2p x 2p, ld LDQ)
+    double* sVb = sQ + 2 * P * S::LDQ;         // this block's reflectors: v (p+1) + tau each
+    double* sTmp = sVb + P * (P + 2);          // 2p x p product scratch
+    double* sHn = sQ + S::nV;     // ||h_j||
     double* sBeta = sHn + P;      // 1 / ||b_i||
     double* sRes = sBeta + P;     // residuals of the last completed iteration
     double* sHist = sRes + P;     // residual rows of this block (P x P)
@@ -543,59 +548,58 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         sCp[s] = st->CprevS[g];
         sZ[s] = 0.0;
     }
-    for (int t = tid; t < W2 * (P + 1); t += K3T) {
-        const int s = t / (P + 1), q = t % (P + 1);
-        sV[s * (P + 2) + q] = st->rv[s * (MAXP + 1) + q];
-    }
-    for (int s = tid; s < W2; s += K3T) sV[s * (P + 2) + P + 1] = st->rtau[s];
     for (int t = tid; t < P; t += K3T) {
         sBeta[t] = st->beta[t] > 0.0 ? 1.0 / st->beta[t] : 0.0;   // 1 / ||b_i|| (0: converged at j = 0)
         sRes[t] = st->res[t];
     }
     __syncthreads();
 
+    // ---- the p new columns of \bar H in the frame of global rows (k-3)p+1 .. (k+1)p
+    //      (symmetric reuse P:923-945)
+    if (warp == 0 && lane < P) {
+        const int m = lane;
+        double hn = 0.0;
+        for (int r = 0; r < P; ++r) sH[r * LD + m] = 0.0;
+        for (int mp = 0; mp < P; ++mp) {
+            const double cv = (k > 1 && mp >= m) ? sCp[m * LD + mp] : 0.0;
+            sH[(P + mp) * LD + m] = cv;
+            const double gv = mp >= m ? sG[mp * LD + m] : sG[m * LD + mp];
+            sH[(2 * P + mp) * LD + m] = gv;
+            const double ck = mp <= m ? sC[mp * LD + m] : 0.0;
+            sH[(3 * P + mp) * LD + m] = ck;
+            hn = fma(cv, cv, fma(gv, gv, fma(ck, ck, hn)));
+        }
+        sHn[m] = sqrt(hn);
+    }
+    // ---- phase A (accumulated Householder): the reflectors
+    //      of the previous two blocks, i = (k-3)p+1 .. (k-1)p in increasing order, applied to the p new
+    //      columns as two dense products -- Q_{k-2} (block k-2's p reflectors accumulated, acting on
+    //      frame rows 0 .. 2p-1) then Q_{k-1} (rows p .. 3p-1) -- by all threads, instead of 2p
+    //      reflector applications in a serial chain per column
+    for (int b = 2; b >= 1; --b) {
+        if (k - b < 1) continue;   // (blocks before the first do not exist)
+        const double* Qg = st->Qacc[(k - b) & 1];
+        for (int t = tid; t < 4 * P * P; t += K3T) sQ[(t / (2 * P)) * S::LDQ + t % (2 * P)] = Qg[(t / (2 * P)) * (2 * MAXP) + t % (2 * P)];
+        __syncthreads();
+        const int r0 = (2 - b) * P;   // frame rows r0 .. r0 + 2p - 1
+        for (int e = tid; e < 2 * P * P; e += K3T) {
+            const int i = e / P, c = e % P;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int t = 0; t < 2 * P; ++t) acc = fma(sQ[i * S::LDQ + t], sH[(r0 + t) * LD + c], acc);
+            sTmp[e] = acc;
+        }
+        __syncthreads();
+        for (int e = tid; e < 2 * P * P; e += K3T) sH[(r0 + e / P) * LD + e % P] = sTmp[e];
+        __syncthreads();
+    }
+
     if (warp == 0) {
         const double tol = s_tol;
-        // ---- the p new columns of \bar H in the frame of global rows (k-3)p+1 .. (k+1)p
-        //      (symmetric reuse P:923-945)
-        if (lane < P) {
-            const int m = lane;
-            double hn = 0.0;
-            for (int r = 0; r < P; ++r) sH[r * LD + m] = 0.0;
-            for (int mp = 0; mp < P; ++mp) {
-                const double cv = (k > 1 && mp >= m) ? sCp[m * LD + mp] : 0.0;
-                sH[(P + mp) * LD + m] = cv;
-                const double gv = mp >= m ? sG[mp * LD + m] : sG[m * LD + mp];
-                sH[(2 * P + mp) * LD + m] = gv;
-                const double ck = mp <= m ? sC[mp * LD + m] : 0.0;
-                sH[(3 * P + mp) * LD + m] = ck;
-                hn = fma(cv, cv, fma(gv, gv, fma(ck, ck, hn)));
-            }
-            sHn[m] = sqrt(hn);
-            // phase A: reflectors i = (k-3)p+1 .. (k-1)p (previous two blocks), increasing i;
-            // frame offset o = i - ((k-3)p+1) touches rows o .. o+p
-            const long long base = (k - 3) * P + 1;
-            int slot = (int)(((base % W2) + W2) % W2);
-            for (int o = 0; o < 2 * P; ++o, slot = (slot + 1 == W2 ? 0 : slot + 1)) {
-                if (base + o < 1) continue;
-                const double* v = sV + slot * (P + 2);
-                const double t = v[P + 1];
-                double* h = sH + o * LD + m;
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q <= P; ++q) s = fma(v[q], h[q * LD], s);
-                s *= t;
-#pragma unroll
-                for (int q = 0; q <= P; ++q) h[q * LD] = fma(-s, v[q], h[q * LD]);
-            }
-        }
-        __syncwarp();
-
         // ---- phase B: generate reflector j, apply it to the later columns and to [T; 0]
         //      (row 1 -> z_j^T), residuals, stop test (Alg. 2)
         int m_last = -1, stop = 0;  // 1 converged, 2 maxit, 3 singular R, 4 pool exhausted
-        int slot = (int)(j0 % W2);
-        for (int m = 0; m < P; ++m, slot = (slot + 1 == W2 ? 0 : slot + 1)) {
+        for (int m = 0; m < P; ++m) {
             const long long j = j0 + m;
             if (j > maxit) {
                 stop = 2;
@@ -626,7 +630,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 break;
             }
             if (lane == 0) sRd[m] = 1.0 / beta;   // 1 / r_jj for R_kk^{-1}
-            double* vj = sV + slot * (P + 2);
+            double* vj = sVb + m * (P + 2);
             for (int q = lane; q <= P; q += 32) vj[q] = (q == 0) ? 1.0 : sH[(o + q) * LD + m] * scl;
             if (lane == 0) vj[P + 1] = tj;
             __syncwarp();
@@ -729,11 +733,26 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             st->ufz[k % 3][t] = st->Zh[k % 3][g];
         }
     }
-    for (int t = tid; t < W2 * (P + 1); t += K3T) {
-        const int s = t / (P + 1), q = t % (P + 1);
-        st->rv[s * (MAXP + 1) + q] = sV[s * (P + 2) + q];
+    // ---- Q_k = H_{kp} ... H_{(k-1)p+1} on the block's 2p rows (f2): the accumulated action of this
+    //      block's reflectors (those generated before a stop), for phase A of blocks k+1 and k+2;
+    //      column c of Q_k is e_c with the reflectors applied in order (one thread per column)
+    {
+        double* Qg = st->Qacc[k & 1];
+        for (int c = tid; c < 2 * P; c += K3T) {
+            double* q = sQ + c;   // column c (stride LDQ; the phase-A buffer is free now)
+            for (int r = 0; r < 2 * P; ++r) q[r * S::LDQ] = r == c ? 1.0 : 0.0;
+            for (int m = 0; m <= m_last; ++m) {   // reflector m acts on block rows m .. m+p
+                const double* v = sVb + m * (P + 2);
+                double s = 0.0;
+#pragma unroll
+                for (int t = 0; t <= P; ++t) s = fma(v[t], q[(m + t) * S::LDQ], s);
+                s *= v[P + 1];
+#pragma unroll
+                for (int t = 0; t <= P; ++t) q[(m + t) * S::LDQ] = fma(-s, v[t], q[(m + t) * S::LDQ]);
+            }
+            for (int r = 0; r < 2 * P; ++r) Qg[r * (2 * MAXP) + c] = q[r * S::LDQ];
+        }
     }
-    for (int s = tid; s < W2; s += K3T) st->rtau[s] = sV[s * (P + 2) + P + 1];
     for (int t = tid; t < P; t += K3T) st->res[t] = sRes[t];
     if (s_hcap > 0)
         for (int t = tid; t < (m_last + 1) * P; t += K3T) {
