@@ -83,8 +83,11 @@ typedef struct {
                                 2 never.  Split: the SpMM A V_k runs alone at full occupancy (K1a) and K1
                                 streams its result; same arithmetic, bitwise */
     int32_t policy;          /* dependence policy: 0 = replace the dependent vector by a random one
-                                (the paper's choice; default); 1 = shrink the block size
-                                (BMINRES_EINVAL where not built) */
+                                (the paper's choice; default); 1 = block-size reduction
+                                ("shrink"): the dependent vector is removed (u_{j+p} = 0),
+                                its lane stays removed (A 0 = 0) and its Hessenberg columns
+                                are deleted; the panels keep p columns, removed ones zero.  The solve
+                                stops (BMINRES_MAXIT unless converged) once every lane is removed */
     int32_t coeff_mode;      /* 0 = the paper's symmetric reuse h_{i,j} = h_{j,i} (default);
                                 other values: BMINRES_EINVAL (not built) */
     int32_t plan_reuse;      /* world > 1: 0 = rebuild the halo plan on every solve (default; the library keeps
@@ -99,7 +102,8 @@ typedef struct {
     int64_t j;       /* iteration (0 = the start block, eqn.init-QR) */
     int32_t col;     /* 1-based block column ((j-1) mod p)+1, or RHS column at j = 0 */
     int32_t kind;    /* 0 exact (h <= 1e-12*omega), 1 near */
-    int32_t action;  /* 1 replaced, 2 replaced + retained, 3 pool exhausted */
+    int32_t action;  /* 1 replaced, 2 replaced + retained, 3 pool exhausted, 4 removed (policy 1),
+                        5 removed + retained */
     int32_t pad;
     double ratio;    /* h / omega */
 } bminres_event;

@@ -89,6 +89,7 @@ struct StartArgs {
     double* part;        // nb x (P + 1) partials
     double* S;           // out
     double* ev;          // out: 2 x P (ratio, kind)
+    int shrink;          // policy 1: a dependent start column is removed (zeroed), not replaced
 };
 
 template <int P>
@@ -197,6 +198,15 @@ __global__ void __launch_bounds__(256, 4) k_start_cgs(StartArgs a) {
                 a.ev[2 * i] = fn > 0.0 ? hh / fn : 0.0;
                 a.ev[2 * i + 1] = hh <= 1e-12 * fn ? 0.0 : 1.0;
             }
+            if (a.shrink) {   // removed: u_i = 0, no normalisation (each thread zeroes the
+                              // elements it reads in the later passes: no grid barrier needed)
+                for (long long eb = e0; eb - sub - rsub * P < ne; eb += stride)
+                    if (in && eb < ne && sub == i) a.F[eb] = 0.0;
+                pend = -1;
+                pinv = 1.0;
+                __syncthreads();
+                continue;
+            }
             // replacement (C17, stream 0, event nrep), orthogonalised twice, normalised (deferred)
             const unsigned long long key = splitmix64(a.seed ^ (0ull << 56) ^ (nrep << 32));
             nrep++;
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(256, 4) k_start_cgs(StartArgs a) {
     }
     // the last column's normalisation
     for (long long eb = e0; eb - sub - rsub * P < ne; eb += stride)
-        if (in && eb < ne && sub == pend) a.F[eb] = a.F[eb] * pinv;
+        if (in && eb < ne && pend >= 0 && sub == pend) a.F[eb] = a.F[eb] * pinv;
 }
 
 // t[i] = scale * (t[i] - sum_k c_k v_k[i]); c_k from cdev (times csign) if non-null else cval

@@ -552,7 +552,7 @@ void launch_colstep(bminres_ctx* h, double* F, long long n, int p, int col, int 
 // k_start_cgs (aux_kernels.cuh): cooperative launch, one wave of co-resident CTAs
 void launch_start_cgs(bminres_ctx* h, double* F, long long n, int p, const double* f0n, double tau,
                       unsigned long long seed, long long row_begin, double* S, double* ev) {
-    StartArgs sa{F, n, f0n, tau, seed, row_begin, h->part, S, ev};
+    StartArgs sa{F, n, f0n, tau, seed, row_begin, h->part, S, ev, h->opt.policy == 1 ? 1 : 0};
     void* args[] = {&sa};
     const void* fn = nullptr;
     switch (p) {
@@ -1019,9 +1019,22 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
     };
     const double* Uprev = nullptr;
     const double* Ucur = nullptr;
+    // shrink policy: the lanes already removed in block b+1, and the ones removed here
+    const bool shrink = h->opt.policy == 1;
+    std::vector<long long> absent_from(MAXP, KINF);
+    if (shrink)
+        CK(cudaMemcpy(absent_from.data(), (char*)h->st + offsetof(DevState, absent_from), MAXP * sizeof(long long),
+                      cudaMemcpyDeviceToHost));
+    bool absent_changed = false;
     for (int m = 0; m < p; ++m) {
         const long long j = j0 + m;
         if (j > maxit) break;
+        if (shrink && absent_from[m] <= b + 1) {
+            // u_{j+p} was removed with an earlier u of this lane (A 0 = 0): the candidate is
+            // zero, h_{j+p,j} = 0, no event
+            Ck[m * MAXP + m] = 0.0;
+            continue;
+        }
         // MGS against the new vectors of this block (u_{bp+1} .. u_{bp+m})
         for (int mp = 0; mp < m; ++mp) {
             double c = dots_host(h, n, {Wc(mp)}, Wc(m))[0];
@@ -1053,7 +1066,14 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
                 h->retained.push_back(r);
                 ev.action = 2;
             }
-            if (q_live > 0) {
+            if (shrink) {
+                // block-size reduction: u_{j+p} = 0 is not added; lane m is removed from
+                // block b+1 on
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Wc(m), 0.0);
+                ev.action = ev.kind == 1 ? 5 : 4;
+                absent_from[m] = b + 1;
+                absent_changed = true;
+            } else if (q_live > 0) {
                 // replacement: pool vector (already orthogonal to u_1..u_{j+p-1}),
                 // orthogonalised twice more against retained + window, normalised
                 std::vector<Col> src = {Col{h->pool + q_first, qc}};
@@ -1099,6 +1119,8 @@ void slow_block(bminres_ctx* h, long long n, int p, long long b, double tau, lon
         if (stop_after) break;
     }
     CK(cudaStreamSynchronize(h->stream));
+    if (absent_changed)
+        h2d(h, (char*)h->st + offsetof(DevState, absent_from), absent_from.data(), MAXP * sizeof(long long));
     h2d(h, (char*)h->st + offsetof(DevState, Ck) + par * MAXP * MAXP * sizeof(double), Ck.data(),
         MAXP * MAXP * sizeof(double));
     SET_STATE(h, q_first, q_first);
@@ -1489,6 +1511,8 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     init.red2_fac = h->red2_fac ? 1 : 0;
     init.fac_bad = 0;
     init.given_blk = -1;
+    init.policy = o.policy;
+    for (int c = 0; c < MAXP; ++c) init.absent_from[c] = KINF;
     init.k_upd_min = KINF;
     init.upd_last = 0;
     // timeline tracing (tooling): BMINRES_TRACE=<launch number> records that launch of every
@@ -1573,9 +1597,10 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
                     e.j = 0;
                     e.col = i + 1;
                     e.kind = (int)ev[2 * i + 1];
-                    e.action = 1;
+                    e.action = o.policy == 1 ? 4 : 1;   // removed (shrink) / replaced
                     e.ratio = ev[2 * i];
                     h->events.push_back(e);
+                    if (o.policy == 1) init.absent_from[i] = 1;
                 }
         }
         for (int i = 0; i < ((fast || coop) ? 0 : p); ++i) {
@@ -1594,7 +1619,20 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
             CK(cudaStreamSynchronize(h->stream));
             const double hh = std::sqrt(c2[2 * MAXP + (i & 1)]);
             for (int l = 0; l < i; ++l) S[l * MAXP + i] = c2[l] + c2[MAXP + l];
-            if (hh <= tau * f0n[i]) {
+            if (hh <= tau * f0n[i] && o.policy == 1) {
+                // shrink: the dependent start column is removed -- u_i = 0
+                bminres_event ev{};
+                ev.j = 0;
+                ev.col = i + 1;
+                ev.kind = hh <= 1e-12 * f0n[i] ? 0 : 1;
+                ev.action = 4;
+                ev.ratio = f0n[i] > 0 ? hh / f0n[i] : 0.0;
+                h->events.push_back(ev);
+                S[i * MAXP + i] = 0.0;
+                init.absent_from[i] = 1;
+                launch_axpy(h, n, {}, nullptr, nullptr, 1.0, Col{F + i, p}, 0.0);
+                pend = -1;
+            } else if (hh <= tau * f0n[i]) {
                 bminres_event ev{};
                 ev.j = 0;
                 ev.col = i + 1;
@@ -1875,8 +1913,8 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
         g_create_err = "split_spmm must be 0 (auto), 1 (always) or 2 (never)";
         return BMINRES_EINVAL;
     }
-    if (o.policy != 0) {
-        g_create_err = "policy: only 0 (replacement, P:690-729) is built";
+    if (o.policy != 0 && o.policy != 1) {
+        g_create_err = "policy must be 0 (replacement, P:690-729) or 1 (block-size reduction, P:582-688)";
         return BMINRES_EINVAL;
     }
     if (o.coeff_mode != 0) {

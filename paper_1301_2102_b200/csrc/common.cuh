@@ -89,6 +89,12 @@ struct DevState {
     // coef_k in the state, and K1(k+1)'s fragments of Tr_{k+1} and -(Tr_k C_k^T) below; fac_bad:
     // breakdown / cancellation of the block (published as by K1's own prologue)
     int red2_fac, fac_bad;
+    // block-size reduction ("shrink", policy 1): lane m of every block
+    // >= absent_from[m] holds a removed (zero) basis vector -- A 0 = 0, so a removed lane stays
+    // removed; KINF: present.  The block form keeps p columns; removed ones are zero.
+    int policy;
+    int pad_policy;
+    long long absent_from[MAXP];
     double fT[MAXP * MAXP], fD[MAXP * MAXP];
     // ---- written by the main branch, double-buffered by block parity
     double G[2][MAXP * MAXP];      // G(a,m) = u_{(k-1)p+a}^T w_m (K1, after the known subtraction)
@@ -132,6 +138,15 @@ struct DevState {
     unsigned* trace_tick;
     long long trace_launch;
 };
+
+// lanes whose basis vector of block blk was removed (shrink policy), bit m = lane m
+__device__ __forceinline__ unsigned absent_mask(const DevState* st, long long blk, int P) {
+    unsigned m = 0u;
+    if (st->policy == 1)
+        for (int l = 0; l < P; ++l)
+            if (st->absent_from[l] <= blk) m |= 1u << l;
+    return m;
+}
 
 // kernel types of the trace buffer
 enum TraceKind { TR_K1 = 0, TR_RED1, TR_K2, TR_RED2, TR_K3B, TR_K4B, TR_K1A, TR_NKIND };
@@ -360,7 +375,10 @@ __global__ void __launch_bounds__(256) k_reduce(DevState* st, int which, int par
 // row m of L^{-1} = (e_m - sum_{i<m} L(m,i) L^{-1}(i,:)) r_m needs only rows < m of C.
 template <int P>
 __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, int Q, double tau, double* sC,
-                             double* sCi, double* sCo) {
+                             double* sCi, double* sCo, unsigned amask = 0u) {
+    // amask (shrink policy): lanes whose candidate is a removed (zero) vector.  Their pivot is a
+    // placeholder 1 (C' = C + e_m e_m^T, so Tr = C'^{-1} keeps the zero column zero) and no
+    // dependence test applies; sC returns the true C (diagonal 0 there: h_{j+p,j} = 0)
     __shared__ int s_bad;
     const int tid = threadIdx.x, lane = tid & 31;
     if constexpr (P <= 16) {
@@ -377,9 +395,10 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
             bool bad = false;
 #pragma unroll
             for (int m = 0; m < P; ++m) {
-                const double dm = __shfl_sync(FULL, g[m], m);
+                const bool gone = (amask >> m) & 1u;
+                const double dm = gone ? 1.0 : __shfl_sync(FULL, g[m], m);
                 const double d0m = __shfl_sync(FULL, d0, m);
-                if (!(dm > tau2 * sOm[m]) || !(dm >= 1e-4 * d0m)) {
+                if (!gone && (!(dm > tau2 * sOm[m]) || !(dm >= 1e-4 * d0m))) {
                     bad = true;
                     break;
                 }
@@ -410,6 +429,8 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
                     for (int r = 0; r < P; ++r) sCi[r * P + lane] = x[r];
                 for (int t = lane; t < P * MAXQ; t += 32) sCo[t] = 0.0;
                 __syncwarp();
+                if (own && ((amask >> lane) & 1u)) sC[lane * P + lane] = 0.0;   // the true C
+                __syncwarp();
                 for (int t = lane; t < P * Q; t += 32) {
                     const int m = t % P, q = t / P;
                     double s = 0.0;
@@ -434,9 +455,10 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
         __syncwarp();
         bool bad = false;
         for (int m = 0; m < P; ++m) {
-            const double d = sG[m * P + m];
+            const bool gone = (amask >> m) & 1u;
+            const double d = gone ? 1.0 : sG[m * P + m];
             const double dm0 = __shfl_sync(FULL, d0[m / 32], m % 32);
-            if (!(d > tau2 * sOm[m]) || !(d >= 1e-4 * dm0)) {
+            if (!gone && (!(d > tau2 * sOm[m]) || !(d >= 1e-4 * dm0))) {
                 bad = true;
                 break;
             }
@@ -464,6 +486,10 @@ __device__ bool factor_block(double* sG, const double* sOm, const double* sPd, i
                 for (int c = 0; c <= m; ++c) s = fma(sCi[c * P + m], sPd[q * P + c], s);
                 sCo[m * MAXQ + q] = s;
             }
+        __syncwarp();
+        if (!bad)
+            for (int m = lane; m < P; m += 32)
+                if ((amask >> m) & 1u) sC[m * P + m] = 0.0;   // the true C
     }
     __syncthreads();
     return s_bad != 0;
@@ -551,7 +577,7 @@ __device__ bool k1_prologue(DevState* st, int par, int sk, double* sTk, double* 
         for (int t = threadIdx.x; t < P * P + Q * P; t += blockDim.x) sRed[t] = st->red2[pp][t];
         for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[pp][t];
         __syncthreads();
-        if (factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo)) {
+        if (factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo, absent_mask(st, k, P))) {
             if (blockIdx.x == 0 && threadIdx.x == 0) publish_breakdown(st, k - 1);
             return false;
         }
@@ -587,7 +613,7 @@ __device__ void red2_factor(DevState* st, int par, double* sm, unsigned long lon
     for (int t = threadIdx.x; t < P; t += blockDim.x) sOm[t] = st->om2[par][t];
     load_pp<P>(sTp, st->Tr[sk]);                 // Tr_k
     __syncthreads();
-    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo);
+    const bool bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sC, sCi, sCo, absent_mask(st, k + 1, P));
     if (bad) {
         if (threadIdx.x == 0) {
             st->fac_bad = 1;

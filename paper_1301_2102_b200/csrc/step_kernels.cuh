@@ -481,8 +481,11 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     __shared__ long long s_k, s_jd, s_maxit, s_hcap;
     __shared__ double s_tol;
     __shared__ int s_valid, s_stop_after, s_mlast, s_stop, s_given;
+    __shared__ unsigned s_am_k, s_am_k1;   // shrink policy: removed lanes of blocks k and k+1
     if (tid == 0) {
         const long long k = st->k_side;
+        s_am_k = absent_mask(st, k, P);
+        s_am_k1 = absent_mask(st, k + 1, P);
         s_valid = (k < st->stop_side_at) && (k < st->bd_at);
         s_given = st->given_blk == k;
         s_k = k;
@@ -527,7 +530,8 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             for (int t = tid; t < P * P + Q * P; t += K3T) sRed[t] = st->red2[par][t];
             for (int t = tid; t < P; t += K3T) sOm[t] = st->om2[par][t];
             __syncthreads();
-            bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sCc, sOm + P, sOm + P + P * P);
+            bad = factor_block<P>(sRed, sOm, sRed + P * P, Q, st->tau, sCc, sOm + P, sOm + P + P * P,
+                                  absent_mask(st, k + 1, P));
         }
         if (bad) {   // breakdown of block k: the host runs the column path, then re-runs this block
             if (tid == 0) {
@@ -598,13 +602,29 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         const double tol = s_tol;
         // ---- phase B: generate reflector j, apply it to the later columns and to [T; 0]
         //      (row 1 -> z_j^T), residuals, stop test (Alg. 2)
-        int m_last = -1, stop = 0;  // 1 converged, 2 maxit, 3 singular R, 4 pool exhausted
+        // 1 converged, 2 maxit, 3 singular R, 4 pool exhausted, 5 basis exhausted (shrink)
+        int m_last = -1, stop = 0;
+        const unsigned am_k = s_am_k, am_k1 = s_am_k1;
         for (int m = 0; m < P; ++m) {
             const long long j = j0 + m;
             if (j > maxit) {
                 stop = 2;
                 break;
             }
+            // shrink: every index of the window j .. j+p-1 removed -> the basis is exhausted
+            // (lanes >= m of this block, lanes < m of the next)
+            if (am_k | am_k1) {
+                const unsigned all = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
+                const unsigned lo = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+                if ((((am_k & ~lo) | (am_k1 & lo)) & all) == all) {
+                    stop = 5;
+                    break;
+                }
+            }
+            // shrink: u_j removed -> column j of \bar H is deleted: identity reflector,
+            // R column zero (placeholder 1 on the diagonal for R_kk^{-1}), z_j = the tail's first
+            // (zero) row, m_j = 0
+            const bool gone = (am_k >> m) & 1u;
             const int o = 2 * P + m;
             const double alpha = sH[o * LD + m];
             double x2 = 0.0;
@@ -614,7 +634,11 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
             // v = x/(alpha - beta); one reciprocal 1/(beta (alpha - beta)) serves both quotients
             double tj, beta, scl;
-            if (xnorm == 0.0) {
+            if (gone) {
+                tj = 0.0;
+                beta = 1.0;
+                scl = 0.0;
+            } else if (xnorm == 0.0) {
                 tj = 0.0;
                 beta = alpha;
                 scl = 0.0;
@@ -625,7 +649,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 tj = -s * s * inv;
                 scl = beta * inv;
             }
-            if (fabs(beta) <= DBL_EPSILON * sHn[m]) {
+            if (!gone && fabs(beta) <= DBL_EPSILON * sHn[m]) {
                 stop = 3;
                 break;
             }
@@ -767,7 +791,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         int status = 1;
         bool end = false;
         if (stop == 1) { status = 0; end = true; }
-        else if (stop == 2) { status = 1; end = true; }
+        else if (stop == 2 || stop == 5) { status = 1; end = true; }
         else if (stop == 3) { status = -6; end = true; }
         else if (stop == 4) { status = -5; end = true; }
         else if (jd >= maxit) { status = 1; end = true; }
