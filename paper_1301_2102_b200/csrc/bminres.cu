@@ -48,6 +48,9 @@ struct Kfn {  // per-p kernel table
     size_t smem1pre;
     void (*k1u)(K1Args);     // split mode, p >= 16: the M/X update of block k-2 as its own kernel
     size_t smem1u;
+    void (*k1ws)(K1Args);    // large panels, p >= 16: the warp-specialised K1 (SpMM + epilogue, one kernel)
+    size_t smem1ws;
+    int nt1ws;
     // start block / exit residual: Gram, V R^{-1}, plain SpMM (DMMA / K1a versions for p = 8, 16, 32)
     void (*red2f)(DevState*, int, int);   // reduce2 + factorisation for the DMMA K1 (null: k_reduce)
     void (*fac2)(DevState*, int);         // row partition: the factorisation after the allreduce
@@ -71,6 +74,9 @@ Kfn make_kfn(int q) {
     f.smem1pre = 0;
     f.k1u = nullptr;
     f.smem1u = 0;
+    f.k1ws = nullptr;
+    f.smem1ws = 0;
+    f.nt1ws = 0;
     f.red2f = nullptr;
     f.fac2 = nullptr;
     f.gram = k_gram;
@@ -102,6 +108,9 @@ Kfn make_kfn(int q) {
             if constexpr (P >= 16) {
                 f.k1u = k1u_update<P>;
                 f.smem1u = UpdB<P>::bytes;
+                f.k1ws = k1_ws<P>;
+                f.smem1ws = K1WS<P>::bytes;
+                f.nt1ws = K1WS<P>::THREADS;
             }
             f.k2 = k2_dmma<P>;
             f.smem2 = K2DSmem<P>::bytes;
@@ -216,6 +225,7 @@ struct bminres_ctx {
     // split mode: K1a (SpMM alone, full occupancy) -> AV, then K1<P, true>
     bool split = false;
     bool upd_sep = false;    // split mode: the M/X update of block k-2 runs as k1u_update before K1a(k)
+    bool ws = false;         // split mode, single rank: K1 = k1_ws (no K1a, no A V_k panel)
     bool red2_fac = false;   // reduce2 factors the new block once (k_red2f)
     bool xdefer = false;   // fused updates defer X in pairs
     int nb1a = 0;
@@ -481,6 +491,13 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         const int o1p = std::min(cap, occ_of((const void*)h->kf.k1pre, h->kf.nt1, h->kf.smem1pre));
         h->nb1 = (std::min(NB_MAX, h->n_sm * o1p) - (o1p > 1 ? h->csz : 0)) / h->csz * h->csz;
     }
+    // BMINRES_WS (experiment): the warp-specialised K1 in place of K1a + K1 on a single rank (a row
+    // partition keeps the split pair: its K1a overlaps the halo exchange with the interior rows).
+    // Measured (one B200): config 4 6.58 ms vs the pair's 2.88 + 3.54 ms, config 5 2.48 ms vs
+    // 1.36 + 0.34 ms -- eight producer warps per SM keep fewer gathers in flight than K1a's forty
+    // (twelve: the consumers spill at 128 registers), so the pair stays the default
+    h->ws = h->split && h->kf.k1ws && !h->tp && getenv("BMINRES_WS") != nullptr;
+    if (h->ws) h->nb1 = h->n_sm / h->csz * h->csz;
     (void)cluster_grid;
 
 }
@@ -785,6 +802,19 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
         if (upd_branch) CK(cudaEventRecord(h->ev_u1, us));
         a.fuse = 0;
         fuse = 0;
+    }
+    if (h->ws) {
+        // one kernel: gathers (producer warps) + DMMA epilogue (consumer warps)
+        if (upd_branch) CK(cudaStreamWaitEvent(s, h->ev_u1, 0));   // the update read V_{k-2}
+        {
+            TimeMark tm(h, PH_SPMM);
+            cudaStream_t keep = h->stream;
+            h->stream = s;
+            launch_cluster(h, h->kf.k1ws, h->nb1, h->kf.nt1ws, h->kf.smem1ws, a, "k1_ws");
+            h->stream = keep;
+        }
+        launch_reduce(h, s, 1, k);
+        return;
     }
     if (h->split) {
         // K1a: AV = A V_k (PDL after reduce2 / K2), then K1 streams AV
@@ -1962,6 +1992,9 @@ int bminres_create(const bminres_options* opt, bminres_handle* out) {
             if (f.k1u)
                 CK(cudaFuncSetAttribute((const void*)f.k1u, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)f.smem1u));
+            if (f.k1ws)
+                CK(cudaFuncSetAttribute((const void*)f.k1ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)f.smem1ws));
             CK(cudaFuncSetAttribute((const void*)f.k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem2));
             CK(cudaFuncSetAttribute((const void*)f.k3b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem3));
             CK(cudaFuncSetAttribute((const void*)f.k4b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem4b));

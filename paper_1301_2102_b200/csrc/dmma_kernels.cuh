@@ -1298,4 +1298,334 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
     trace_pt(tr, 5);
 }
 
+// ------------------------------------------------------------------ K1, warp-specialised (large panels)
+//
+// Row a1 for large panels (p in {16, 32}) in ONE kernel instead of K1a + K1<P, true>: per CTA,
+// NPW producer warps run the SpMM gathers (A V_k, each row summed in CSR order with fma from 0 --
+// bitwise K1a's rows) into a ring of NSLOT shared-memory tiles of T rows, and NCW consumer warps run
+// the DMMA epilogue on them (W = (A V_k) Tr_k - V_{k-1} D, ||A u_j||^2, V_k^T W; per output the same
+// DMMA order as K1<P, true>, so W is bitwise the split mode's), register-blocked 16 rows per warp.
+// The A V_k panel never goes to HBM (split mode wrote it and read it back: 2 panels per block
+// step), and the latency-bound gathers overlap the tensor-pipe-bound epilogue.  Producers and
+// consumers hand tiles over with named barriers (FULL / EMPTY per slot, bar.arrive + bar.sync).
+// Tiles are dealt round-robin over the CTAs, so all SMs sweep the rows together and the far
+// stencil neighbours (z planes at config 4) are re-read from L2.
+template <int P>
+struct K1WS {
+#ifndef K1WS_NPW
+#define K1WS_NPW 8   // (12 producers: 128 registers per thread, the consumers spill -- config 4 9.2 ms)
+#endif
+    static constexpr int NPW = K1WS_NPW, NCW = 4;
+    static constexpr int THREADS = (NPW + NCW) * 32;
+    static constexpr int TRW = 16, MC = TRW / 8;       // rows per consumer warp (two DMMA row chunks)
+    static constexpr int T = NCW * TRW;                // rows per CTA tile
+    static constexpr int RS = P + 4;
+    static constexpr int NSLOT = 3, NSC = 2;           // A V_k ring slots; consumer cp.async stages
+    static constexpr int VEC = 4, LANES = P / VEC, RPW = 32 / LANES, CH = 8;
+    static constexpr int FR = DM<P>::FR;
+    static constexpr int ring = NSLOT * T * RS;
+    static constexpr int stage = NCW * NSC * 2 * TRW * RS;   // V_k, V_{k-1} rows of each consumer warp
+    static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
+    static constexpr int body = ring + stage > scr ? ring + stage : scr;
+    static constexpr size_t bytes = sizeof(double) * (2 * FR + body + P * P + P);
+};
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(K1WS<P>::THREADS, 1) k1_ws(K1Args a) {
+    using S = K1WS<P>;
+    using D = DM<P>;
+    constexpr int NPW = S::NPW, NCW = S::NCW, TH = S::THREADS, TRW = S::TRW, MC = S::MC, T = S::T, RS = S::RS;
+    constexpr int NSLOT = S::NSLOT, NSC = S::NSC, VEC = S::VEC, LANES = S::LANES, RPW = S::RPW, CH = S::CH;
+    constexpr int KC = D::KC, NC = D::NC, FR = D::FR, E = P * P + P;
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + NSLOT;
+    DevState* st = a.st;
+    unsigned long long* tr = trace_begin(st, TR_K1);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    extern __shared__ __align__(16) double dynws[];
+    double* fT = dynws;             // Tr_k in fragment order
+    double* fD = fT + FR;           // -(Tr_{k-1} C_{k-1}^T)
+    double* ring = fD + FR;         // NSLOT x T x RS: A V_k rows, overwritten by W rows
+    double* stg = ring + S::ring;   // consumer staging
+    double* sAcc = fD + FR + S::body;
+    if (!st->run_main) return;
+    pdl_wait();   // V_k (K2 of block k-1), the reduce2 totals / fragments, the update kernel are complete
+    trace_pt(tr, 2);
+    const bool has_prev = st->k_main > 1;
+    // ---- prologue (all threads): C_{k-1}, Tr_k, D (the scratch overlays the ring)
+    {
+        if (st->red2_fac && st->k_main > 1 && st->given_blk != st->k_main - 1) {
+            if (st->fac_bad) return;
+            for (int t = threadIdx.x; t < FR; t += blockDim.x) {
+                fT[t] = st->fT[t];
+                fD[t] = st->fD[t];
+            }
+        } else {
+            double* sTk = ring;
+            double* sD = ring + P * P;
+            if (!k1_prologue<P>(st, a.par, a.sk, sTk, sD, ring + 2 * P * P)) return;
+            to_frag<P>(sTk, P, 1.0, fT);
+            to_frag<P>(sD, P, -1.0, fD);
+        }
+        __syncthreads();
+    }
+    trace_pt(tr, 3);
+    const long long ntiles = (a.n + T - 1) / T;
+    double g[NC][NC][2], om[NC][2];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+        om[i][0] = om[i][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    }
+    if (warp < NPW) {
+        // ================= producers: A V_k rows of each tile into the ring.  A warp walks its row
+        // groups (G per tile, tiles round-robin over the CTAs) as one stream with a software
+        // pipeline: while group q's gathers are in flight, the column indices / values of group
+        // q+1 and the row pointers of group q+2 are loaded (one dependent round trip per group
+        // instead of three).  The slot's EMPTY barrier is taken just before the first store.
+        const int sub = lane % LANES, rsub = lane / LANES;
+        const int c0 = sub * VEC;
+        constexpr int NG = T / RPW;   // row groups per tile
+        const int G = warp < NG ? (NG - warp + NPW - 1) / NPW : 0;   // this warp's groups per tile
+        const long long my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const long long nq = my_tiles * G;
+        if (G == 0)   // (no rows in a tile: the barriers only)
+            for (long long it = 0; it < my_tiles; ++it) {
+                const int s = (int)(it % NSLOT);
+                if (it >= NSLOT) named_sync(BAR_EMPTY + s, TH);
+                named_arrive(BAR_FULL + s, TH);
+            }
+        auto row_of = [&](long long q) -> long long {
+            const long long it = q / G;
+            const int gi = (int)(q % G);
+            return (blockIdx.x + it * gridDim.x) * T + (warp + gi * NPW) * RPW + rsub;
+        };
+        auto load_rp = [&](long long q, int& r0, int& r1) {
+            r0 = r1 = 0;
+            if (q < nq) {
+                const long long i = row_of(q);
+                if (i < a.n) {
+                    r0 = __ldg(a.rowptr + i);
+                    r1 = __ldg(a.rowptr + i + 1);
+                }
+            }
+        };
+        auto load_cv = [&](int r0, int r1, int (&c)[CH], double (&v)[CH]) {
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                const bool pr = r0 + t < r1;
+                c[t] = pr ? __ldg(a.col + r0 + t) : -1;
+                v[t] = pr ? __ldg(a.val + r0 + t) : 0.0;
+            }
+        };
+        int k0 = 0, k1 = 0, rn0 = 0, rn1 = 0;
+        int cc[CH];
+        double avv[CH];
+        load_rp(0, k0, k1);
+        load_rp(1, rn0, rn1);
+        load_cv(k0, k1, cc, avv);
+        for (long long q = 0; q < nq; ++q) {
+            const long long it = q / G;
+            const int gi = (int)(q % G);
+            const int s = (int)(it % NSLOT);
+            double xv[CH][VEC];
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                if (cc[t] >= 0) {
+                    ldg_vec<VEC>(a.X + (long long)cc[t] * P + c0, xv[t]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
+                }
+            }
+            const int gk0 = k0, gk1 = k1;
+            k0 = rn0;
+            k1 = rn1;
+            int cn[CH];
+            double an[CH];
+            load_cv(k0, k1, cn, an);
+            load_rp(q + 2, rn0, rn1);
+            double acc[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+#pragma unroll
+            for (int t = 0; t < CH; ++t)
+                if (cc[t] >= 0) {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fma(avv[t], xv[t][v], acc[v]);
+                }
+            // rows longer than CH entries: the remaining chunks, in CSR order
+            for (int kb = gk0 + CH; __any_sync(FULL, kb < gk1); kb += CH) {
+                int c2[CH];
+                double a2[CH];
+                load_cv(kb, gk1, c2, a2);
+#pragma unroll
+                for (int t = 0; t < CH; ++t) {
+                    if (c2[t] >= 0) {
+                        ldg_vec<VEC>(a.X + (long long)c2[t] * P + c0, xv[t]);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] = fma(a2[t], xv[t][v], acc[v]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                cc[t] = cn[t];
+                avv[t] = an[t];
+            }
+            if (gi == 0 && it >= NSLOT) named_sync(BAR_EMPTY + s, TH);
+            double* tl = ring + s * T * RS;
+            const int rl = (warp + gi * NPW) * RPW + rsub;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) tl[rl * RS + c0 + v] = acc[v];   // (rows past n: zeros)
+            if (gi == G - 1) named_arrive(BAR_FULL + s, TH);
+        }
+        // complete the EMPTY barriers of the last slots (every arrival gets its matching sync)
+        for (long long q = my_tiles > NSLOT ? my_tiles - NSLOT : 0; q < my_tiles; ++q)
+            named_sync(BAR_EMPTY + (int)(q % NSLOT), TH);
+    } else {
+        // ================= consumers: the DMMA epilogue on their 16 rows of each tile
+        const int cw = warp - NPW;
+        const int fr = lane >> 2, fc = lane & 3;
+        double* wst = stg + cw * NSC * 2 * TRW * RS;
+        auto issue = [&](long long itn) {
+            const long long t = blockIdx.x + itn * gridDim.x;
+            if (t < ntiles) {
+                double* sl = wst + (int)(itn % NSC) * 2 * TRW * RS;
+                const long long base = t * T + cw * TRW;
+                stage_rows<P, TRW>(sl, a.X, base, a.n, lane);
+                if (has_prev) stage_rows<P, TRW>(sl + TRW * RS, a.Vprev, base, a.n, lane);
+            }
+            cp_commit();
+        };
+#pragma unroll
+        for (int q = 0; q < NSC - 1; ++q) issue(q);
+        long long it = 0;
+        for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            issue(it + NSC - 1);
+            cp_wait<NSC - 1>();
+            __syncwarp();
+            const int s = (int)(it % NSLOT);
+            named_sync(BAR_FULL + s, TH);
+            const double* tV = wst + (int)(it % NSC) * 2 * TRW * RS;
+            const double* tP = tV + TRW * RS;
+            double* tW = ring + s * T * RS + cw * TRW * RS;   // A V_k rows in, W rows out
+            const long long base = t * T + cw * TRW;
+            double w[MC][NC][2];
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc)
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) w[mc][nc][0] = w[mc][nc][1] = 0.0;
+            // W = (A V_k) Tr_k (Tr_k upper triangular: k-chunks below the column block are zero)
+#pragma unroll
+            for (int kc = 0; kc < KC; ++kc) {
+                double av[MC];
+#pragma unroll
+                for (int mc = 0; mc < MC; ++mc) av[mc] = tW[(mc * 8 + fr) * RS + kc * 4 + fc];
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc)
+                    if (kc <= 2 * nc + 1) {
+                        const double b = fT[(kc * NC + nc) * 32 + lane];
+#pragma unroll
+                        for (int mc = 0; mc < MC; ++mc) dmma(w[mc][nc][0], w[mc][nc][1], av[mc], b);
+                    }
+            }
+            // ||A u_j||^2 (C14)
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc)
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    om[nc][0] = fma(w[mc][nc][0], w[mc][nc][0], om[nc][0]);
+                    om[nc][1] = fma(w[mc][nc][1], w[mc][nc][1], om[nc][1]);
+                }
+            // W -= U_{k-1} C_{k-1}^T = V_{k-1} D (h_{i,j} = h_{j,i})
+            if (has_prev) {
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc) {
+                    double ap[MC];
+#pragma unroll
+                    for (int mc = 0; mc < MC; ++mc) ap[mc] = tP[(mc * 8 + fr) * RS + kc * 4 + fc];
+#pragma unroll
+                    for (int nc = 0; nc < NC; ++nc) {
+                        const double b = fD[(kc * NC + nc) * 32 + lane];
+#pragma unroll
+                        for (int mc = 0; mc < MC; ++mc) dmma(w[mc][nc][0], w[mc][nc][1], ap[mc], b);
+                    }
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int mc = 0; mc < MC; ++mc) {
+                const long long row = base + mc * 8 + fr;
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    const int col = nc * 8 + 2 * fc;
+                    tW[(mc * 8 + fr) * RS + col] = w[mc][nc][0];
+                    tW[(mc * 8 + fr) * RS + col + 1] = w[mc][nc][1];
+                    if (row < a.n) *reinterpret_cast<double2*>(a.Y + row * P + col) = make_double2(w[mc][nc][0], w[mc][nc][1]);
+                }
+            }
+            __syncwarp();
+            // V_k^T W over the warp's rows (rows past n are zero in both tiles)
+#pragma unroll
+            for (int k0 = 0; k0 < TRW; k0 += 4) {
+                const double* rv = tV + (k0 + fc) * RS;
+                const double* rw = tW + (k0 + fc) * RS;
+                double bw[NC];
+#pragma unroll
+                for (int j = 0; j < NC; ++j) bw[j] = rw[j * 8 + fr];
+#pragma unroll
+                for (int i = 0; i < NC; ++i) {
+                    const double av = rv[i * 8 + fr];
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) dmma(g[i][j][0], g[i][j][1], av, bw[j]);
+                }
+            }
+            __syncwarp();
+            named_arrive(BAR_EMPTY + s, TH);
+        }
+        cp_wait<0>();
+    }
+    trace_pt(tr, 4);
+    pdl_trigger();   // the dependent (reduce1) launches while this grid reduces its partials
+    __syncthreads();
+    if (warp >= NPW) {
+        // om: sum over the 8 row-lanes that share a column pair
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
+                om[nc][0] += __shfl_xor_sync(FULL, om[nc][0], o);
+                om[nc][1] += __shfl_xor_sync(FULL, om[nc][1], o);
+            }
+    }
+    // consumer warps in fixed order -> sAcc (the ring is idle now)
+    for (int w2 = NPW; w2 < NPW + NCW; ++w2) {
+        if (warp == w2) {
+#pragma unroll
+            for (int i = 0; i < NC; ++i)
+#pragma unroll
+                for (int j = 0; j < NC; ++j) frag_acc(sAcc, 0, P, i * 8, j * 8, g[i][j], w2 == NPW, lane);
+            if ((lane >> 2) == 0) {
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc) {
+                    double* d = sAcc + P * P + nc * 8 + 2 * (lane & 3);
+                    d[0] = (w2 == NPW ? 0.0 : d[0]) + om[nc][0];
+                    d[1] = (w2 == NPW ? 0.0 : d[1]) + om[nc][1];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    cluster_partials(sAcc, E, st->part1);   // reduce1, then K2 forms G = Tr_k^T (V_k^T W)
+    trace_pt(tr, 5);
+}
+
 }  // namespace bmr

@@ -111,10 +111,11 @@ def test_history_parity_small(p):
 
 
 @pytest.mark.parametrize("p", [8, 16, 32])
-def test_split_mode_bitwise(p):
+def test_split_mode_bitwise(p, monkeypatch):
     """Split mode (K1a computes A V_k alone, K1 streams it) sums every row
     in the same CSR order as the fused K1's gathers: graph, plain-launch and timing-mode solves are
-    bitwise identical to the fused path, and match the oracle (ragged tail: n = 40*37 rows)."""
+    bitwise identical to the fused path, and match the oracle (ragged tail: n = 40*37 rows).
+    (the warp-specialised K1, an option: test_warp_specialised_k1)"""
     A = synth.laplacian_2d(40, 37, shift=1.7)
     B = synth.gaussian_rhs(A.n, p, seed=p)
     base = gpu_solve(A, B, tol=0.0, maxit=120, split_spmm=2)
@@ -131,6 +132,32 @@ def test_split_mode_bitwise(p):
             # p >= 16: the M/X update runs as its own register-blocked kernel (k1u_update), bitwise
             # the fused update of the other mode
             assert (r.stats["phase_launches"]["update_main"] > 0) == (p >= 16)
+
+
+@pytest.mark.parametrize("p", [16, 32])
+def test_warp_specialised_k1(p):
+    """The warp-specialised K1 (k1_ws: gathers in producer warps, the DMMA epilogue in consumer
+    warps, no A V_k panel) in split mode: W per row is bitwise the split pair's (same CSR order, same
+    DMMA order per output); the Gram partials are summed over a different row partition, so the
+    solve equals the K1a + K1 pair to rounding and the oracle to the parity bar -- graphs, plain
+    launches and timing mode (where it is the only K1 launch kind)."""
+    import os
+    A = synth.laplacian_2d(40, 37, shift=1.7)
+    B = synth.gaussian_rhs(A.n, p, seed=p)
+    ref = oracle.solve(A, B, tol=0.0, maxit=120)
+    pair = gpu_solve(A, B, tol=0.0, maxit=120, split_spmm=1)
+    for kw in (dict(use_graphs=True), dict(use_graphs=False), dict(use_graphs=False, timing=True)):
+        os.environ["BMINRES_WS"] = "1"   # (an option: measured slower than the K1a + K1 pair)
+        try:
+            r = gpu_solve(A, B, tol=0.0, maxit=120, split_spmm=1, **kw)
+        finally:
+            del os.environ["BMINRES_WS"]
+        assert r.iterations == 120
+        assert_hist_close(r.history, ref.history)
+        np.testing.assert_allclose(r.history, pair.history, rtol=1e-11, atol=1e-15)
+        np.testing.assert_allclose(r.X, ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+        if kw.get("timing"):
+            assert r.stats["phase_launches"]["spmm"] > 0 and r.stats["phase_launches"]["spmm_av"] == 0
 
 
 @pytest.mark.parametrize("p,maxit", [(8, 120), (8, 128), (16, 144), (32, 160)])
