@@ -82,6 +82,20 @@ def lib():
         _lib.orc_house_gen.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_house_apply.restype = None
         _lib.orc_house_apply.argtypes = [C.c_int32, C.c_void_p, C.c_double, C.c_void_p]
+        _lib.orc_ic0.restype = C.c_int
+        _lib.orc_ic0.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.POINTER(C.c_int64)]
+        _lib.orc_trsv_lower.restype = None
+        _lib.orc_trsv_lower.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_trsv_upper.restype = None
+        _lib.orc_trsv_upper.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_prec_op_block.restype = None
+        _lib.orc_prec_op_block.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        _lib.orc_solve_prec.restype = C.c_int
+        _lib.orc_solve_prec.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Config), C.POINTER(Result),
+                                        C.c_void_p]
     return _lib
 
 
@@ -101,6 +115,7 @@ class OracleResult:
     dbg: dict = field(default_factory=dict)
     start_s: float = 0.0           # wall time of the start block + pool (instrumentation)
     loop_s: float = 0.0            # wall time of the iteration loop (instrumentation)
+    ptrue_res: np.ndarray | None = None   # preconditioned solves: unpreconditioned ||b - A x|| / ||b||
 
     @property
     def status_name(self) -> str:
@@ -108,9 +123,12 @@ class OracleResult:
 
 
 def solve(A, B, *, tol=1e-8, maxit=100, tau=1e-8, seed=0, pool_size=1, X0=None,
-          history=True, events_cap=4096, debug_iters=0, policy=0) -> OracleResult:
+          history=True, events_cap=4096, debug_iters=0, policy=0, prec=None) -> OracleResult:
     """Run the oracle.  A: synth.Csr; B: n×p float64 (row-major).  policy: 0 replacement
-    (P:690-729), 1 block-size reduction "shrink"."""
+    (P:690-729), 1 block-size reduction "shrink".  prec: an IC(0) factor L (from
+    ``ic0``) -- the split-preconditioned solve of reading R8 (f3): the method on
+    L^-1 A L^-T with Rhat_0 = L^-1 (B - A X0), X = X0 + L^-T Yhat; history / comp_res / true_res are
+    the preconditioned residuals (relative to ||Rhat_0||), ptrue_res the unpreconditioned one."""
     B = np.ascontiguousarray(B, dtype=np.float64)
     n, p = B.shape
     indptr = np.ascontiguousarray(A.indptr, dtype=np.int32)
@@ -134,7 +152,16 @@ def solve(A, B, *, tol=1e-8, maxit=100, tau=1e-8, seed=0, pool_size=1, X0=None,
         cfg.dbg_U, cfg.dbg_H, cfg.dbg_R = _ptr(dbg["U"]).value, _ptr(dbg["H"]).value, _ptr(dbg["R"]).value
         cfg.dbg_M, cfg.dbg_Z, cfg.dbg_S = _ptr(dbg["M"]).value, _ptr(dbg["Z"]).value, _ptr(dbg["S"]).value
     res = Result()
-    lib().orc_solve(n, _ptr(indptr), _ptr(indices), _ptr(data), _ptr(B), _ptr(X), C.byref(cfg), C.byref(res))
+    ptrue = None
+    if prec is None:
+        lib().orc_solve(n, _ptr(indptr), _ptr(indices), _ptr(data), _ptr(B), _ptr(X), C.byref(cfg), C.byref(res))
+    else:
+        if debug_iters:
+            raise ValueError("debug dumps are not kept for preconditioned solves")
+        Lp, Li, Lx = _csr_arrays(prec)
+        ptrue = np.zeros(p)
+        lib().orc_solve_prec(n, _ptr(indptr), _ptr(indices), _ptr(data), _ptr(Lp), _ptr(Li), _ptr(Lx), _ptr(B),
+                             _ptr(X), C.byref(cfg), C.byref(res), _ptr(ptrue))
     it = int(res.iterations)
     events = [dict(j=int(e.j), col=int(e.col), kind=int(e.kind), action=int(e.action), ratio=float(e.ratio))
               for e in ev[: min(res.n_events, events_cap)]]
@@ -144,7 +171,7 @@ def solve(A, B, *, tol=1e-8, maxit=100, tau=1e-8, seed=0, pool_size=1, X0=None,
                    Z=dbg["Z"], S=dbg["S"])
     return OracleResult(int(res.status), it, hist[: it + 1].copy() if hist is not None else None, events, X,
                         np.array(res.true_res[:p]), np.array(res.comp_res[:p]), dbg, float(res.start_s),
-                        float(res.loop_s))
+                        float(res.loop_s), ptrue)
 
 
 def csr_block(A, X: np.ndarray) -> np.ndarray:
@@ -179,3 +206,83 @@ def house_apply(v: np.ndarray, tau: float, y: np.ndarray) -> np.ndarray:
     y = np.array(y, dtype=np.float64, copy=True)
     lib().orc_house_apply(len(v), _ptr(v), tau, _ptr(y))
     return y
+
+
+# ---- f3: IC(0) split preconditioning (reading R8) ----
+
+def _csr_arrays(A):
+    return (np.ascontiguousarray(A.indptr, dtype=np.int32), np.ascontiguousarray(A.indices, dtype=np.int32),
+            np.ascontiguousarray(A.data, dtype=np.float64))
+
+
+class PivotBreakdown(ValueError):
+    def __init__(self, row):
+        super().__init__(f"IC(0) pivot <= 0 at row {row}")
+        self.row = row
+
+
+def ic0(M):
+    """Zero-fill incomplete Cholesky L of the symmetric CSR M (both triangles, columns ascending):
+    L has the pattern of M's lower triangle, the diagonal last per row, and (L L^T)_ik = m_ik on it.
+    Returns a synth-style Csr (same class as M).  Raises PivotBreakdown on a pivot <= 0."""
+    ip, ix, dx = _csr_arrays(M)
+    n = len(ip) - 1
+    nzl = int(np.count_nonzero(ix <= np.repeat(np.arange(n), np.diff(ip))))
+    Lp = np.zeros(n + 1, dtype=np.int32)
+    Li = np.zeros(max(nzl, 1), dtype=np.int32)
+    Lx = np.zeros(max(nzl, 1))
+    bad = C.c_int64(-1)
+    st = lib().orc_ic0(n, _ptr(ip), _ptr(ix), _ptr(dx), _ptr(Lp), _ptr(Li), _ptr(Lx), C.byref(bad))
+    if st == -7:
+        raise PivotBreakdown(int(bad.value))
+    if st != 0:
+        raise ValueError(f"orc_ic0: status {st} (row {bad.value}: missing diagonal?)")
+    return type(M)(n, Lp, Li[:nzl].copy(), Lx[:nzl].copy())
+
+
+def trsv_lower(L, b: np.ndarray) -> np.ndarray:
+    """y = L^-1 b (forward substitution); b a vector or a row-major n x p block (column by column)."""
+    return _trsv(L, b, lib().orc_trsv_lower, transpose=False)
+
+
+def trsv_upper(L, v: np.ndarray) -> np.ndarray:
+    """z = L^-T v (backward substitution on L^T)."""
+    return _trsv(L, v, lib().orc_trsv_upper, transpose=True)
+
+
+def _transpose(L):
+    n = len(L.indptr) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(L.indptr))
+    order = np.lexsort((rows, L.indices))      # by column, then row
+    Up = np.zeros(n + 1, dtype=np.int32)
+    np.add.at(Up, L.indices.astype(np.int64) + 1, 1)
+    return np.cumsum(Up).astype(np.int32), rows[order].astype(np.int32), np.ascontiguousarray(L.data[order])
+
+
+def _trsv(L, b, fn, transpose):
+    b = np.asarray(b, dtype=np.float64)
+    vec = b.ndim == 1
+    Bm = b.reshape(len(b), -1)
+    if transpose:
+        ip, ix, dx = _transpose(L)
+    else:
+        ip, ix, dx = _csr_arrays(L)
+    n = len(ip) - 1
+    out = np.empty_like(Bm)
+    for c in range(Bm.shape[1]):
+        x = np.ascontiguousarray(Bm[:, c])
+        y = np.empty(n)
+        fn(n, _ptr(ip), _ptr(ix), _ptr(dx), _ptr(x), _ptr(y))
+        out[:, c] = y
+    return out[:, 0].copy() if vec else out
+
+
+def prec_op_block(A, L, X: np.ndarray) -> np.ndarray:
+    """Y = L^-1 A L^-T X for a row-major n x p block (the operator of the preconditioned solve)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n, p = X.shape
+    Y = np.empty_like(X)
+    ip, ix, dx = _csr_arrays(A)
+    Lp, Li, Lx = _csr_arrays(L)
+    lib().orc_prec_op_block(n, _ptr(ip), _ptr(ix), _ptr(dx), _ptr(Lp), _ptr(Li), _ptr(Lx), p, _ptr(X), _ptr(Y))
+    return Y

@@ -27,6 +27,9 @@
  *   Update           X += m_j z_j^T                                 eqn.approx-update
  *   Residual         ||f_j^(i)|| = ||tail(:,i)||                    eqn.comp-resid
  *   Stop             max_i ||tail(:,i)||/||b_i|| < tol or j = maxit Alg. 2, C7, C22
+ *   Preconditioning  (f3) IC(0) of an SPD M, split form L^-1 A L^-T  P:1026-1027, reading R8
+ *                    (orc_ic0, orc_trsv_lower/upper, orc_solve_prec; pinned in
+ *                    tests/test_precond_oracle.py, incl. the paper's Fig. 1 counts P:1034-1035)
  *
  * Parity pins (tests/test_oracle_pins.py): dense least squares over an
  * explicitly built block Krylov basis, p = 1 against SciPy MINRES, the paper's
@@ -211,8 +214,33 @@ static void record_event(const orc_config *cfg, int64_t *nev, int64_t j, int32_t
     (*nev)++;
 }
 
+/* The operator the method is applied to: A itself, or (f3) the split-preconditioned
+   L^{-1} A L^{-T} of an IC(0) factor L (see "f3" below). */
+typedef struct {
+    const int32_t *indptr, *indices;
+    const double *data;          /* A in CSR */
+    const int32_t *Lp, *Li;      /* NULL = no preconditioner; else L (lower, diagonal last per row) */
+    const double *Lx;
+    const int32_t *Up, *Ui;      /* L^T in CSR (column i of L as row i, ascending) */
+    const double *Ux;
+    double *t, *u;               /* n-length scratch */
+} orc_op;
+
+static void op_apply(int64_t n, const orc_op *op, const double *x, double *y);
+
+static int solve_core(int64_t n, const orc_op *op, const double *B, double *X, const orc_config *cfg,
+                      orc_result *res);
+
 int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const double *data,
               const double *B, double *X, const orc_config *cfg, orc_result *res) {
+    orc_op op;
+    memset(&op, 0, sizeof(op));
+    op.indptr = indptr; op.indices = indices; op.data = data;
+    return solve_core(n, &op, B, X, cfg, res);
+}
+
+static int solve_core(int64_t n, const orc_op *op, const double *B, double *X, const orc_config *cfg,
+                      orc_result *res) {
     const int p = cfg->p;
     memset(res, 0, sizeof(*res));
     if (p < 1 || p > ORC_MAX_P || n < p || !(cfg->tol >= 0.0) || cfg->maxit < 0) {
@@ -272,7 +300,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
     for (int c = 0; c < p; ++c) {
         double *f = F + (int64_t)c * n;
         for (int64_t i = 0; i < n; ++i) f[i] = X[i * p + c];
-        csr_matvec(n, indptr, indices, data, f, w);
+        op_apply(n, op, f, w);
         for (int64_t i = 0; i < n; ++i) f[i] = B[i * p + c] - w[i];
     }
 
@@ -346,7 +374,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
         const int m = (int)((j - 1) % p);          /* 0-based column within the block (C2) */
         /* block operator application every p iterations (Alg. 2, C2) */
         if (m == 0)
-            for (int c = 0; c < p; ++c) csr_matvec(n, indptr, indices, data, U(j + c), Wblk + (int64_t)c * n);
+            for (int c = 0; c < p; ++c) op_apply(n, op, U(j + c), Wblk + (int64_t)c * n);
         /* shrink: the basis is exhausted once every index of the window j .. j+p-1 is removed */
         if (shrink) {
             int live = 0;
@@ -536,7 +564,7 @@ int orc_solve(int64_t n, const int32_t *indptr, const int32_t *indices, const do
         for (int r = 0; r < p; ++r) s += T[r * p + c] * T[r * p + c];
         res->comp_res[c] = bnorm[c] > 0.0 ? sqrt(s) / bnorm[c] : 0.0;
         for (int64_t i = 0; i < n; ++i) w[i] = X[i * p + c];
-        csr_matvec(n, indptr, indices, data, w, mj);
+        op_apply(n, op, w, mj);
         double t = 0.0;
         for (int64_t i = 0; i < n; ++i) {
             double d = B[i * p + c] - mj[i];
@@ -551,5 +579,198 @@ done:
     free(Vref); free(tauref); free(hl); free(hcol); free(work); free(absent);
 #undef U
 #undef MV
+    return res->status;
+}
+
+/* ====================================================================================
+ * f3: split preconditioning with an incomplete Cholesky factor.
+ *
+ * "we precondition with the incomplete Cholesky factors of -L constructed
+ * using Matlab's ichol() function with the default settings" -- the default is the
+ * zero-fill factorisation IC(0): L lower triangular with the sparsity pattern of the
+ * lower triangle of M, and (L L^T)_{ik} = m_{ik} for every (i, k) in that pattern.  The
+ * paper does not state how the factor enters MINRES; reading R8: the split
+ * (two-sided) form, which keeps the operator symmetric:
+ *
+ *     Ahat = L^{-1} A L^{-T},   Rhat_0 = L^{-1} (B - A X_0),   Ahat Yhat = Rhat_0, Yhat_0 = 0,
+ *     X = X_0 + L^{-T} Yhat,
+ *
+ * i.e. the unpreconditioned method above (solve_core) run on the transformed system; its
+ * residual norms are ||L^{-1}(b_i - A x_i)|| relative to ||L^{-1}(b_i - A x0_i)||.
+ * ==================================================================================== */
+
+/* IC(0) of the symmetric matrix M (both triangles stored, columns ascending per row).
+ * Row-oriented ("up-looking") definition, row i in order:
+ *   l_ik = (m_ik - sum_{j<k, j in pat(i) and pat(k)} l_ij l_kj) / l_kk     (k < i in pat(i), ascending)
+ *   l_ii = sqrt(m_ii - sum_{k<i} l_ik^2)
+ * (sums in ascending j, each term subtracted with fma).  Output: L in CSR (Lp: n+1, Li/Lx: the lower
+ * entries of M in M's order, the diagonal last in each row).  Returns 0, ORC_EINVAL (missing diagonal),
+ * or -7 with *bad_row = the row whose pivot is <= 0 (IC(0) breakdown). */
+int orc_ic0(int64_t n, const int32_t *indptr, const int32_t *indices, const double *data,
+            int32_t *Lp, int32_t *Li, double *Lx, int64_t *bad_row) {
+    int64_t nz = 0;
+    Lp[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k)
+            if (indices[k] <= i) { Li[nz] = indices[k]; Lx[nz] = data[k]; ++nz; }
+        Lp[i + 1] = (int32_t)nz;
+        if (nz == Lp[i] || Li[nz - 1] != i) { if (bad_row) *bad_row = i; return ORC_EINVAL; }
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t e0 = Lp[i], ed = Lp[i + 1] - 1;   /* ed = the diagonal */
+        for (int64_t e = e0; e < ed; ++e) {
+            const int64_t k = Li[e];
+            double s = Lx[e];                             /* m_ik */
+            /* sum over j < k in pat(i) and pat(k): merge row i (entries before e) with row k */
+            int64_t a = e0, b = Lp[k];
+            const int64_t bend = Lp[k + 1] - 1;           /* row k's off-diagonal entries */
+            while (a < e && b < bend) {
+                if (Li[a] < Li[b]) ++a;
+                else if (Li[a] > Li[b]) ++b;
+                else { s = fma(-Lx[a], Lx[b], s); ++a; ++b; }
+            }
+            Lx[e] = s / Lx[Lp[k + 1] - 1];                /* / l_kk */
+        }
+        double d = Lx[ed];                                /* m_ii */
+        for (int64_t e = e0; e < ed; ++e) d = fma(-Lx[e], Lx[e], d);
+        if (!(d > 0.0)) { if (bad_row) *bad_row = i; return -7; }
+        Lx[ed] = sqrt(d);
+    }
+    return 0;
+}
+
+/* y = L^{-1} b: forward substitution, row i ascending, y_i = (b_i - sum_{j<i} l_ij y_j) / l_ii. */
+void orc_trsv_lower(int64_t n, const int32_t *Lp, const int32_t *Li, const double *Lx, const double *b,
+                    double *y) {
+    for (int64_t i = 0; i < n; ++i) {
+        double s = b[i];
+        for (int64_t e = Lp[i]; e < Lp[i + 1] - 1; ++e) s = fma(-Lx[e], y[Li[e]], s);
+        y[i] = s / Lx[Lp[i + 1] - 1];
+    }
+}
+
+/* z = L^{-T} v: backward substitution on U = L^T (row i of U = column i of L, the diagonal FIRST),
+   row i descending, z_i = (v_i - sum_{j>i} l_ji z_j) / l_ii, sum in ascending j. */
+void orc_trsv_upper(int64_t n, const int32_t *Up, const int32_t *Ui, const double *Ux, const double *v,
+                    double *z) {
+    for (int64_t i = n - 1; i >= 0; --i) {
+        double s = v[i];
+        for (int64_t e = Up[i] + 1; e < Up[i + 1]; ++e) s = fma(-Ux[e], z[Ui[e]], s);
+        z[i] = s / Ux[Up[i]];
+    }
+}
+
+/* U = L^T as CSR (plain counting transpose; rows of U ascending in column). */
+static int transpose_lower(int64_t n, const int32_t *Lp, const int32_t *Li, const double *Lx,
+                           int32_t **Up, int32_t **Ui, double **Ux) {
+    const int64_t nz = Lp[n];
+    *Up = calloc((size_t)(n + 1), sizeof(int32_t));
+    *Ui = malloc(sizeof(int32_t) * (size_t)(nz > 0 ? nz : 1));
+    *Ux = malloc(sizeof(double) * (size_t)(nz > 0 ? nz : 1));
+    int32_t *fill = calloc((size_t)(n + 1), sizeof(int32_t));
+    if (!*Up || !*Ui || !*Ux || !fill) { free(fill); return ORC_ENOMEM; }
+    for (int64_t e = 0; e < nz; ++e) (*Up)[Li[e] + 1]++;
+    for (int64_t i = 0; i < n; ++i) (*Up)[i + 1] += (*Up)[i];
+    for (int64_t i = 0; i < n; ++i)          /* rows of L ascending -> each U row ascending in column */
+        for (int64_t e = Lp[i]; e < Lp[i + 1]; ++e) {
+            const int64_t c = Li[e];
+            const int64_t d = (*Up)[c] + fill[c]++;
+            (*Ui)[d] = (int32_t)i;
+            (*Ux)[d] = Lx[e];
+        }
+    free(fill);
+    return 0;
+}
+
+/* y = op x: A x, or L^{-1} (A (L^{-T} x)) -- the three steps in that order. */
+static void op_apply(int64_t n, const orc_op *op, const double *x, double *y) {
+    if (!op->Lp) {
+        csr_matvec(n, op->indptr, op->indices, op->data, x, y);
+        return;
+    }
+    orc_trsv_upper(n, op->Up, op->Ui, op->Ux, x, op->t);
+    csr_matvec(n, op->indptr, op->indices, op->data, op->t, op->u);
+    orc_trsv_lower(n, op->Lp, op->Li, op->Lx, op->u, y);
+}
+
+/* Y = op X for a row-major n x p block (test helper). */
+void orc_prec_op_block(int64_t n, const int32_t *indptr, const int32_t *indices, const double *data,
+                       const int32_t *Lp, const int32_t *Li, const double *Lx, int32_t p, const double *X,
+                       double *Y) {
+    orc_op op;
+    memset(&op, 0, sizeof(op));
+    op.indptr = indptr; op.indices = indices; op.data = data;
+    op.Lp = Lp; op.Li = Li; op.Lx = Lx;
+    double *x = malloc(sizeof(double) * (size_t)n), *y = malloc(sizeof(double) * (size_t)n);
+    op.t = malloc(sizeof(double) * (size_t)n);
+    op.u = malloc(sizeof(double) * (size_t)n);
+    int32_t *Up = NULL, *Ui = NULL;
+    double *Ux = NULL;
+    if (x && y && op.t && op.u && transpose_lower(n, Lp, Li, Lx, &Up, &Ui, &Ux) == 0) {
+        op.Up = Up; op.Ui = Ui; op.Ux = Ux;
+        for (int32_t c = 0; c < p; ++c) {
+            for (int64_t i = 0; i < n; ++i) x[i] = X[i * p + c];
+            op_apply(n, &op, x, y);
+            for (int64_t i = 0; i < n; ++i) Y[i * p + c] = y[i];
+        }
+    }
+    free(x); free(y); free(op.t); free(op.u); free(Up); free(Ui); free(Ux);
+}
+
+/* The preconditioned solve (reading R8): Rhat_0 = L^{-1}(B - A X_0), solve_core on
+   (L^{-1} A L^{-T}, Rhat_0) from Yhat_0 = 0, X = X_0 + L^{-T} Yhat.  res->comp_res / ->true_res
+   are the core's (preconditioned: relative to ||Rhat_0(:,i)||); ptrue_res[i] (p entries, may be NULL)
+   receives the unpreconditioned ||b_i - A x_i|| / ||b_i||. */
+int orc_solve_prec(int64_t n, const int32_t *indptr, const int32_t *indices, const double *data,
+                   const int32_t *Lp, const int32_t *Li, const double *Lx, const double *B, double *X,
+                   const orc_config *cfg, orc_result *res, double *ptrue_res) {
+    const int p = cfg->p;
+    memset(res, 0, sizeof(*res));
+    if (p < 1 || p > ORC_MAX_P || n < p) { res->status = ORC_EINVAL; return ORC_EINVAL; }
+    orc_op op;
+    memset(&op, 0, sizeof(op));
+    op.indptr = indptr; op.indices = indices; op.data = data;
+    op.Lp = Lp; op.Li = Li; op.Lx = Lx;
+    int32_t *Up = NULL, *Ui = NULL;
+    double *Ux = NULL;
+    double *Bh = calloc((size_t)(n * p), sizeof(double));
+    double *Yh = calloc((size_t)(n * p), sizeof(double));
+    double *a = malloc(sizeof(double) * (size_t)n), *b = malloc(sizeof(double) * (size_t)n);
+    op.t = malloc(sizeof(double) * (size_t)n);
+    op.u = malloc(sizeof(double) * (size_t)n);
+    int st = ORC_ENOMEM;
+    if (!Bh || !Yh || !a || !b || !op.t || !op.u || transpose_lower(n, Lp, Li, Lx, &Up, &Ui, &Ux) != 0) {
+        res->status = ORC_ENOMEM;
+        goto out;
+    }
+    op.Up = Up; op.Ui = Ui; op.Ux = Ux;
+    if (!cfg->use_x0) memset(X, 0, sizeof(double) * (size_t)(n * p));
+    for (int c = 0; c < p; ++c) {        /* Rhat_0(:,c) = L^{-1} (b_c - A x0_c) */
+        for (int64_t i = 0; i < n; ++i) a[i] = X[i * p + c];
+        csr_matvec(n, indptr, indices, data, a, b);
+        for (int64_t i = 0; i < n; ++i) a[i] = B[i * p + c] - b[i];
+        orc_trsv_lower(n, Lp, Li, Lx, a, b);
+        for (int64_t i = 0; i < n; ++i) Bh[i * p + c] = b[i];
+    }
+    orc_config c2 = *cfg;
+    c2.use_x0 = 0;
+    st = solve_core(n, &op, Bh, Yh, &c2, res);
+    if (st == ORC_EINVAL || st == ORC_ENOMEM) goto out;
+    for (int c = 0; c < p; ++c) {        /* X = X_0 + L^{-T} Yhat; unpreconditioned true residual */
+        for (int64_t i = 0; i < n; ++i) a[i] = Yh[i * p + c];
+        orc_trsv_upper(n, Up, Ui, Ux, a, b);
+        for (int64_t i = 0; i < n; ++i) X[i * p + c] += b[i];
+        for (int64_t i = 0; i < n; ++i) a[i] = X[i * p + c];
+        csr_matvec(n, indptr, indices, data, a, b);
+        double t = 0.0, bn = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            const double d = B[i * p + c] - b[i];
+            t += d * d;
+            bn += B[i * p + c] * B[i * p + c];
+        }
+        if (ptrue_res) ptrue_res[c] = bn > 0.0 ? sqrt(t) / sqrt(bn) : 0.0;
+    }
+out:
+    free(Up); free(Ui); free(Ux); free(Bh); free(Yh); free(a); free(b); free(op.t); free(op.u);
     return res->status;
 }
