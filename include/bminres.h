@@ -47,6 +47,7 @@ extern "C" {
 #define BMINRES_ENOMEM (-4)    /* device allocation failed */
 #define BMINRES_EPOOL (-5)     /* breakdown with the replacement pool empty, not converged */
 #define BMINRES_ESINGULAR_R (-6) /* |r_jj| <= eps_mach*||h_j||: R_j singular, X cannot be updated */
+#define BMINRES_EPIVOT (-7)    /* bminres_set_preconditioner: IC(0) pivot <= 0 (row in bminres_last_error) */
 
 #define BMINRES_MAX_P 32       /* block sizes 1..8, 16 and 32 are compiled */
 #define BMINRES_MAX_POOL 8
@@ -108,12 +109,13 @@ typedef struct {
     double ratio;    /* h / omega */
 } bminres_event;
 
-#define BMINRES_NPHASE 14  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
+#define BMINRES_NPHASE 15  /* spmm (K1), orth (K2), smallqr (K3b), update (K4b), slowpath, start, resid, other,
                               reduce (k_reduce), spmm_fused (K1 with the M/X update of block k-2),
                               split mode (large panels): spmm_av (K1a, A V_k alone), epilogue (K1 streaming
                               A V_k), epilogue_fused (the same with the M/X update of block k-2),
                               update_main (split mode, p >= 16: the M/X update of block k-2 as its own
-                              kernel before K1a(k)) */
+                              kernel before K1a(k)), prec (preconditioned solves: the two triangular
+                              kernels of L^-1 A L^-T, in place of K1a) */
 
 typedef struct {
     int32_t status;           /* return code of the last solve */
@@ -133,6 +135,12 @@ typedef struct {
     int64_t phase_launches[BMINRES_NPHASE];   /* timing = 1 only */
     double bytes_per_block_step;  /* algorithmic bytes model: CSR A + 10 panels */
     double spmm_bytes_per_launch; /* algorithmic bytes of one SpMM launch: CSR A + U_k + U_{k-1} + W */
+    /* preconditioned solves (bminres_set_preconditioner): comp_res / history are the transformed
+     * system's ||L^-1 (b_i - A x_i)|| / ||L^-1 (b_i - A x0_i)||, prec_true_res the same quantity
+     * recomputed from X, and true_res the UNpreconditioned ||b_i - A x_i|| / ||b_i|| */
+    double prec_true_res[BMINRES_MAX_P];
+    int32_t preconditioned;   /* 1: the last solve ran on L^-1 A L^-T */
+    int32_t prec_levels;      /* levels of the forward triangular DAG (the solves' dependency depth) */
 } bminres_stats_t;
 
 /* Default options (device 0, world 1, seed 0, pool_size 1, history on, graphs on). */
@@ -232,6 +240,30 @@ int bminres_halo_plan(int32_t world, int32_t rank, const int64_t *offsets, int64
  * the next basis block is exchanged (overlap), then the rows [0, lo) and [hi, n_loc).
  * row_ptr: n_loc+1 offsets into local_col.  lo = hi = 0 when no row is interior. */
 int bminres_interior_rows(int64_t n_loc, const int32_t *row_ptr, const int32_t *local_col, int64_t *lo, int64_t *hi);
+
+/* ---- Preconditioning ----
+ * "we precondition with the incomplete Cholesky factors of -L constructed using
+ * Matlab's ichol() function with the default settings" (zero fill).  Reading R8: the
+ * split form.  With a factor set, bminres_solve runs the method on L^-1 A L^-T with
+ * Rhat_0 = L^-1 (B - A X_0) from Yhat_0 = 0 and returns X = X_0 + L^-T Yhat; the stop test and
+ * the history use the transformed residuals (relative to ||Rhat_0(:,i)||).  Single rank only. */
+
+/* Compute and keep the IC(0) factor L of M (n x n symmetric positive definite, both triangles,
+ * columns strictly increasing per row, every diagonal entry present; host or device pointers;
+ * copied -- the caller keeps ownership).  L has the pattern of M's lower triangle and
+ * (L L^T)_ik = m_ik on it (the up-looking row algorithm, rows in dependency order on the device).
+ * M = NULL removes the factor.  Returns BMINRES_OK, BMINRES_EINVAL (malformed M, world > 1) or
+ * BMINRES_EPIVOT (a pivot <= 0: IC(0) does not exist for this M; no factor is kept). */
+int bminres_set_preconditioner(bminres_handle h, const bminres_csr *M);
+
+/* The factor's values (host or device buffer) in the order of M's lower-triangle entries (row by
+ * row, columns ascending, the diagonal last).  Copies min(cap, nnz_L); returns nnz_L (0: none). */
+int64_t bminres_get_preconditioner(bminres_handle h, double *l_values, int64_t cap);
+
+/* Component entry point of the preconditioned operator (device pointers, n x p row-major):
+ * mode 0: Y = L^-1 X;  mode 1: Y = L^-T X;  mode 2: Y = L^-1 A L^-T X (A: the n x n operator). */
+int bminres_precond_apply(bminres_handle h, const bminres_csr *A, const double *X, double *Y, int32_t p,
+                          int32_t mode);
 
 /* Message of the last error on this handle (or the last create error if h is NULL). */
 const char *bminres_last_error(bminres_handle h);

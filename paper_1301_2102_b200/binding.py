@@ -15,11 +15,11 @@ import numpy as np
 from . import _build
 
 MAX_P = 32
-NPHASE = 14
+NPHASE = 15
 PHASES = ["spmm", "orth", "smallqr", "update", "slowpath", "start", "resid", "other", "reduce", "spmm_fused",
-          "spmm_av", "epilogue", "epilogue_fused", "update_main"]
+          "spmm_av", "epilogue", "epilogue_fused", "update_main", "prec"]
 STATUS = {0: "OK", 1: "MAXIT", -1: "EINVAL", -2: "ECUDA", -3: "ENCCL", -4: "ENOMEM", -5: "EPOOL",
-          -6: "ESINGULAR_R"}
+          -6: "ESINGULAR_R", -7: "EPIVOT"}
 SUPPORTED_P = (1, 2, 3, 4, 5, 6, 7, 8, 16, 32)
 
 
@@ -63,7 +63,8 @@ class Stats(C.Structure):
                 ("comp_res", C.c_double * MAX_P), ("true_res", C.c_double * MAX_P),
                 ("solve_ms", C.c_double), ("loop_ms", C.c_double),
                 ("phase_ms", C.c_double * NPHASE), ("phase_launches", C.c_int64 * NPHASE),
-                ("bytes_per_block_step", C.c_double), ("spmm_bytes_per_launch", C.c_double)]
+                ("bytes_per_block_step", C.c_double), ("spmm_bytes_per_launch", C.c_double),
+                ("prec_true_res", C.c_double * MAX_P), ("preconditioned", C.c_int32), ("prec_levels", C.c_int32)]
 
 
 _lib = None
@@ -98,6 +99,11 @@ def lib():
                                         C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
         L.bminres_interior_rows.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
                                             C.POINTER(C.c_int64)]
+        L.bminres_set_preconditioner.argtypes = [C.c_void_p, C.POINTER(CsrStruct)]
+        L.bminres_get_preconditioner.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.bminres_get_preconditioner.restype = C.c_int64
+        L.bminres_precond_apply.argtypes = [C.c_void_p, C.POINTER(CsrStruct), C.c_void_p, C.c_void_p, C.c_int32,
+                                            C.c_int32]
         L.bminres_last_error.argtypes = [C.c_void_p]
         L.bminres_last_error.restype = C.c_char_p
         L.bminres_destroy.argtypes = [C.c_void_p]
@@ -109,7 +115,8 @@ def lib():
 EXPORTED = ["bminres_default_options", "bminres_create", "bminres_solve", "bminres_stats", "bminres_get_history",
             "bminres_get_events", "bminres_spmm", "bminres_random_vector", "bminres_workspace_bytes",
             "bminres_get_unique_id", "bminres_init_nccl", "bminres_set_comm_callbacks", "bminres_halo_plan",
-            "bminres_interior_rows", "bminres_last_error", "bminres_destroy"]
+            "bminres_interior_rows", "bminres_set_preconditioner", "bminres_get_preconditioner",
+            "bminres_precond_apply", "bminres_last_error", "bminres_destroy"]
 
 
 def _ptr(x):
@@ -456,7 +463,42 @@ class Solver:
                     solve_ms=s.solve_ms, loop_ms=s.loop_ms,
                     phase_ms={PHASES[i]: s.phase_ms[i] for i in range(NPHASE)},
                     phase_launches={PHASES[i]: s.phase_launches[i] for i in range(NPHASE)},
-                    bytes_per_block_step=s.bytes_per_block_step, spmm_bytes_per_launch=s.spmm_bytes_per_launch)
+                    bytes_per_block_step=s.bytes_per_block_step, spmm_bytes_per_launch=s.spmm_bytes_per_launch,
+                    preconditioned=bool(s.preconditioned), prec_true_res=list(s.prec_true_res[:p]),
+                    prec_levels=s.prec_levels)
+
+    # ---- f3: IC(0) split preconditioning (bminres_set_preconditioner)
+
+    def set_preconditioner(self, M):
+        """Factor M (SPD CSR, DeviceCsr or host) with IC(0) and precondition later solves; None clears."""
+        if M is None:
+            rc = lib().bminres_set_preconditioner(self._h, None)
+        else:
+            s = _csr_struct(M)
+            rc = lib().bminres_set_preconditioner(self._h, C.byref(s))
+        if rc != 0:
+            raise BminresError(f"bminres_set_preconditioner: {STATUS.get(rc, rc)}: {self.last_error()}")
+
+    def get_preconditioner(self) -> np.ndarray:
+        """The IC(0) factor's values in the order of M's lower-triangle entries (diagonal last per row)."""
+        nz = int(lib().bminres_get_preconditioner(self._h, None, 0))
+        out = np.zeros(max(nz, 1))
+        lib().bminres_get_preconditioner(self._h, out.ctypes.data, nz)
+        return out[:nz]
+
+    def precond_apply(self, X, mode: int, A: DeviceCsr | None = None, Y=None):
+        """mode 0: L^-1 X, 1: L^-T X, 2: L^-1 A L^-T X (device tensors)."""
+        import torch
+        if Y is None:
+            Y = torch.empty_like(X)
+        _check_panel(X, "X")
+        _check_panel(Y, "Y", X.shape)
+        s = _csr_struct(A) if A is not None else None
+        rc = lib().bminres_precond_apply(self._h, C.byref(s) if s is not None else None, _ptr(X), _ptr(Y),
+                                         int(X.shape[1]), int(mode))
+        if rc != 0:
+            raise BminresError(f"bminres_precond_apply: {STATUS.get(rc, rc)}: {self.last_error()}")
+        return Y
 
     def spmm(self, A: DeviceCsr, X, Y=None):
         """Y = A X through the solver's SpMM kernel (device tensors)."""

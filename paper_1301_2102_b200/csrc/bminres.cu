@@ -27,13 +27,14 @@
 #include "dmma_kernels.cuh"
 #include "row_kernels.cuh"
 #include "comm.cuh"
+#include "prec_kernels.cuh"
 
 using namespace bmr;
 
 namespace {
 
 enum Phase { PH_SPMM = 0, PH_ORTH, PH_SMALLQR, PH_UPDATE, PH_SLOW, PH_START, PH_RESID, PH_OTHER, PH_REDUCE,
-             PH_SPMM_FUSED, PH_SPMM_AV, PH_EPI, PH_EPI_FUSED, PH_UPD_MAIN };
+             PH_SPMM_FUSED, PH_SPMM_AV, PH_EPI, PH_EPI_FUSED, PH_UPD_MAIN, PH_PREC };
 
 struct Retained {
     double* v;
@@ -63,6 +64,10 @@ struct Kfn {  // per-p kernel table
     size_t smem1, smem2, smem3, smem4b;
     int nt1, nt2, nt4b;
     bool fused;   // K1 applies the M/X update of block k-2 in graph mode (DMMA K1)
+    // f3 (prec_kernels.cuh): Z = L^-T V (backward), AV = L^-1 (A Z) (SpMM + forward), Y = L^-1 X
+    void (*tbwd)(TriArgs);
+    void (*tfwd)(TriArgs);
+    void (*tfwdp)(TriArgs);
 };
 
 template <int P>
@@ -90,6 +95,9 @@ Kfn make_kfn(int q) {
     f.nt2 = NT;
     f.smem2 = K2Smem<P>::bytes;
     f.k3b = k3b_smallqr<P>;
+    f.tbwd = k_trsv<P, true, false>;
+    f.tfwd = k_trsv<P, false, true>;
+    f.tfwdp = k_trsv<P, false, false>;
     if constexpr (P % 8 == 0) {
         if (!getenv("BMINRES_NO_DMMA")) {
             f.k1 = k1_dmma<P>;
@@ -210,7 +218,7 @@ struct bminres_ctx {
     // graphs
     cudaGraphExec_t gexec[6] = {};
     long long graph_launches = 0;   // kernels captured in one graph
-    const void* gkey[8] = {};
+    const void* gkey[9] = {};
     // per-solve
     std::vector<Retained> retained;
     std::vector<bminres_event> events;
@@ -256,6 +264,30 @@ struct bminres_ctx {
     cudaStream_t hstream = nullptr;
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
     int world() const { return opt.world; }
+    // f3: IC(0) split preconditioning (bminres_set_preconditioner; prec_kernels.cuh)
+    struct Sched {
+        int* order = nullptr;   // device: rows by level
+        int* tstart = nullptr;  // device: task offsets
+        long long ntask = 0;
+        int rpw = 0;            // rows per task (0: not built)
+    };
+    struct Prec {
+        bool on = false;
+        bool active = false;
+        bool ws = false;        // the workspace was sized for a preconditioned core (split, AV)    // inside the core solve of a preconditioned bminres_solve
+        unsigned gen = 0;       // generation (graph key)
+        long long n = 0, nnzl = 0;
+        int levels_f = 0, levels_b = 0;
+        int *Lp = nullptr, *Li = nullptr, *Up = nullptr, *Ui = nullptr, *Uperm = nullptr;
+        double *Lx = nullptr, *Ux = nullptr;
+        std::vector<int> lev_f, lev_b;     // host: level of each row (forward / backward DAG)
+        Sched fs, bs, fac;                 // forward / backward task lists (per rpw), factor (rows)
+        unsigned* flags = nullptr;
+        TriCtl* ctl = nullptr;
+        double *Bh = nullptr, *Yh = nullptr, *Z = nullptr;
+        size_t panel_cap = 0;
+        std::vector<std::pair<const void*, int>> occ;   // resident CTAs per SM of each triangular kernel
+    } prec;
 };
 
 namespace {
@@ -398,8 +430,9 @@ void launch_cluster(bminres_ctx* h, K kern, int grid, int nt, size_t smem, A arg
 }
 
 void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
-    if (h->n_ws == n && h->p_ws == p && h->q_ws == q && h->next_ws == h->n_ext) return;
+    if (h->n_ws == n && h->p_ws == p && h->q_ws == q && h->next_ws == h->n_ext && h->prec.ws == h->prec.active) return;
     h->next_ws = h->n_ext;
+    h->prec.ws = h->prec.active;
     for (int s = 0; s < 6; ++s) {
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
         h->gexec[s] = nullptr;
@@ -420,10 +453,12 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         const char* se = getenv("BMINRES_SPLIT");
         const bool can = h->kf.k1pre != nullptr;
         const int mode = se ? (atoi(se) != 0 ? 1 : 2) : h->opt.split_spmm;
-        h->split = can && (mode == 1 || (mode == 0 && (double)n * p * 8.0 >= 128e6));
+        // (a preconditioned solve always splits: its operator L^-1 A L^-T runs as its own kernels
+        // into AV -- prec_kernels.cuh -- and K1 streams AV)
+        h->split = can && (h->prec.active || mode == 1 || (mode == 0 && (double)n * p * 8.0 >= 128e6));
         // the update as its own kernel (k1u_update) in split mode where it is compiled
         h->upd_sep = h->split && h->kf.k1u != nullptr && getenv("BMINRES_FUSED_UPD") == nullptr;
-        if (h->split) {
+        if (h->split || h->prec.active) {   // (generic p, preconditioned: the generic K1 reads AV)
             dalloc(h, &h->AV, panel);
         } else if (h->AV) {
             cudaFree(h->AV);
@@ -496,7 +531,7 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     // Measured (one B200): config 4 6.58 ms vs the pair's 2.88 + 3.54 ms, config 5 2.48 ms vs
     // 1.36 + 0.34 ms -- eight producer warps per SM keep fewer gathers in flight than K1a's forty
     // (twelve: the consumers spill at 128 registers), so the pair stays the default
-    h->ws = h->split && h->kf.k1ws && !h->tp && getenv("BMINRES_WS") != nullptr;
+    h->ws = h->split && h->kf.k1ws && !h->tp && !h->prec.active && getenv("BMINRES_WS") != nullptr;
     if (h->ws) h->nb1 = h->n_sm / h->csz * h->csz;
     (void)cluster_grid;
 
@@ -762,6 +797,55 @@ void spmm_plain(bminres_ctx* h, const Kfn& f, const int* rowptr, const int* col,
     }
 }
 
+// ------------------------------------------------------------------ f3: the preconditioned operator
+// One triangular kernel over a task list (prec_kernels.cuh), persistent: the grid never exceeds
+// the resident capacity (the flag waits are deadlock-free only among resident warps), less one
+// CTA slot for the side branch.
+void launch_trsv(bminres_ctx* h, cudaStream_t s, void (*kern)(TriArgs), const bminres_ctx::Sched& sc, bool upper,
+                 const StepPtrs* sp, const double* X, double* Y, long long n) {
+    auto& pr = h->prec;
+    TriArgs a{};
+    if (sp) {
+        a.rowptr = sp->rowptr;
+        a.col = sp->col;
+        a.val = sp->val;
+    }
+    a.Tp = upper ? pr.Up : pr.Lp;
+    a.Ti = upper ? pr.Ui : pr.Li;
+    a.Tx = upper ? pr.Ux : pr.Lx;
+    a.X = X;
+    a.Y = Y;
+    a.flags = pr.flags;
+    a.ctl = pr.ctl;
+    a.s = TriSched{sc.order, sc.tstart, sc.ntask};
+    a.n = n;
+    int occ = 0;
+    for (auto& c : pr.occ)
+        if (c.first == (const void*)kern) occ = c.second;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)kern, NT, 0);
+        occ = std::max(1, occ);
+        pr.occ.push_back({(const void*)kern, occ});
+    }
+    const long long cap = std::max(1ll, (long long)h->n_sm * occ - 1);
+    const long long need = (sc.ntask + NT / 32 - 1) / (NT / 32);
+    const int grid = (int)std::max(1ll, std::min(cap, need));
+    kern<<<grid, NT, 0, s>>>(a);
+    check_launch(h, "k_trsv");
+}
+
+// out = L^-1 A L^-T V (reading R8): Z = L^-T V, then out = L^-1 (A Z)
+void launch_prec_op(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, const double* V, double* out, long long n) {
+    cudaStream_t keep = h->stream;
+    h->stream = s;   // (TimeMark records on h->stream)
+    {
+        TimeMark tm(h, PH_PREC);
+        launch_trsv(h, s, h->kf.tbwd, h->prec.bs, true, nullptr, V, h->prec.Z, n);
+        launch_trsv(h, s, h->kf.tfwd, h->prec.fs, false, &sp, h->prec.Z, out, n);
+    }
+    h->stream = keep;
+}
+
 void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, long long k, int fuse = 0) {
     const int sk = (int)(k % 3), par = (int)(k & 1);
     K1Args a{sp.rowptr, sp.col, sp.val, h->V[sk], h->V[(sk + 2) % 3], h->V[(sk + 1) % 3], n, h->st, h->part,
@@ -843,7 +927,9 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
             if (e != cudaSuccess) fail(h, BMINRES_ECUDA, std::string("k1a_spmm: ") + cudaGetErrorString(e));
             h->launches++;
         };
-        if (h->halo_pending) {
+        if (h->prec.active) {
+            launch_prec_op(h, s, sp, h->V[sk], h->AV, n);   // (f3: in place of K1a)
+        } else if (h->halo_pending) {
             // row partition: the interior rows while V_k's halo is in flight, then the boundary
             // rows [0, int_lo) and [int_hi, n) once it has landed
             K1Args ai = aa;
@@ -872,6 +958,10 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
         return;
     }
     halo_join(h, s);
+    if (h->prec.active) {   // (f3, generic p: the generic K1 reads A V_k from AV)
+        launch_prec_op(h, s, sp, h->V[sk], h->AV, n);
+        a.AV = h->AV;
+    }
     {
         TimeMark tm(h, fuse ? PH_SPMM_FUSED : PH_SPMM);
         cudaStream_t keep = h->stream;
@@ -946,9 +1036,10 @@ int choose_gblocks(long long nblocks) {
 // graph every main-branch edge is programmatic (PDL).  Fused mode: K1(s+1) applies the M/X
 // update of block s-1 and the side branch is K3b alone.
 void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
-    const void* key[8] = {sp.rowptr, sp.col, sp.val, sp.X, h->V[0], h->M[0], (const void*)(intptr_t)n,
-                          (const void*)(intptr_t)((h->p_ws * 16 + h->gblocks) * 2 + (h->red2_fac ? 1 : 0))};
-    bool same = h->gexec[0] && std::equal(key, key + 8, h->gkey);
+    const void* key[9] = {sp.rowptr, sp.col, sp.val, sp.X, h->V[0], h->M[0], (const void*)(intptr_t)n,
+                          (const void*)(intptr_t)((h->p_ws * 16 + h->gblocks) * 2 + (h->red2_fac ? 1 : 0)),
+                          (const void*)(intptr_t)(h->prec.active ? (long long)h->prec.gen + 1 : 0)};
+    bool same = h->gexec[0] && std::equal(key, key + 9, h->gkey);
     if (same) return;
     for (int q = 0; q < 6; ++q) {
         if (h->gexec[q]) cudaGraphExecDestroy(h->gexec[q]);
@@ -979,7 +1070,7 @@ void build_graphs(bminres_ctx* h, const StepPtrs& sp, long long n) {
         CK(cudaGraphInstantiate(&h->gexec[q], g, 0));
         cudaGraphDestroy(g);
     }
-    std::copy(key, key + 8, h->gkey);
+    std::copy(key, key + 9, h->gkey);
 }
 
 // write a few DevState fields from the host (after draining the stream)
@@ -1842,8 +1933,12 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     {
         seg.mark("loop");
         TimeMark tm(h, PH_RESID);
-        const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);   // (V slots are free now)
-        spmm_plain(h, h->kf, sp.rowptr, sp.col, sp.val, Xe, h->M[0], n, h->stream, h->tpw);
+        if (h->prec.active) {   // f3: the transformed system's residual Rhat_0 - Ahat Yhat
+            launch_prec_op(h, h->stream, sp, sp.X, h->M[0], n);
+        } else {
+            const double* Xe = extended_input(h, sp.X, n, p, h->V[0]);   // (V slots are free now)
+            spmm_plain(h, h->kf, sp.rowptr, sp.col, sp.val, Xe, h->M[0], n, h->stream, h->tpw);
+        }
         launch_colsq(h, B, h->M[0], n, p, h->dsc);
     }
     std::vector<double> r2(p);
@@ -1899,6 +1994,325 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     return fin->status;
 }
 
+
+// ------------------------------------------------------------------ f3: IC(0) split preconditioning
+// (reading R8 and "Preconditioning")
+
+void free_sched(bminres_ctx::Sched& sc) {
+    if (sc.order) cudaFree(sc.order);
+    if (sc.tstart) cudaFree(sc.tstart);
+    sc = bminres_ctx::Sched{};
+}
+
+void prec_free(bminres_ctx* h) {
+    auto& pr = h->prec;
+    for (int* q : {pr.Lp, pr.Li, pr.Up, pr.Ui, pr.Uperm})
+        if (q) cudaFree(q);
+    for (double* q : {pr.Lx, pr.Ux, pr.Bh, pr.Yh, pr.Z})
+        if (q) cudaFree(q);
+    if (pr.flags) cudaFree(pr.flags);
+    if (pr.ctl) cudaFree(pr.ctl);
+    free_sched(pr.fs);
+    free_sched(pr.bs);
+    free_sched(pr.fac);
+    const unsigned gen = pr.gen;
+    pr = bminres_ctx::Prec{};
+    pr.gen = gen + 1;
+}
+
+// Rows sorted by level (ascending row within a level) and tasks of at most rpw rows that never
+// cross a level (the rows of one task are independent); host analysis, setup only.
+void build_sched(bminres_ctx* h, bminres_ctx::Sched& sc, const std::vector<int>& lev, int nlev, int rpw) {
+    free_sched(sc);
+    const long long n = (long long)lev.size();
+    std::vector<long long> cnt((size_t)nlev + 1, 0);
+    for (int l : lev) cnt[(size_t)l + 1]++;
+    for (int l = 0; l < nlev; ++l) cnt[(size_t)l + 1] += cnt[(size_t)l];
+    std::vector<int> order((size_t)n);
+    {
+        std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
+        for (long long i = 0; i < n; ++i) order[(size_t)pos[(size_t)lev[(size_t)i]]++] = (int)i;
+    }
+    std::vector<int> ts;
+    ts.reserve((size_t)(n / rpw + nlev + 1));
+    for (int l = 0; l < nlev; ++l)
+        for (long long r = cnt[(size_t)l]; r < cnt[(size_t)l + 1]; r += rpw) ts.push_back((int)r);
+    ts.push_back((int)n);
+    CK(cudaMalloc((void**)&sc.order, std::max<size_t>(1, (size_t)n) * sizeof(int)));
+    CK(cudaMalloc((void**)&sc.tstart, ts.size() * sizeof(int)));
+    CK(cudaMemcpy(sc.order, order.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(sc.tstart, ts.data(), ts.size() * sizeof(int), cudaMemcpyHostToDevice));
+    sc.ntask = (long long)ts.size() - 1;
+    sc.rpw = rpw;
+}
+
+// IC(0) of M: host analysis (pattern of M's lower triangle, the forward and backward level DAGs,
+// the pattern of U = L^T), then the numeric factorisation on the device (k_ic0) and U's values.
+void prec_setup(bminres_ctx* h, const bminres_csr* M) {
+    if (h->opt.world != 1) fail(h, BMINRES_EINVAL, "preconditioning is single-rank only");
+    const long long n = M->n;
+    if (n < 1 || M->n_loc != n || M->row_begin != 0) fail(h, BMINRES_EINVAL, "M: n_loc = n >= 1, row_begin = 0");
+    if (M->nnz < n || M->nnz >= (1ll << 31) || n >= (1ll << 31))
+        fail(h, BMINRES_EINVAL, "M: nnz must be in [n, 2^31)");
+    if (!M->row_ptr || !M->col_idx || !M->values) fail(h, BMINRES_EINVAL, "M: null array");
+    CK(cudaSetDevice(h->device));
+    std::vector<int> rp((size_t)n + 1), ci((size_t)M->nnz);
+    std::vector<double> va((size_t)M->nnz);
+    CK(cudaMemcpy(rp.data(), M->row_ptr, rp.size() * sizeof(int), cudaMemcpyDefault));
+    CK(cudaMemcpy(ci.data(), M->col_idx, ci.size() * sizeof(int), cudaMemcpyDefault));
+    CK(cudaMemcpy(va.data(), M->values, va.size() * sizeof(double), cudaMemcpyDefault));
+    if (rp[0] != 0 || rp[(size_t)n] != M->nnz) fail(h, BMINRES_EINVAL, "M: row_ptr[0] = 0, row_ptr[n] = nnz");
+    std::vector<int> Lp((size_t)n + 1, 0), Li;
+    std::vector<double> Lx;
+    Li.reserve((size_t)(M->nnz / 2 + n));
+    Lx.reserve((size_t)(M->nnz / 2 + n));
+    for (long long i = 0; i < n; ++i) {
+        if (rp[(size_t)i + 1] < rp[(size_t)i]) fail(h, BMINRES_EINVAL, "M: row_ptr not monotone");
+        int prev = -1;
+        for (int k = rp[(size_t)i]; k < rp[(size_t)i + 1]; ++k) {
+            const int c = ci[(size_t)k];
+            if (c <= prev || c >= n) fail(h, BMINRES_EINVAL, "M: columns must be strictly increasing and < n");
+            prev = c;
+            if (c <= i) {
+                Li.push_back(c);
+                Lx.push_back(va[(size_t)k]);
+            }
+        }
+        Lp[(size_t)i + 1] = (int)Li.size();
+        if (Lp[(size_t)i + 1] == Lp[(size_t)i] || Li.back() != i)
+            fail(h, BMINRES_EINVAL, "M: no diagonal entry in row " + std::to_string(i));
+    }
+    const long long nzl = (long long)Li.size();
+    // levels: forward (row i after the rows j < i of its L row), backward (after j > i of its U row)
+    std::vector<int> lf((size_t)n, 0), lb((size_t)n, 0);
+    int nlf = 0, nlb = 0;
+    for (long long i = 0; i < n; ++i) {
+        int l = 0;
+        for (int e = Lp[(size_t)i]; e < Lp[(size_t)i + 1] - 1; ++e) l = std::max(l, lf[(size_t)Li[(size_t)e]] + 1);
+        lf[(size_t)i] = l;
+        nlf = std::max(nlf, l + 1);
+    }
+    std::vector<int> Up((size_t)n + 1, 0), Ui((size_t)nzl), Uperm((size_t)nzl);
+    for (long long e = 0; e < nzl; ++e) Up[(size_t)Li[(size_t)e] + 1]++;
+    for (long long i = 0; i < n; ++i) Up[(size_t)i + 1] += Up[(size_t)i];
+    {
+        std::vector<int> fill((size_t)n, 0);
+        for (long long i = 0; i < n; ++i)   // rows of L ascending: each U row ascending, diagonal first
+            for (int e = Lp[(size_t)i]; e < Lp[(size_t)i + 1]; ++e) {
+                const int c = Li[(size_t)e];
+                const int d = Up[(size_t)c] + fill[(size_t)c]++;
+                Ui[(size_t)d] = (int)i;
+                Uperm[(size_t)d] = e;
+            }
+    }
+    for (long long i = n - 1; i >= 0; --i) {
+        int l = 0;
+        for (int e = Up[(size_t)i] + 1; e < Up[(size_t)i + 1]; ++e) l = std::max(l, lb[(size_t)Ui[(size_t)e]] + 1);
+        lb[(size_t)i] = l;
+        nlb = std::max(nlb, l + 1);
+    }
+    prec_free(h);
+    auto& pr = h->prec;
+    try {
+        CK(cudaMalloc((void**)&pr.Lp, Lp.size() * sizeof(int)));
+        CK(cudaMalloc((void**)&pr.Li, (size_t)nzl * sizeof(int)));
+        CK(cudaMalloc((void**)&pr.Lx, (size_t)nzl * sizeof(double)));
+        CK(cudaMalloc((void**)&pr.Up, Up.size() * sizeof(int)));
+        CK(cudaMalloc((void**)&pr.Ui, (size_t)nzl * sizeof(int)));
+        CK(cudaMalloc((void**)&pr.Uperm, (size_t)nzl * sizeof(int)));
+        CK(cudaMalloc((void**)&pr.Ux, (size_t)nzl * sizeof(double)));
+        CK(cudaMalloc((void**)&pr.flags, (size_t)n * sizeof(unsigned)));
+        CK(cudaMalloc((void**)&pr.ctl, sizeof(TriCtl)));
+        CK(cudaMemcpy(pr.Lp, Lp.data(), Lp.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pr.Li, Li.data(), (size_t)nzl * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pr.Lx, Lx.data(), (size_t)nzl * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pr.Up, Up.data(), Up.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pr.Ui, Ui.data(), (size_t)nzl * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pr.Uperm, Uperm.data(), (size_t)nzl * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemset(pr.flags, 0, (size_t)n * sizeof(unsigned)));
+        TriCtl c0{0u, 0u, 0x7fffffff, 0};
+        CK(cudaMemcpy(pr.ctl, &c0, sizeof(c0), cudaMemcpyHostToDevice));
+        pr.n = n;
+        pr.nnzl = nzl;
+        pr.levels_f = nlf;
+        pr.levels_b = nlb;
+        pr.lev_f = std::move(lf);
+        pr.lev_b = std::move(lb);
+        build_sched(h, pr.fac, pr.lev_f, nlf, 1);
+        // numeric IC(0): one thread per row, a persistent grid within the resident capacity
+        TriArgs a{};
+        a.Tp = pr.Lp;
+        a.Ti = pr.Li;
+        a.Tx = pr.Lx;
+        a.flags = pr.flags;
+        a.ctl = pr.ctl;
+        a.s = TriSched{pr.fac.order, pr.fac.tstart, pr.fac.ntask};
+        a.n = n;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_ic0, NT, 0);
+        const long long cap = std::max(1ll, (long long)h->n_sm * std::max(1, occ) - 1);
+        const int grid = (int)std::max(1ll, std::min(cap, (n + NT - 1) / NT));
+        k_ic0<<<grid, NT, 0, h->stream>>>(a);
+        check_launch(h, "k_ic0");
+        k_gather_vals<<<grid_for(h, nzl, 256, 8 * h->n_sm), 256, 0, h->stream>>>(pr.Lx, pr.Uperm, pr.Ux, nzl);
+        check_launch(h, "k_gather_vals");
+        TriCtl c1{};
+        CK(cudaMemcpyAsync(&c1, pr.ctl, sizeof(c1), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (c1.bad_row != 0x7fffffff)
+            fail(h, BMINRES_EPIVOT, "IC(0) pivot <= 0 at row " + std::to_string(c1.bad_row));
+        pr.on = true;
+    } catch (Err&) {
+        prec_free(h);
+        throw;
+    }
+}
+
+// panels and this p's task lists
+void prec_ensure(bminres_ctx* h, int p) {
+    auto& pr = h->prec;
+    const size_t panel = (size_t)pr.n * p + 32;
+    if (pr.panel_cap < panel) {
+        dalloc(h, &pr.Bh, panel);
+        dalloc(h, &pr.Yh, panel);
+        dalloc(h, &pr.Z, panel);
+        CK(cudaMemsetAsync(pr.Z, 0, panel * sizeof(double), h->stream));
+        pr.panel_cap = panel;
+    }
+    const int vec = (p % 2 == 0) ? 2 : 1, lanes = p / vec;
+    int lp = 1;
+    while (lp < lanes) lp <<= 1;
+    const int rpw = 32 / lp;   // PC<P>::RPW
+    if (pr.fs.rpw != rpw) {
+        build_sched(h, pr.fs, pr.lev_f, pr.levels_f, rpw);
+        build_sched(h, pr.bs, pr.lev_b, pr.levels_b, rpw);
+    }
+}
+
+// Preconditioned solve (reading R8): Rhat_0 = L^-1 (B - A X_0); the core solve (do_solve) on
+// (L^-1 A L^-T, Rhat_0) from Yhat_0 = 0; X = X_0 + L^-T Yhat.
+int do_solve_prec(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xin, int p, double tol,
+                  long long maxit, double tau) {
+    auto& pr = h->prec;
+    const bminres_options o = h->opt;
+    if (!A || !Bin || !Xin) fail(h, BMINRES_EINVAL, "null argument");
+    if (o.world != 1) fail(h, BMINRES_EINVAL, "preconditioning is single-rank only");
+    if (A->n != pr.n || A->n_loc != pr.n || A->row_begin != 0)
+        fail(h, BMINRES_EINVAL, "A and the preconditioner M differ in size");
+    Kfn f;
+    if (p < 1 || p > BMINRES_MAX_P || !kfn_for(p, &f, o.pool_size)) fail(h, BMINRES_EINVAL, "unsupported block size p");
+    const long long n = pr.n;
+    if (n < p) fail(h, BMINRES_EINVAL, "n < p");
+    if (A->nnz < 0 || A->nnz >= (1ll << 31)) fail(h, BMINRES_EINVAL, "nnz must be < 2^31");
+    CK(cudaSetDevice(h->device));
+    const size_t panel = (size_t)n * p;
+    h->launches = 0;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, h->stream));
+    // host inputs are staged here, so the core sees device pointers
+    bminres_csr Ad = *A;
+    if (!(is_device_ptr(A->row_ptr) && is_device_ptr(A->col_idx) && is_device_ptr(A->values))) {
+        if (h->a_rows_cap < (size_t)n + 1) {
+            dalloc(h, &h->a_rowptr, n + 1);
+            h->a_rows_cap = n + 1;
+        }
+        if (h->a_nnz_cap < (size_t)std::max<long long>(A->nnz, 1)) {
+            dalloc(h, &h->a_col, std::max<long long>(A->nnz, 1));
+            dalloc(h, &h->a_val, std::max<long long>(A->nnz, 1));
+            h->a_nnz_cap = std::max<long long>(A->nnz, 1);
+        }
+        CK(cudaMemcpyAsync(h->a_rowptr, A->row_ptr, (n + 1) * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->a_col, A->col_idx, A->nnz * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->a_val, A->values, A->nnz * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        Ad.row_ptr = h->a_rowptr;
+        Ad.col_idx = h->a_col;
+        Ad.values = h->a_val;
+    }
+    const double* B = Bin;
+    if (!is_device_ptr(Bin)) {
+        if (h->bx_cap < panel) {
+            dalloc(h, &h->bx, panel);
+            h->bx_cap = panel;
+        }
+        CK(cudaMemcpyAsync(h->bx, Bin, panel * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        B = h->bx;
+    }
+    double* X = Xin;
+    const bool x_host = !is_device_ptr(Xin);
+    if (x_host) {
+        if (h->xx_cap < panel) {
+            dalloc(h, &h->xx, panel);
+            h->xx_cap = panel;
+        }
+        if (o.use_x0) CK(cudaMemcpyAsync(h->xx, Xin, panel * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        X = h->xx;
+    }
+    if ((((uintptr_t)B) | ((uintptr_t)X)) & 15) fail(h, BMINRES_EINVAL, "B and X must be 16-byte aligned");
+    prec_ensure(h, p);
+    StepPtrs sp{};
+    sp.rowptr = Ad.row_ptr;
+    sp.col = Ad.col_idx;
+    sp.val = Ad.values;
+    // Rhat_0 = L^-1 (B - A X_0)
+    const double* R0 = B;
+    if (o.use_x0) {
+        spmm_plain(h, f, sp.rowptr, sp.col, sp.val, X, pr.Z, n, h->stream, h->tpw);
+        k_sub_from<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(B, pr.Z, (long long)panel);
+        check_launch(h, "k_sub_from");
+        R0 = pr.Z;
+    }
+    launch_trsv(h, h->stream, f.tfwdp, pr.fs, false, nullptr, R0, pr.Bh, n);
+    const long long pre_launches = h->launches;
+    // the core solve on the transformed system
+    h->opt.use_x0 = 0;
+    pr.active = true;
+    int r;
+    try {
+        r = do_solve(h, &Ad, pr.Bh, pr.Yh, p, tol, maxit, tau);
+    } catch (Err&) {
+        h->opt.use_x0 = o.use_x0;
+        pr.active = false;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw;
+    }
+    h->opt.use_x0 = o.use_x0;
+    pr.active = false;
+    const long long core_launches = h->launches;
+    // X = X_0 + L^-T Yhat; the unpreconditioned true residual ||b_i - A x_i|| / ||b_i||
+    launch_trsv(h, h->stream, f.tbwd, pr.bs, true, nullptr, pr.Yh, pr.Z, n);
+    k_add_panel<<<grid_for(h, panel, 256, 8 * h->n_sm), 256, 0, h->stream>>>(X, pr.Z, (long long)panel, o.use_x0);
+    check_launch(h, "k_add_panel");
+    spmm_plain(h, f, sp.rowptr, sp.col, sp.val, X, pr.Z, n, h->stream, h->tpw);
+    std::vector<double> r2(p), b2(p);
+    launch_colsq(h, B, pr.Z, n, p, h->dsc);
+    CK(cudaMemcpyAsync(r2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    launch_colsq(h, B, nullptr, n, p, h->dsc);
+    CK(cudaMemcpyAsync(b2.data(), h->dsc, p * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    if (x_host) CK(cudaMemcpyAsync(Xin, X, panel * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaEventRecord(e1, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    bminres_stats_t& s = h->stats;
+    for (int c = 0; c < p; ++c) {
+        s.prec_true_res[c] = s.true_res[c];
+        s.true_res[c] = b2[c] > 0 ? std::sqrt(r2[c]) / std::sqrt(b2[c]) : 0.0;
+    }
+    s.preconditioned = 1;
+    s.prec_levels = pr.levels_f;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    s.solve_ms = ms;
+    s.gpu_launches += pre_launches + (h->launches - core_launches);   // (the core counted its own)
+    // the triangular factors (fp64 + int32 entries, int32 row offsets) are read twice per block step,
+    // and Z = L^-T V_k is written once and gathered once
+    s.bytes_per_block_step += 2.0 * (12.0 * (double)pr.nnzl + 4.0 * (double)(n + 1)) + 2.0 * 8.0 * (double)panel;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return r;
+}
 }  // namespace
 
 // ================================================================== C ABI
@@ -2012,7 +2426,8 @@ int bminres_solve(bminres_handle h, const bminres_csr* A, const double* B, doubl
                   int64_t maxit, double deflation_tol) {
     if (!h) return BMINRES_EINVAL;
     try {
-        int r = do_solve(h, A, B, X, p, tol, maxit, deflation_tol);
+        int r = h->prec.on ? do_solve_prec(h, A, B, X, p, tol, maxit, deflation_tol)
+                           : do_solve(h, A, B, X, p, tol, maxit, deflation_tol);
         h->stats.status = r;
         return r;
     } catch (Err& x) {
@@ -2164,6 +2579,68 @@ int bminres_interior_rows(int64_t n_loc, const int32_t* row_ptr, const int32_t* 
     return BMINRES_OK;
 }
 
+int bminres_set_preconditioner(bminres_handle h, const bminres_csr* M) {
+    if (!h) return BMINRES_EINVAL;
+    try {
+        if (!M) {
+            prec_free(h);
+            return BMINRES_OK;
+        }
+        prec_setup(h, M);
+        return BMINRES_OK;
+    } catch (Err& x) {
+        return x.code;
+    }
+}
+
+int64_t bminres_get_preconditioner(bminres_handle h, double* l_values, int64_t cap) {
+    if (!h || !h->prec.on) return 0;
+    if (!l_values || cap <= 0) return h->prec.nnzl;
+    const int64_t c = std::min<int64_t>(cap, h->prec.nnzl);
+    if (cudaMemcpy(l_values, h->prec.Lx, (size_t)c * sizeof(double), cudaMemcpyDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return h->prec.nnzl;
+}
+
+int bminres_precond_apply(bminres_handle h, const bminres_csr* A, const double* X, double* Y, int32_t p,
+                          int32_t mode) {
+    if (!h || !X || !Y) return BMINRES_EINVAL;
+    try {
+        if (!h->prec.on) fail(h, BMINRES_EINVAL, "no preconditioner set");
+        Kfn f;
+        if (!kfn_for(p, &f)) fail(h, BMINRES_EINVAL, "unsupported block size p");
+        if (mode < 0 || mode > 2) fail(h, BMINRES_EINVAL, "mode must be 0, 1 or 2");
+        if (!is_device_ptr(X) || !is_device_ptr(Y)) fail(h, BMINRES_EINVAL, "bminres_precond_apply takes device pointers");
+        if ((((uintptr_t)X) | ((uintptr_t)Y)) & 15) fail(h, BMINRES_EINVAL, "X and Y must be 16-byte aligned");
+        if (mode == 2 && (!A || A->n != h->prec.n || A->n_loc != h->prec.n || !is_device_ptr(A->row_ptr) ||
+                          !is_device_ptr(A->col_idx) || !is_device_ptr(A->values)))
+            fail(h, BMINRES_EINVAL, "mode 2 needs the n x n operator A in device memory");
+        CK(cudaSetDevice(h->device));
+        prec_ensure(h, p);
+        const long long n = h->prec.n;
+        if (mode == 0) {
+            launch_trsv(h, h->stream, f.tfwdp, h->prec.fs, false, nullptr, X, Y, n);
+        } else if (mode == 1) {
+            launch_trsv(h, h->stream, f.tbwd, h->prec.bs, true, nullptr, X, Y, n);
+        } else {
+            StepPtrs sp{};
+            sp.rowptr = A->row_ptr;
+            sp.col = A->col_idx;
+            sp.val = A->values;
+            const Kfn keep = h->kf;
+            h->kf = f;
+            launch_prec_op(h, h->stream, sp, X, Y, n);
+            h->kf = keep;
+        }
+        CK(cudaStreamSynchronize(h->stream));
+        return BMINRES_OK;
+    } catch (Err& x) {
+        return x.code;
+    }
+}
+
 const char* bminres_last_error(bminres_handle h) {
     if (!h) return g_create_err.c_str();
     return h->err.c_str();
@@ -2172,6 +2649,7 @@ const char* bminres_last_error(bminres_handle h) {
 void bminres_destroy(bminres_handle h) {
     if (!h) return;
     cudaSetDevice(h->device);
+    prec_free(h);
     for (int s = 0; s < 6; ++s)
         if (h->gexec[s]) cudaGraphExecDestroy(h->gexec[s]);
     for (double* p : {h->V[0], h->V[1], h->V[2], h->M[0], h->M[1], h->AV, h->scr[0], h->scr[1], h->pool, h->part, h->dsc,

@@ -143,6 +143,11 @@ __global__ void __launch_bounds__(NT, k1_min_blocks<P>()) k1_spmm(K1Args a) {
                 if (has_prev) ldv<VEC>(a.Vprev + i * P + c0, up);
             }
         }
+        // (f3, preconditioned solves: A V_k is L^-1 A L^-T V_k, computed into AV by prec_kernels.cuh)
+        if (EPI && a.AV) {
+            if (valid) ldv<VEC>(a.AV + i * P + c0, acc);
+            k1 = k0;
+        }
         for (int kb = k0; kb < k1; kb += CH) {
             int cc[CH];
             double av[CH];
