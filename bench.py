@@ -409,6 +409,81 @@ def time_to_tol(cfg, local, dev):
     return out
 
 
+def precond_block(which, args, local, dev):
+    """f3: IC(0) split-preconditioned solves (reading R8).
+    model200: the paper's own preconditioned experiment (A = -L - 200 I on 200 x 200, h = 1/199,
+    IC(0) of -L, tol 1e-8) at p = 8, solved to tol (the paper's p = 10 is not a compiled
+    block size); cfg4: config 4's operator with IC(0) of the unshifted Laplacian, iterations/s over a
+    fixed window.  The triangular kernels are latency-bound by the dependency depth (levels): their
+    line reports achieved GB/s on their algorithmic bytes and the time per level."""
+    import torch
+    import synth
+    from synth.studies import model_matrix
+    from paper_1301_2102_b200 import DeviceCsr, Solver
+    peak, _ = load_peaks()
+    out = {}
+    for w in which.split(","):
+        if w == "model200":
+            N = 200
+            A = model_matrix(N)
+            s_ = float((N - 1) ** 2)
+            M = synth.stencil_csr((N, N), 4.0 * s_, -s_)
+            B = np.random.default_rng(0).standard_normal((A.n, 8))
+            tol, maxit, name = 1e-8, 20000, "paper_model_200_ic0_p8"
+        elif w == "cfg4":
+            P = problem("4")
+            A, B, tol, name = P.A, P.B, P.tol, "cfg4_lap3d_256_shift3_ic0"
+            M = synth.laplacian_3d(256)
+            maxit = args.iters if args.iters > 0 else 256
+            del P
+        else:
+            continue
+        dA, dM = DeviceCsr.from_host(A, dev), DeviceCsr.from_host(M, dev)
+        dB = torch.from_numpy(np.ascontiguousarray(B)).to(dev)
+        n, p = A.n, B.shape[1]
+        with Solver(local, pool_size=1, record_history=False) as s:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s.set_preconditioner(dM)
+            torch.cuda.synchronize()
+            setup_s = time.perf_counter() - t0
+            s.solve(dA, dB, tol=tol, maxit=maxit, history=False, raise_on_error=False)   # warm-up
+            ms, its = [], 0
+            for _ in range(max(1, min(3, args.steps))):
+                r = s.solve(dA, dB, tol=tol, maxit=maxit, history=False, raise_on_error=False)
+                ms.append(r.stats["solve_ms"])
+                its = r.iterations
+            st = r.stats
+        with Solver(local, pool_size=1, record_history=False, use_graphs=False, timing=True) as s:
+            s.set_preconditioner(dM)
+            r2 = s.solve(dA, dB, tol=tol, maxit=min(maxit, 64 * p), history=False, raise_on_error=False)
+            ph, pn = r2.stats["phase_ms"], r2.stats["phase_launches"]
+        nnzl = (M.nnz + n) // 2
+        tri_bytes = 2 * (12.0 * nnzl + 4.0 * (n + 1)) + 12.0 * A.nnz + 4.0 * (n + 1) + 4 * 8.0 * n * p
+        prec_ms = ph["prec"] / max(1, pn["prec"])
+        d = {"n": n, "p": p, "tol": tol, "maxit": maxit, "status": r.status_name, "iterations": its,
+             "device_ms": statistics.median(ms), "iterations_per_s": its / (statistics.median(ms) / 1e3),
+             "ic0_setup_s": setup_s, "levels": st["prec_levels"],
+             "max_true_res_unpreconditioned": max(st["true_res"]), "max_comp_res": max(st["comp_res"]),
+             "slow_blocks": st["slow_blocks"],
+             "prec_op_us_per_block_step": prec_ms * 1e3,
+             "prec_op": {"bound": "latency (dependency depth) and hbm", "bytes_per_launch_pair": tri_bytes,
+                         "achieved_GBps": tri_bytes / (prec_ms / 1e3) / 1e9,
+                         "frac_of_hbm": tri_bytes / (prec_ms / 1e3) / 1e9 / peak,
+                         "us_per_level": prec_ms * 1e3 / (2.0 * st["prec_levels"]),
+                         "note": "Z = L^-T V_k then AV = L^-1 (A Z): 2 sync-free level-scheduled launches per block "
+                                 "step, timed with CUDA events (timing mode)"},
+             "phase_us_per_block_step": {k: 1e3 * ph[k] / max(1, pn[k]) for k in ph if pn[k]}}
+        if w == "model200":
+            d["paper_context"] = {"block_minres_iterations_p10": 1048, "sequential_minres_iterations": 3787,
+                                  "source": "P:1034-1035 (Matlab R2011b, 2.3 GHz Core i5; ten Matlab rand() "
+                                            "right-hand sides): context only"}
+        out[name] = d
+        del dA, dM, dB
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_init()
@@ -443,6 +518,10 @@ def run_ours(args):
     if world == 1 and args.time_to_tol and args.time_to_tol != "none":
         ttt = time_to_tol(args.time_to_tol, local, dev)
 
+    prec = None
+    if world == 1 and args.precond and args.precond != "none":
+        prec = precond_block(args.precond, args, local, dev)
+
     cpu = finish_oracle_sample(cpu_proc) if cpu_proc else None
 
     if rank == 0:
@@ -463,7 +542,7 @@ def run_ours(args):
                 "gpu_launches": main["launches"], "slow_blocks": main["slow_blocks"],
                 "roofline": main["roofline"], "step_roofline": main["step_roofline"], "cpu_baseline": cpu,
                 "e2e": main["e2e"], "clocks": main["clocks"], "hbm_peak_GBps": main["peak"],
-                "secondary": secondary or None, "time_to_tol": ttt}
+                "secondary": secondary or None, "time_to_tol": ttt, "preconditioned": prec}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -488,6 +567,8 @@ def main():
                                                           "2000 otherwise)")
     ap.add_argument("--secondary", default="2", help="comma-separated configs measured after the main one (N = 1; 'none' to skip)")
     ap.add_argument("--time-to-tol", default="2", help="config solved to tol at N = 1 ('none' to skip)")
+    ap.add_argument("--precond", default="model200,cfg4",
+                    help="f3 IC(0)-preconditioned measurements at N = 1 ('none' to skip)")
     ap.add_argument("--no-graphs", action="store_true", help="plain launches instead of CUDA graphs")
     ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel event region")
     ap.add_argument("--no-e2e", action="store_true")
