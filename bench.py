@@ -5,8 +5,8 @@ Workload (default): BASELINE.json configs[3] -- config 4, the 3-D 7-point Laplac
 grid shifted by -3 (n = 16.8M, nnz = 117M), p = 32 Gaussian right-hand sides from seed 0, fp64:
 the configuration BASELINE.json's metric ("... 1/2/4/8 B200") and the north star's targets are
 quoted on, and the largest one that fits one GPU.  A "step" is one bminres_solve call with a fixed
-budget of --iters banded iterations (default 1024 = 32 block steps at p = 32): the start block
-(row a0), then every row a1..a5 of the hot path once per block step.
+budget of --iters banded iterations (default 6400 = 200 block steps at p = 32, SURVEY §8(d)'s
+window): the start block (row a0), then every row a1..a5 of the hot path once per block step.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
 
@@ -57,7 +57,8 @@ PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 8, "orth": 3, "update": 6,
                       # M_{k-2} written, X read + written every other block: 5 on average)
                       "update_main": 5}
 PHASE_READS_A = {"spmm", "spmm_fused", "spmm_av"}
-DEFAULT_ITERS = {"1": 2000, "1c": 2000, "2": 2000, "3": 2000, "4": 1024, "5": 1024}
+# (configs 4 and 5: a window of 200 block steps per solve, SURVEY §8(d)'s timing protocol)
+DEFAULT_ITERS = {"1": 2000, "1c": 2000, "2": 2000, "3": 2000, "4": 6400, "5": 3200}
 
 
 def load_peaks():
@@ -434,7 +435,7 @@ def precond_block(which, args, local, dev):
             P = problem("4")
             A, B, tol, name = P.A, P.B, P.tol, "cfg4_lap3d_256_shift3_ic0"
             M = synth.laplacian_3d(256)
-            maxit = args.iters if args.iters > 0 else 256
+            maxit = 256   # (8 block steps: the triangular pair dominates; a window for iterations/s)
             del P
         else:
             continue
@@ -563,7 +564,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="4")
-    ap.add_argument("--iters", type=int, default=0, help="banded iterations per step (0: 1024 for configs 4/5, "
+    ap.add_argument("--iters", type=int, default=0, help="banded iterations per step (0: 6400 / 3200 for configs 4 / 5, "
                                                           "2000 otherwise)")
     ap.add_argument("--secondary", default="2", help="comma-separated configs measured after the main one (N = 1; 'none' to skip)")
     ap.add_argument("--time-to-tol", default="2", help="config solved to tol at N = 1 ('none' to skip)")

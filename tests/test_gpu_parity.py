@@ -641,3 +641,39 @@ def test_start_block_large_deflation_tol():
     r = gpu_solve(A, B, tol=0.0, maxit=40, deflation_tol=0.05)
     same_events(r.events, ref.events)
     assert_hist_close(r.history, ref.history, rtol=1e-8)
+
+
+# ----------------------------------------------------------------------------- convergence at scale
+
+
+def _count_gate(it_gpu, g, tol):
+    """Counts within +-2% (or +-2) of the oracle's golden run (the north star's bar)."""
+    it_ref = g["iterations"]
+    if abs(it_gpu - it_ref) <= max(2, 0.02 * it_ref):
+        return
+    raise AssertionError(f"count {it_gpu} vs oracle {it_ref}")
+
+
+@pytest.mark.parametrize("cfg,eps", [(2, None), (3, 0.0), (3, 1e-10), (3, 1e-6)])
+def test_full_size_solve_to_tol(cfg, eps):
+    """North-star convergence gates at BASELINE sizes (Alg. 2 stop): config 2 (64^3,
+    p = 8) and config 3 (512^2, p = 16, eps in {0, 1e-10, 1e-6}) solved to tol 1e-8 in the bench's
+    launch configuration: status OK, every column's TRUE residual <= tol, no column-path blocks,
+    the step-0 events of the recipe (8 replacements for eps = 0, 1e-10; none for 1e-6), and the
+    iteration count against the oracle's golden run when scripts/make_golden.py has written it."""
+    import os
+    P = synth.config(cfg) if eps is None else synth.config(cfg, eps=eps)
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=4 * P.maxit, deflation_tol=P.tau)
+    assert r.status_name == "OK"
+    assert max(r.stats["true_res"]) <= P.tol, r.stats["true_res"]
+    assert max(r.stats["comp_res"]) < P.tol
+    assert r.stats["slow_blocks"] == 0
+    if cfg == 3:
+        ev0 = [e for e in r.events if e["j"] == 0]
+        assert len(ev0) == (0 if eps == 1e-6 else 8), r.events
+    gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{P.name}_tol.json")
+    if os.path.exists(gpath):
+        g = _golden(f"{P.name}_tol.json")
+        assert g["status"] == "OK" and g["p"] == P.p and g["n"] == P.n
+        assert_hist_close(r.history, np.array(g["history_first50"]))
+        _count_gate(r.iterations, g, P.tol)
