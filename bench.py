@@ -57,6 +57,30 @@ PHASE_BYTES_PANELS = {"spmm": 3, "spmm_fused": 8, "orth": 3, "update": 6,
                       # M_{k-2} written, X read + written every other block: 5 on average)
                       "update_main": 5}
 PHASE_READS_A = {"spmm", "spmm_fused", "spmm_av"}
+
+
+def phase_flops_per_row(k: str, p: int) -> float:
+    """Algorithmic fp64 flops per row and launch of the DMMA kernels (DESIGN.md §6 "fp64 tensor
+    roofline"): an upper-triangular p x p factor costs p(p+1), a full one 2p^2, a symmetric Gram
+    p(p+1); X += M Z (2p^2) runs every other block in pairs, so 2p^2 on average.  The pool's
+    4Qp and the norms' 2p are left out (< 1%)."""
+    tri, full = p * (p + 1), 2.0 * p * p
+    epi = tri + 2 * full              # (A V_k) Tr_k, V_{k-1} D, V_k^T W
+    upd = tri + 2 * full + full       # V_k (Tr_k R^-1), M_{k-2} B2, M_{k-1} B1; X += M Z (average)
+    orth = full + tri                 # V_k (Tr_k G_s), W'^T W'
+    return {"epilogue": epi, "update_main": upd, "orth": orth, "epilogue_fused": epi + upd,
+            "spmm_fused": epi + upd, "update": upd}.get(k, 0.0)
+
+
+def load_fp64_peak():
+    """fp64 tensor-core (DMMA m8n8k4) peak measured on this pool's B200 by scripts/micro/fp64_mix.cu
+    (profiles/r02_fp64_peaks.json); NVIDIA's nominal B200 fp64 tensor figure is 40 TF/s."""
+    path = os.path.join(ROOT, "profiles", "r02_fp64_peaks.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["dmma_tflops"]), "measured (profiles/r02_fp64_peaks.json, scripts/micro/fp64_mix.cu)"
+    except Exception:
+        return 37.1, "measured (DESIGN.md §6, scripts/micro/spmm_lab.cu)"
 # (configs 4 and 5: a window of 200 block steps per solve, SURVEY §8(d)'s timing protocol)
 DEFAULT_ITERS = {"1": 2000, "1c": 2000, "2": 2000, "3": 2000, "4": 6400, "5": 3200}
 
@@ -332,6 +356,22 @@ def measure(P, args, iters, world, rank, local, dev, *, e2e: bool, kernel_timing
                 "timing": "CUDA events around every launch on the solver stream, the graph's kernels issued "
                           "explicitly in the graph's order and serialised (timing mode)",
                 "phase_us_per_block_step": {k: 1e3 * phase_ms[k] / max(1, phase_n[k]) for k in phase_ms if phase_n[k]}}
+        # the same kernel against the fp64 tensor-core (DMMA) peak: at p = 32 the DMMA kernels are
+        # bound by both (ncu: DMMA pipe 68-76% busy beside 58-61% of DRAM peak)
+        fl = phase_flops_per_row(dom, p) * n_loc
+        if fl > 0:
+            tpk, tkind = load_fp64_peak()
+            t_ach = fl / (per_launch_ms / 1e3) / 1e12
+            roof["tensor"] = {"achieved": t_ach, "peak": tpk, "peak_kind": tkind, "unit": "TFLOP/s",
+                              "frac": t_ach / tpk, "flops_per_launch": fl}
+            roof["tensor_by_kernel"] = {
+                k: (phase_flops_per_row(k, p) * n_loc) / (phase_ms[k] / phase_n[k] / 1e3) / 1e12 / tpk
+                for k in phase_ms if phase_n.get(k) and phase_flops_per_row(k, p) > 0}
+            if t_ach / tpk > roof["frac"]:
+                # the binding resource is the fp64 tensor pipe: report it as the primary bound
+                hb = {kk: roof[kk] for kk in ("achieved", "peak", "peak_kind", "unit", "frac")}
+                roof.update({"bound": "tensor", "achieved": t_ach, "peak": tpk, "peak_kind": tkind,
+                             "unit": "TFLOP/s", "frac": t_ach / tpk, "hbm": hb})
     # whole-step algorithmic roofline (CSR A + 10 panels per block step)
     blk_bytes = abytes + 10 * panel
     blocks = total_iters / p
@@ -339,6 +379,14 @@ def measure(P, args, iters, world, rank, local, dev, *, e2e: bool, kernel_timing
                  "achieved_GBps": blk_bytes * blocks / (ms_max / 1e3) / 1e9,
                  "note": "graph-mode device time of the whole solve (start block included) per block step"}
     step_roof["frac_of_measured"] = step_roof["achieved_GBps"] / peak
+    # the whole step against the fp64 tensor peak: the DMMA kernels' algorithmic flops per block step
+    dm_flops = sum(phase_flops_per_row(k, p) for k in ("epilogue", "update_main", "orth")) * n_loc if p >= 16 else 0.0
+    if dm_flops > 0:
+        tpk, _ = load_fp64_peak()
+        step_roof["dmma_flops_per_block_step"] = dm_flops
+        step_roof["tensor_TFps"] = dm_flops * blocks / (ms_max / 1e3) / 1e12
+        step_roof["tensor_frac_of_measured"] = step_roof["tensor_TFps"] / tpk
+        step_roof["tensor_floor_ms_per_block_step"] = dm_flops / (tpk * 1e12) * 1e3
 
     # ---- end to end through the C ABI with host buffers (pinned A arrays, B and X)
     e2e_d = None

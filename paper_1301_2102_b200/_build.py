@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import os
+import shlex
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -35,7 +36,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
+    # BMINRES_NVCC_EXTRA: extra -D flags for launch-shape experiments (the defaults are the product)
+    extra = shlex.split(os.environ.get("BMINRES_NVCC_EXTRA", ""))
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

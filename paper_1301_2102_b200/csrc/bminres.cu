@@ -49,6 +49,7 @@ struct Kfn {  // per-p kernel table
     size_t smem1pre;
     void (*k1u)(K1Args);     // split mode, p >= 16: the M/X update of block k-2 as its own kernel
     size_t smem1u;
+    int nt1u = 256;          // k1u_update threads per CTA
     void (*k1ws)(K1Args);    // large panels, p >= 16: the warp-specialised K1 (SpMM + epilogue, one kernel)
     size_t smem1ws;
     int nt1ws;
@@ -116,6 +117,7 @@ Kfn make_kfn(int q) {
             if constexpr (P >= 16) {
                 f.k1u = k1u_update<P>;
                 f.smem1u = UpdB<P>::bytes;
+                f.nt1u = UpdB<P>::WARPS * 32;
                 f.k1ws = k1_ws<P>;
                 f.smem1ws = K1WS<P>::bytes;
                 f.nt1ws = K1WS<P>::THREADS;
@@ -522,6 +524,8 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
     if (h->split) {
         int oa = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oa, (const void*)h->kf.k1a, NT, 0);
+        // (BMINRES_K1A_CPS, experiment: fewer K1a CTAs per SM, so the update branch's CTA fits beside them)
+        if (const char* ce = getenv("BMINRES_K1A_CPS")) oa = std::min(oa, std::max(1, atoi(ce)));
         h->nb1a = h->n_sm * std::max(1, oa) - 1;   // one CTA slot left for K3b (side stream)
         const int o1p = std::min(cap, occ_of((const void*)h->kf.k1pre, h->kf.nt1, h->kf.smem1pre));
         h->nb1 = (std::min(NB_MAX, h->n_sm * o1p) - (o1p > 1 ? h->csz : 0)) / h->csz * h->csz;
@@ -873,7 +877,7 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             at[0].val.programmaticStreamSerializationAllowed = (h->pdl && !upd_branch) ? 1 : 0;
             cfg.gridDim = dim3(h->n_sm - 1);   // (one SM left for K3b: the two do not fit one SM together)
-            cfg.blockDim = dim3(UPD_THREADS);
+            cfg.blockDim = dim3(h->kf.nt1u);
             cfg.dynamicSmemBytes = h->kf.smem1u;
             cfg.stream = us;
             cfg.attrs = at;

@@ -627,8 +627,11 @@ constexpr size_t mat_dmma_smem() { return sizeof(double) * (DM<P>::FR + 8 * 2 * 
 // (at p = 32 the fused update was bound by shared-memory bandwidth: 2 LDS.64 per DMMA).
 template <int P>
 struct UpdB {
-    static constexpr int WARPS = 8;
-    static constexpr int TRU = 16;
+    // p = 32: sixteen warps of 8-row tiles (single-staged: shared-memory budget) -- twice the warps
+    // in flight per SM of sixteen-row tiles, at 82 registers (config 4: 4.83 -> 4.56 ms per launch;
+    // 8 rows double-staged: 5.13 ms); p = 16: eight warps of 16 rows, double-staged
+    static constexpr int WARPS = P >= 32 ? 16 : 8;
+    static constexpr int TRU = P >= 32 ? 8 : 16;
     static constexpr int MC = TRU / 8;
     static constexpr int NS = P >= 32 ? 1 : 2;     // cp.async stages per warp (shared-memory budget)
     static constexpr int RS = P + 4;
@@ -638,10 +641,8 @@ struct UpdB {
 };
 
 
-constexpr int UPD_THREADS = 256;
 template <int P>
-__global__ void __launch_bounds__(UPD_THREADS, 1) k1u_update(K1Args a) {
-    static_assert(UpdB<P>::WARPS * 32 == UPD_THREADS, "k1u_update block size");
+__global__ void __launch_bounds__(UpdB<P>::WARPS * 32, 1) k1u_update(K1Args a) {
     using U = UpdB<P>;
     using D = DM<P>;
     constexpr int WARPS = U::WARPS, TRU = U::TRU, MC = U::MC, NS = U::NS, RS = U::RS, TILE = U::TILE;

@@ -7,6 +7,7 @@ per-iteration algorithm) on the seeded ``synth`` inputs -- never from the CUDA p
   python scripts/make_golden.py first50 4      # config 4: first 50 iterations (history, events)
   python scripts/make_golden.py first50 5      # config 5
   python scripts/make_golden.py tol 2          # config 2 run to tol 1e-8 (hours, one thread)
+  python scripts/make_golden.py tol 3 600000 1e-6   # config 3 at eps = 1e-6
 
 Files: tests/golden/<workload>_first50.json and <workload>_tol.json, each naming the oracle
 call that produced it, the host (nproc, CPU model) and the wall time.
@@ -66,15 +67,16 @@ def first50(cfg) -> None:
         "wall_s": dt, "host": host()})
 
 
-def to_tol(cfg, maxit: int) -> None:
-    P = synth.config(cfg)
+def to_tol(cfg, maxit: int, eps: float | None = None) -> None:
+    P = synth.config(cfg) if eps is None else synth.config(cfg, eps=eps)
     t0 = time.perf_counter()
     r = oracle.solve(P.A, P.B, tol=P.tol, maxit=maxit, tau=P.tau, pool_size=1)
     dt = time.perf_counter() - t0
     h = r.history
     every = 1000
     write(f"{P.name}_tol.json", {
-        "source": f"oracle.solve(synth.config({cfg!r}), tol={P.tol}, maxit={maxit}, tau={P.tau}, pool_size=1, seed=0)",
+        "source": (f"oracle.solve(synth.config({cfg!r}" + ("" if eps is None else f", eps={eps!r}")
+                   + f"), tol={P.tol}, maxit={maxit}, tau={P.tau}, pool_size=1, seed=0)"),
         "workload": P.name, "n": P.n, "p": P.p, "nnz": P.A.nnz,
         "status": r.status, "iterations": r.iterations,
         "history_first50": h[:51].tolist(),
@@ -89,6 +91,7 @@ if __name__ == "__main__":
     if mode == "first50":
         first50(cfg)
     elif mode == "tol":
-        to_tol(cfg, int(sys.argv[3]) if len(sys.argv) > 3 else 600_000)
+        to_tol(cfg, int(sys.argv[3]) if len(sys.argv) > 3 else 600_000,
+               float(sys.argv[4]) if len(sys.argv) > 4 else None)
     else:
         raise SystemExit(__doc__)

@@ -24,7 +24,7 @@ __global__ void k(double* out, int iters, double a, double b) {
     } else {
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r)   // 16 x 16 = 256 FMA per lane = 8 DMMA-equivalents (512 flops each / 32 lanes)
+            for (int r = 0; r < 16; ++r)   // 16 x 16 = 256 FMA per lane (32 DMMA-equivalents of 512 flops per warp)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], a, b);
         }
@@ -55,8 +55,10 @@ int main() {
             cudaEventSynchronize(e1);
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
-            // every warp does iters * 8 DMMA-equivalents of 512 flops
-            const double flops = (double)blocks * (threads / 32) * iters * 8 * 512.0;
+            // per warp and iteration: 8 DMMA of 512 flops (4096), or 256 FMA per lane (16384 flops);
+            // mixed: half the warps each
+            const double wi = (double)blocks * (threads / 32) * iters;
+            const double flops = mode == 0 ? wi * 4096.0 : mode == 1 ? wi * 16384.0 : wi * 0.5 * (4096.0 + 16384.0);
             if (rep) printf("%-20s %.2f ms  %.1f TFLOP/s\n", names[mode], ms, flops / ms / 1e9);
         }
     }
