@@ -602,6 +602,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         for (int e = tid; e < 2 * P * P; e += K3T) sH[(r0 + e / P) * LD + e % P] = sTmp[e];
         __syncthreads();
     }
+    trace_pt(tr, 4);
 
     if (warp == 0) {
         const double tol = s_tol;
@@ -609,6 +610,13 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         //      (row 1 -> z_j^T), residuals, stop test (Alg. 2)
         // 1 converged, 2 maxit, 3 singular R, 4 pool exhausted, 5 basis exhausted (shrink)
         int m_last = -1, stop = 0;
+#ifdef K3B_PROF
+        long long pc[6] = {0, 0, 0, 0, 0, 0};
+        long long pt0 = clock64();
+#define K3P(i) { const long long t_ = clock64(); pc[i] += t_ - pt0; pt0 = t_; }
+#else
+#define K3P(i)
+#endif
         const unsigned am_k = s_am_k, am_k1 = s_am_k1;
         for (int m = 0; m < P; ++m) {
             const long long j = j0 + m;
@@ -635,6 +643,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             double x2 = 0.0;
             for (int q = 1 + lane; q <= P; q += 32) x2 = fma(sH[(o + q) * LD + m], sH[(o + q) * LD + m], x2);
             x2 = warp_sum(x2);
+            K3P(0)
             const double xnorm = sqrt(x2);
             // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
             // v = x/(alpha - beta); one reciprocal 1/(beta (alpha - beta)) serves both quotients
@@ -658,45 +667,59 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 stop = 3;
                 break;
             }
-            if (lane == 0) sRd[m] = 1.0 / beta;   // 1 / r_jj for R_kk^{-1}
+            if (lane == 0) sRd[m] = 1.0 / beta;   // 1 / r_jj for R_kk^{-1} (off the chain: lane 0 only)
+            K3P(1)
             double* vj = sVb + m * (P + 2);
             for (int q = lane; q <= P; q += 32) vj[q] = (q == 0) ? 1.0 : sH[(o + q) * LD + m] * scl;
             if (lane == 0) vj[P + 1] = tj;
             __syncwarp();
             for (int q = lane; q <= P; q += 32) sH[(o + q) * LD + m] = (q == 0) ? beta : 0.0;
             double rel = 0.0;
+            K3P(2)
             if (lane < P) {
                 const int c = lane;
+                // (the serial chain of this loop bounds K3b: each dot product runs as two interleaved
+                // partial sums -- half the dependent FMA latency per reflector)
                 if (c > m) {   // later columns of this block
                     double* h = sH + o * LD + c;
-                    double s = 0.0;
+                    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-                    for (int q = 0; q <= P; ++q) s = fma(vj[q], h[q * LD], s);
-                    s *= tj;
+                    for (int q = 0; q <= P; q += 2) {
+                        s0 = fma(vj[q], h[q * LD], s0);
+                        if (q + 1 <= P) s1 = fma(vj[q + 1], h[(q + 1) * LD], s1);
+                    }
+                    const double s = (s0 + s1) * tj;
 #pragma unroll
                     for (int q = 0; q <= P; ++q) h[q * LD] = fma(-s, vj[q], h[q * LD]);
                 }
                 // [T; 0] -> reflector j -> z_j^T = row 0, new tail = rows 1..p
-                double s = 0.0;
+                double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-                for (int q = 0; q < P; ++q) s = fma(vj[q], sT[q * LD + c], s);
-                s *= tj;
+                for (int q = 0; q < P; q += 2) {
+                    s0 = fma(vj[q], sT[q * LD + c], s0);
+                    if (q + 1 < P) s1 = fma(vj[q + 1], sT[(q + 1) * LD + c], s1);
+                }
+                const double s = (s0 + s1) * tj;
                 sZ[m * LD + c] = sT[c] - s;
-                double r2 = 0.0;
+                double r2a = 0.0, r2b = 0.0;
 #pragma unroll
                 for (int q = 0; q < P - 1; ++q) {
                     const double tv = fma(-s, vj[q + 1], sT[(q + 1) * LD + c]);
                     sT[q * LD + c] = tv;
-                    r2 = fma(tv, tv, r2);
+                    if (q & 1)
+                        r2b = fma(tv, tv, r2b);
+                    else
+                        r2a = fma(tv, tv, r2a);
                 }
                 const double tl = -s * vj[P];
                 sT[(P - 1) * LD + c] = tl;
-                r2 = fma(tl, tl, r2);
+                const double r2 = fma(tl, tl, r2a + r2b);
                 rel = sqrt(r2) * sBeta[c];
                 sRes[c] = rel;
                 sHist[m * P + c] = rel;
             }
             const double mx = warp_max(rel);
+            K3P(3)
             m_last = m;
             if (mx < tol) {
                 stop = 1;
@@ -709,6 +732,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             __syncwarp();
         }
         __syncwarp();
+        K3P(4)
         // ---- Ainv = R_kk^{-1} (columns past m_last: identity) (eqn.search-dir-comp)
         if (lane < P) {
             const int l = lane;
@@ -722,6 +746,11 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 }
             }
         }
+        K3P(5)
+#ifdef K3B_PROF
+        if (lane == 0 && tr)
+            for (int i = 0; i < 6; ++i) tr[TRACE_PTS + i] = (unsigned long long)pc[i];   // (CTA 1's unused slot)
+#endif
         if (lane == 0) {
             s_mlast = m_last;
             s_stop = stop;
@@ -762,26 +791,42 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             st->ufz[k % 3][t] = st->Zh[k % 3][g];
         }
     }
+    trace_pt(tr, 6);
     // ---- Q_k = H_{kp} ... H_{(k-1)p+1} on the block's 2p rows (f2): the accumulated action of this
     //      block's reflectors (those generated before a stop), for phase A of blocks k+1 and k+2;
     //      column c of Q_k is e_c with the reflectors applied in order (one thread per column)
     {
+        // TPC threads per column (consecutive lanes): each sums and updates the rows t = sub (mod TPC)
+        // of a reflector's p+1, the partial dots combined by xor shuffles inside the group
+        constexpr int TPC0 = K3T / (2 * P);
+        constexpr int TPC = TPC0 >= 32 ? 32 : TPC0 >= 16 ? 16 : TPC0 >= 8 ? 8 : TPC0 >= 4 ? 4 : TPC0 >= 2 ? 2 : 1;
         double* Qg = st->Qacc[k & 1];
-        for (int c = tid; c < 2 * P; c += K3T) {
-            double* q = sQ + c;   // column c (stride LDQ; the phase-A buffer is free now)
-            for (int r = 0; r < 2 * P; ++r) q[r * S::LDQ] = r == c ? 1.0 : 0.0;
+        for (int c0 = 0; c0 < 2 * P; c0 += K3T / TPC) {
+            const int c = c0 + tid / TPC, sub = tid % TPC;
+            const bool live = c < 2 * P;
+            double* q = sQ + (live ? c : 0);   // column c (stride LDQ; the phase-A buffer is free now)
+            if (live)
+                for (int r = sub; r < 2 * P; r += TPC) q[r * S::LDQ] = r == c ? 1.0 : 0.0;
+            __syncwarp();
             for (int m = 0; m <= m_last; ++m) {   // reflector m acts on block rows m .. m+p
                 const double* v = sVb + m * (P + 2);
                 double s = 0.0;
+                if (live)
 #pragma unroll
-                for (int t = 0; t <= P; ++t) s = fma(v[t], q[(m + t) * S::LDQ], s);
+                    for (int t = sub; t <= P; t += TPC) s = fma(v[t], q[(m + t) * S::LDQ], s);
+#pragma unroll
+                for (int o = 1; o < TPC; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
                 s *= v[P + 1];
+                if (live)
 #pragma unroll
-                for (int t = 0; t <= P; ++t) q[(m + t) * S::LDQ] = fma(-s, v[t], q[(m + t) * S::LDQ]);
+                    for (int t = sub; t <= P; t += TPC) q[(m + t) * S::LDQ] = fma(-s, v[t], q[(m + t) * S::LDQ]);
+                __syncwarp();
             }
-            for (int r = 0; r < 2 * P; ++r) Qg[r * (2 * MAXP) + c] = q[r * S::LDQ];
+            if (live)
+                for (int r = sub; r < 2 * P; r += TPC) Qg[r * (2 * MAXP) + c] = q[r * S::LDQ];
         }
     }
+    trace_pt(tr, 7);
     for (int t = tid; t < P; t += K3T) st->res[t] = sRes[t];
     if (s_hcap > 0)
         for (int t = tid; t < (m_last + 1) * P; t += K3T) {

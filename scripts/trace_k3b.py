@@ -19,6 +19,14 @@ for graphs in (False, True):
         s.solve(dA, dB, tol=0.0, maxit=40 * p, history=False)
     t = np.fromfile(f, dtype=np.uint64).reshape(7, 1024, -1).astype(np.int64)
     x = t[4, 0]
-    d = np.diff(x[[0, 2, 3, 5]]) / 1e3
-    print(f"p={p} graphs={graphs}: K3b prologue+load {d[0]:.1f} us, serial chain {d[1]:.1f} us, stores {d[2]:.1f} us, "
-          f"total {(x[5]-x[0])/1e3:.1f} us")
+    # points: 0 begin, 2 prologue (factor) done, 4 phase A done, 3 phase B + R^-1 done, 6 stores +
+    # update factors done, 7 Q_k accumulated, 5 end
+    seq = [(0, "begin"), (2, "prologue+factor"), (4, "load+H+phaseA"), (3, "phaseB+Rinv"), (6, "stores+uf"),
+           (7, "Qacc"), (5, "tail")]
+    parts = []
+    for (a, _), (b, name) in zip(seq, seq[1:]):
+        parts.append(f"{name} {(x[b] - x[a]) / 1e3:.1f}")
+    print(f"p={p} graphs={graphs}: " + ", ".join(parts) + f" us; total {(x[5] - x[0]) / 1e3:.1f} us")
+    if os.environ.get("K3B_PROF"):   # (library built with -DK3B_PROF: phase-B cycle sums in CTA 1's slot)
+        c = t[4, 1][:6]
+        print("   phase B cycles: (loop tail)+x2+sum %d, dlarfg %d, vj+sH %d, cols+T+max %d, tail-of-loop %d, Rinv %d" % tuple(c))
