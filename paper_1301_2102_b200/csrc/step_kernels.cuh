@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     __shared__ long long s_k, s_jd, s_maxit, s_hcap;
     __shared__ double s_tol;
     __shared__ int s_valid, s_stop_after, s_mlast, s_stop, s_given;
+    __shared__ volatile int s_ready, s_done;   // phase B -> Q_k accumulation: reflectors published
     __shared__ unsigned s_am_k, s_am_k1;   // shrink policy: removed lanes of blocks k and k+1
     if (tid == 0) {
         const long long k = st->k_side;
@@ -500,6 +501,8 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         s_tol = st->tol;
         s_stop_after = st->stop_after;
         if (!s_valid) st->side_go = 0;
+        s_ready = 0;
+        s_done = 0;
     }
     __syncthreads();
     if (!s_valid) return;
@@ -617,132 +620,332 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
 #else
 #define K3P(i)
 #endif
-        const unsigned am_k = s_am_k, am_k1 = s_am_k1;
-        for (int m = 0; m < P; ++m) {
-            const long long j = j0 + m;
-            if (j > maxit) {
-                stop = 2;
-                break;
+        if constexpr (P <= 16) {
+            const unsigned am_k = s_am_k, am_k1 = s_am_k1;
+            // The chain runs in registers: lane c (< p) holds column c of the frame rows 2p .. 4p-1
+            // (hc; reflector m acts on rows 2p+m .. 3p+m) and, for p <= 16, column c of the tail T (tc);
+            // each reflector is broadcast from its pivot lane by shuffles.  (Through shared memory every
+            // column update waited on the previous store: 1.8k cycles per reflector at p = 16.)
+            constexpr bool TREG = P <= 16;
+            const int c = lane;
+            const bool cl = lane < P;
+            double hc[2 * P];
+    #pragma unroll
+            for (int r = 0; r < 2 * P; ++r) hc[r] = cl ? sH[(2 * P + r) * LD + c] : 0.0;
+            double tc[TREG ? P : 1];
+            if constexpr (TREG) {
+    #pragma unroll
+                for (int q = 0; q < P; ++q) tc[q] = cl ? sT[q * LD + c] : 0.0;
             }
-            // shrink: every index of the window j .. j+p-1 removed -> the basis is exhausted
-            // (lanes >= m of this block, lanes < m of the next)
-            if (am_k | am_k1) {
-                const unsigned all = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
-                const unsigned lo = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
-                if ((((am_k & ~lo) | (am_k1 & lo)) & all) == all) {
-                    stop = 5;
+            const double bet_c = cl ? sBeta[c] : 0.0;
+    #pragma unroll
+            for (int m = 0; m < P; ++m) {
+                const long long j = j0 + m;
+                if (j > maxit) {
+                    stop = 2;
+                    break;
+                }
+                // shrink: every index of the window j .. j+p-1 removed -> the basis is exhausted
+                // (lanes >= m of this block, lanes < m of the next)
+                if (am_k | am_k1) {
+                    const unsigned all = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
+                    const unsigned lo = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+                    if ((((am_k & ~lo) | (am_k1 & lo)) & all) == all) {
+                        stop = 5;
+                        break;
+                    }
+                }
+                // shrink: u_j removed -> column j of \bar H is deleted: identity reflector,
+                // R column zero (placeholder 1 on the diagonal for R_kk^{-1}), z_j = the tail's first
+                // (zero) row, m_j = 0
+                const bool gone = (am_k >> m) & 1u;
+                // pivot column m (lane m): alpha = row 2p+m, x = rows 2p+m+1 .. 3p+m
+                double x2a = 0.0, x2b = 0.0;
+    #pragma unroll
+                for (int q = 1; q <= P; ++q) {
+                    if (q & 1)
+                        x2a = fma(hc[m + q], hc[m + q], x2a);
+                    else
+                        x2b = fma(hc[m + q], hc[m + q], x2b);
+                }
+                const double alpha = __shfl_sync(FULL, hc[m], m);
+                const double x2 = __shfl_sync(FULL, x2a + x2b, m);
+                K3P(0)
+                // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
+                // v = x/(alpha - beta); one reciprocal 1/(beta (alpha - beta)) serves both quotients
+                double tj, beta, scl, rbeta;   // (rbeta = 1 / beta)
+                if (gone) {
+                    tj = 0.0;
+                    beta = 1.0;
+                    scl = 0.0;
+                    rbeta = 1.0;
+                } else if (x2 == 0.0) {   // (||x|| = 0)
+                    tj = 0.0;
+                    beta = alpha;
+                    scl = 0.0;
+                    rbeta = 1.0 / beta;
+                } else {
+                    beta = -copysign(sqrt(fma(alpha, alpha, x2)), alpha);
+                    const double s = alpha - beta;
+                    const double inv = 1.0 / (beta * s);
+                    tj = -s * s * inv;
+                    scl = beta * inv;
+                    rbeta = s * inv;
+                }
+                if (!gone && fabs(beta) <= DBL_EPSILON * sHn[m]) {
+                    stop = 3;
+                    break;
+                }
+                K3P(1)
+                double vq[P + 1];   // v = (1, x scl)
+                vq[0] = 1.0;
+    #pragma unroll
+                for (int q = 1; q <= P; ++q) vq[q] = __shfl_sync(FULL, hc[m + q], m) * scl;
+                if (lane == 0) {
+                    sRd[m] = rbeta;   // 1 / r_jj for R_kk^{-1}
+                    double* vj = sVb + m * (P + 2);
+    #pragma unroll
+                    for (int q = 0; q <= P; ++q) vj[q] = vq[q];
+                    vj[P + 1] = tj;
+                    __threadfence_block();
+                    s_ready = m + 1;   // (warps 1-3 accumulate Q_k meanwhile)
+                }
+                K3P(2)
+                double rel = 0.0, rel2 = 0.0;
+                if (cl) {
+                    if (c > m) {   // later columns of this block
+                        double sp[4] = {0.0, 0.0, 0.0, 0.0};
+    #pragma unroll
+                        for (int q = 0; q <= P; ++q) sp[q & 3] = fma(vq[q], hc[m + q], sp[q & 3]);
+                        const double s = ((sp[0] + sp[1]) + (sp[2] + sp[3])) * tj;
+    #pragma unroll
+                        for (int q = 0; q <= P; ++q) hc[m + q] = fma(-s, vq[q], hc[m + q]);
+                    } else if (c == m) {   // the pivot column becomes (beta, 0, ..., 0)
+                        hc[m] = beta;
+    #pragma unroll
+                        for (int q = 1; q <= P; ++q) hc[m + q] = 0.0;
+                    }
+                    // [T; 0] -> reflector j -> z_j^T = row 0, new tail = rows 1..p
+                    double s0 = 0.0, s1 = 0.0, r2a = 0.0, r2b = 0.0, tl;
+                    if constexpr (TREG) {
+                        double sp[4] = {0.0, 0.0, 0.0, 0.0};
+    #pragma unroll
+                        for (int q = 0; q < P; ++q) sp[q & 3] = fma(vq[q], tc[q], sp[q & 3]);
+                        const double s = ((sp[0] + sp[1]) + (sp[2] + sp[3])) * tj;
+                        sZ[m * LD + c] = tc[0] - s;
+    #pragma unroll
+                        for (int q = 0; q < P - 1; ++q) {
+                            tc[q] = fma(-s, vq[q + 1], tc[q + 1]);
+                            if (q & 1)
+                                r2b = fma(tc[q], tc[q], r2b);
+                            else
+                                r2a = fma(tc[q], tc[q], r2a);
+                        }
+                        tl = -s * vq[P];
+                        tc[P - 1] = tl;
+                    } else {
+    #pragma unroll
+                        for (int q = 0; q < P; ++q) {
+                            if (q & 1)
+                                s1 = fma(vq[q], sT[q * LD + c], s1);
+                            else
+                                s0 = fma(vq[q], sT[q * LD + c], s0);
+                        }
+                        const double s = (s0 + s1) * tj;
+                        sZ[m * LD + c] = sT[c] - s;
+    #pragma unroll
+                        for (int q = 0; q < P - 1; ++q) {
+                            const double tv = fma(-s, vq[q + 1], sT[(q + 1) * LD + c]);
+                            sT[q * LD + c] = tv;
+                            if (q & 1)
+                                r2b = fma(tv, tv, r2b);
+                            else
+                                r2a = fma(tv, tv, r2a);
+                        }
+                        tl = -s * vq[P];
+                        sT[(P - 1) * LD + c] = tl;
+                    }
+                    const double r2 = fma(tl, tl, r2a + r2b);
+                    rel2 = r2 * bet_c * bet_c;   // (the stop test on squares: no sqrt on the chain)
+                    rel = sqrt(r2) * bet_c;
+                    sRes[c] = rel;
+                    sHist[m * P + c] = rel;
+                }
+                const double mx2 = warp_max(rel2);
+                K3P(3)
+                m_last = m;
+                if (mx2 < tol * tol) {
+                    stop = 1;
+                    break;
+                }
+                if (s_stop_after > 0 && m == s_stop_after - 1) {
+                    stop = 4;
                     break;
                 }
             }
-            // shrink: u_j removed -> column j of \bar H is deleted: identity reflector,
-            // R column zero (placeholder 1 on the diagonal for R_kk^{-1}), z_j = the tail's first
-            // (zero) row, m_j = 0
-            const bool gone = (am_k >> m) & 1u;
-            const int o = 2 * P + m;
-            const double alpha = sH[o * LD + m];
-            double x2 = 0.0;
-            for (int q = 1 + lane; q <= P; q += 32) x2 = fma(sH[(o + q) * LD + m], sH[(o + q) * LD + m], x2);
-            x2 = warp_sum(x2);
-            K3P(0)
-            const double xnorm = sqrt(x2);
-            // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
-            // v = x/(alpha - beta); one reciprocal 1/(beta (alpha - beta)) serves both quotients
-            double tj, beta, scl;
-            if (gone) {
-                tj = 0.0;
-                beta = 1.0;
-                scl = 0.0;
-            } else if (xnorm == 0.0) {
-                tj = 0.0;
-                beta = alpha;
-                scl = 0.0;
-            } else {
-                beta = -copysign(sqrt(fma(alpha, alpha, x2)), alpha);
-                const double s = alpha - beta;
-                const double inv = 1.0 / (beta * s);
-                tj = -s * s * inv;
-                scl = beta * inv;
+            if (cl) {
+    #pragma unroll
+                for (int r = 0; r < 2 * P; ++r) sH[(2 * P + r) * LD + c] = hc[r];
+                if constexpr (TREG) {
+    #pragma unroll
+                    for (int q = 0; q < P; ++q) sT[q * LD + c] = tc[q];
+                }
             }
-            if (!gone && fabs(beta) <= DBL_EPSILON * sHn[m]) {
-                stop = 3;
-                break;
-            }
-            if (lane == 0) sRd[m] = 1.0 / beta;   // 1 / r_jj for R_kk^{-1} (off the chain: lane 0 only)
-            K3P(1)
-            double* vj = sVb + m * (P + 2);
-            for (int q = lane; q <= P; q += 32) vj[q] = (q == 0) ? 1.0 : sH[(o + q) * LD + m] * scl;
-            if (lane == 0) vj[P + 1] = tj;
             __syncwarp();
-            for (int q = lane; q <= P; q += 32) sH[(o + q) * LD + m] = (q == 0) ? beta : 0.0;
-            double rel = 0.0;
-            K3P(2)
-            if (lane < P) {
-                const int c = lane;
-                // (the serial chain of this loop bounds K3b: each dot product runs as two interleaved
-                // partial sums -- half the dependent FMA latency per reflector)
-                if (c > m) {   // later columns of this block
-                    double* h = sH + o * LD + c;
+            K3P(4)
+            // ---- Ainv = R_kk^{-1} (columns past m_last: identity) (eqn.search-dir-comp):
+            //      column l of the back substitution in registers (lane l), in the same FMA order
+            if (cl) {
+                const int l = lane;
+                double ic[P];
+    #pragma unroll
+                for (int r = P - 1; r >= 0; --r) {
+                    double s = (r == l) ? 1.0 : 0.0;
+                    if (l <= m_last && r <= l) {
+    #pragma unroll
+                        for (int c2 = r + 1; c2 < P; ++c2)
+                            if (c2 <= l) s = fma(-sH[(2 * P + r) * LD + c2], ic[c2], s);
+                        ic[r] = s * sRd[r];
+                    } else {
+                        ic[r] = s;
+                    }
+                    sI[r * LD + l] = ic[r];
+                }
+            }
+        } else {
+            const unsigned am_k = s_am_k, am_k1 = s_am_k1;
+            for (int m = 0; m < P; ++m) {
+                const long long j = j0 + m;
+                if (j > maxit) {
+                    stop = 2;
+                    break;
+                }
+                // shrink: every index of the window j .. j+p-1 removed -> the basis is exhausted
+                // (lanes >= m of this block, lanes < m of the next)
+                if (am_k | am_k1) {
+                    const unsigned all = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
+                    const unsigned lo = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+                    if ((((am_k & ~lo) | (am_k1 & lo)) & all) == all) {
+                        stop = 5;
+                        break;
+                    }
+                }
+                // shrink: u_j removed -> column j of \bar H is deleted: identity reflector,
+                // R column zero (placeholder 1 on the diagonal for R_kk^{-1}), z_j = the tail's first
+                // (zero) row, m_j = 0
+                const bool gone = (am_k >> m) & 1u;
+                const int o = 2 * P + m;
+                const double alpha = sH[o * LD + m];
+                double x2 = 0.0;
+                for (int q = 1 + lane; q <= P; q += 32) x2 = fma(sH[(o + q) * LD + m], sH[(o + q) * LD + m], x2);
+                x2 = warp_sum(x2);
+                K3P(0)
+                // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
+                // v = x/(alpha - beta); one reciprocal 1/(beta (alpha - beta)) serves both quotients
+                double tj, beta, scl, rbeta;   // (rbeta = 1 / beta)
+                if (gone) {
+                    tj = 0.0;
+                    beta = 1.0;
+                    scl = 0.0;
+                    rbeta = 1.0;
+                } else if (x2 == 0.0) {   // (||x|| = 0)
+                    tj = 0.0;
+                    beta = alpha;
+                    scl = 0.0;
+                    rbeta = 1.0 / beta;
+                } else {
+                    beta = -copysign(sqrt(fma(alpha, alpha, x2)), alpha);
+                    const double s = alpha - beta;
+                    const double inv = 1.0 / (beta * s);
+                    tj = -s * s * inv;
+                    scl = beta * inv;
+                    rbeta = s * inv;
+                }
+                if (!gone && fabs(beta) <= DBL_EPSILON * sHn[m]) {
+                    stop = 3;
+                    break;
+                }
+                if (lane == 0) sRd[m] = rbeta;   // 1 / r_jj for R_kk^{-1}
+                K3P(1)
+                double* vj = sVb + m * (P + 2);
+                for (int q = lane; q <= P; q += 32) vj[q] = (q == 0) ? 1.0 : sH[(o + q) * LD + m] * scl;
+                if (lane == 0) vj[P + 1] = tj;
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    s_ready = m + 1;   // (warps 1-3 accumulate Q_k meanwhile)
+                }
+                for (int q = lane; q <= P; q += 32) sH[(o + q) * LD + m] = (q == 0) ? beta : 0.0;
+                double rel = 0.0;
+                K3P(2)
+                if (lane < P) {
+                    const int c = lane;
+                    // (the serial chain of this loop bounds K3b: each dot product runs as two interleaved
+                    // partial sums -- half the dependent FMA latency per reflector)
+                    if (c > m) {   // later columns of this block
+                        double* h = sH + o * LD + c;
+                        double s0 = 0.0, s1 = 0.0;
+    #pragma unroll
+                        for (int q = 0; q <= P; q += 2) {
+                            s0 = fma(vj[q], h[q * LD], s0);
+                            if (q + 1 <= P) s1 = fma(vj[q + 1], h[(q + 1) * LD], s1);
+                        }
+                        const double s = (s0 + s1) * tj;
+    #pragma unroll
+                        for (int q = 0; q <= P; ++q) h[q * LD] = fma(-s, vj[q], h[q * LD]);
+                    }
+                    // [T; 0] -> reflector j -> z_j^T = row 0, new tail = rows 1..p
                     double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-                    for (int q = 0; q <= P; q += 2) {
-                        s0 = fma(vj[q], h[q * LD], s0);
-                        if (q + 1 <= P) s1 = fma(vj[q + 1], h[(q + 1) * LD], s1);
+    #pragma unroll
+                    for (int q = 0; q < P; q += 2) {
+                        s0 = fma(vj[q], sT[q * LD + c], s0);
+                        if (q + 1 < P) s1 = fma(vj[q + 1], sT[(q + 1) * LD + c], s1);
                     }
                     const double s = (s0 + s1) * tj;
-#pragma unroll
-                    for (int q = 0; q <= P; ++q) h[q * LD] = fma(-s, vj[q], h[q * LD]);
+                    sZ[m * LD + c] = sT[c] - s;
+                    double r2a = 0.0, r2b = 0.0;
+    #pragma unroll
+                    for (int q = 0; q < P - 1; ++q) {
+                        const double tv = fma(-s, vj[q + 1], sT[(q + 1) * LD + c]);
+                        sT[q * LD + c] = tv;
+                        if (q & 1)
+                            r2b = fma(tv, tv, r2b);
+                        else
+                            r2a = fma(tv, tv, r2a);
+                    }
+                    const double tl = -s * vj[P];
+                    sT[(P - 1) * LD + c] = tl;
+                    const double r2 = fma(tl, tl, r2a + r2b);
+                    rel = sqrt(r2) * sBeta[c];
+                    sRes[c] = rel;
+                    sHist[m * P + c] = rel;
                 }
-                // [T; 0] -> reflector j -> z_j^T = row 0, new tail = rows 1..p
-                double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-                for (int q = 0; q < P; q += 2) {
-                    s0 = fma(vj[q], sT[q * LD + c], s0);
-                    if (q + 1 < P) s1 = fma(vj[q + 1], sT[(q + 1) * LD + c], s1);
+                const double mx = warp_max(rel);
+                K3P(3)
+                m_last = m;
+                if (mx < tol) {
+                    stop = 1;
+                    break;
                 }
-                const double s = (s0 + s1) * tj;
-                sZ[m * LD + c] = sT[c] - s;
-                double r2a = 0.0, r2b = 0.0;
-#pragma unroll
-                for (int q = 0; q < P - 1; ++q) {
-                    const double tv = fma(-s, vj[q + 1], sT[(q + 1) * LD + c]);
-                    sT[q * LD + c] = tv;
-                    if (q & 1)
-                        r2b = fma(tv, tv, r2b);
-                    else
-                        r2a = fma(tv, tv, r2a);
+                if (s_stop_after > 0 && m == s_stop_after - 1) {
+                    stop = 4;
+                    break;
                 }
-                const double tl = -s * vj[P];
-                sT[(P - 1) * LD + c] = tl;
-                const double r2 = fma(tl, tl, r2a + r2b);
-                rel = sqrt(r2) * sBeta[c];
-                sRes[c] = rel;
-                sHist[m * P + c] = rel;
-            }
-            const double mx = warp_max(rel);
-            K3P(3)
-            m_last = m;
-            if (mx < tol) {
-                stop = 1;
-                break;
-            }
-            if (s_stop_after > 0 && m == s_stop_after - 1) {
-                stop = 4;
-                break;
+                __syncwarp();
             }
             __syncwarp();
-        }
-        __syncwarp();
-        K3P(4)
-        // ---- Ainv = R_kk^{-1} (columns past m_last: identity) (eqn.search-dir-comp)
-        if (lane < P) {
-            const int l = lane;
-            for (int r = P - 1; r >= 0; --r) {
-                double s = (r == l) ? 1.0 : 0.0;
-                if (l <= m_last && r <= l) {
-                    for (int c = r + 1; c <= l; ++c) s = fma(-sH[(2 * P + r) * LD + c], sI[c * LD + l], s);
-                    sI[r * LD + l] = s * sRd[r];
-                } else {
-                    sI[r * LD + l] = s;
+            K3P(4)
+            // ---- Ainv = R_kk^{-1} (columns past m_last: identity) (eqn.search-dir-comp)
+            if (lane < P) {
+                const int l = lane;
+                for (int r = P - 1; r >= 0; --r) {
+                    double s = (r == l) ? 1.0 : 0.0;
+                    if (l <= m_last && r <= l) {
+                        for (int c = r + 1; c <= l; ++c) s = fma(-sH[(2 * P + r) * LD + c], sI[c * LD + l], s);
+                        sI[r * LD + l] = s * sRd[r];
+                    } else {
+                        sI[r * LD + l] = s;
+                    }
                 }
             }
         }
@@ -754,6 +957,45 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         if (lane == 0) {
             s_mlast = m_last;
             s_stop = stop;
+            __threadfence_block();
+            s_done = 1;
+        }
+    } else {
+        // ---- Q_k = H_{kp} ... H_{(k-1)p+1} on the block's 2p rows (f2), accumulated by warps 1-3 while
+        //      warp 0 generates the reflectors: the action of this block's reflectors (those
+        //      generated before a stop) for phase A of blocks k+1 and k+2; column c of Q_k is e_c with
+        //      the reflectors applied in order.  TPC consecutive lanes per column, each summing and
+        //      updating the rows t = sub (mod TPC) of a reflector's p+1, the partial dots combined by
+        //      xor shuffles inside the group
+        constexpr int TPC0 = (K3T - 32) / (2 * P);
+        constexpr int TPC = TPC0 >= 32 ? 32 : TPC0 >= 16 ? 16 : TPC0 >= 8 ? 8 : TPC0 >= 4 ? 4 : TPC0 >= 2 ? 2 : 1;
+        static_assert((K3T - 32) / TPC >= 2 * P, "one pass over the columns");
+        const int ct = tid - 32, c = ct / TPC, sub = ct % TPC;
+        const bool live = c < 2 * P;
+        double* q = sQ + (live ? c : 0);   // column c (stride LDQ; phase A is done with sQ)
+        if (live)
+            for (int r = sub; r < 2 * P; r += TPC) q[r * S::LDQ] = r == c ? 1.0 : 0.0;
+        __syncwarp();
+        for (int m = 0; m < P; ++m) {   // reflector m acts on block rows m .. m+p
+            while (s_ready <= m && !s_done) __nanosleep(32);
+            if (s_ready <= m) break;   // (warp 0 stopped before generating reflector m)
+            __threadfence_block();
+            const double* v = sVb + m * (P + 2);
+            double sd = 0.0;
+            if (live)
+#pragma unroll
+                for (int t = sub; t <= P; t += TPC) sd = fma(v[t], q[(m + t) * S::LDQ], sd);
+#pragma unroll
+            for (int o = 1; o < TPC; o <<= 1) sd += __shfl_xor_sync(FULL, sd, o);
+            sd *= v[P + 1];
+            if (live)
+#pragma unroll
+                for (int t = sub; t <= P; t += TPC) q[(m + t) * S::LDQ] = fma(-sd, v[t], q[(m + t) * S::LDQ]);
+            __syncwarp();
+        }
+        if (live) {
+            double* Qg = st->Qacc[k & 1];
+            for (int r = sub; r < 2 * P; r += TPC) Qg[r * (2 * MAXP) + c] = q[r * S::LDQ];
         }
     }
     __syncthreads();
@@ -792,40 +1034,6 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         }
     }
     trace_pt(tr, 6);
-    // ---- Q_k = H_{kp} ... H_{(k-1)p+1} on the block's 2p rows (f2): the accumulated action of this
-    //      block's reflectors (those generated before a stop), for phase A of blocks k+1 and k+2;
-    //      column c of Q_k is e_c with the reflectors applied in order (one thread per column)
-    {
-        // TPC threads per column (consecutive lanes): each sums and updates the rows t = sub (mod TPC)
-        // of a reflector's p+1, the partial dots combined by xor shuffles inside the group
-        constexpr int TPC0 = K3T / (2 * P);
-        constexpr int TPC = TPC0 >= 32 ? 32 : TPC0 >= 16 ? 16 : TPC0 >= 8 ? 8 : TPC0 >= 4 ? 4 : TPC0 >= 2 ? 2 : 1;
-        double* Qg = st->Qacc[k & 1];
-        for (int c0 = 0; c0 < 2 * P; c0 += K3T / TPC) {
-            const int c = c0 + tid / TPC, sub = tid % TPC;
-            const bool live = c < 2 * P;
-            double* q = sQ + (live ? c : 0);   // column c (stride LDQ; the phase-A buffer is free now)
-            if (live)
-                for (int r = sub; r < 2 * P; r += TPC) q[r * S::LDQ] = r == c ? 1.0 : 0.0;
-            __syncwarp();
-            for (int m = 0; m <= m_last; ++m) {   // reflector m acts on block rows m .. m+p
-                const double* v = sVb + m * (P + 2);
-                double s = 0.0;
-                if (live)
-#pragma unroll
-                    for (int t = sub; t <= P; t += TPC) s = fma(v[t], q[(m + t) * S::LDQ], s);
-#pragma unroll
-                for (int o = 1; o < TPC; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
-                s *= v[P + 1];
-                if (live)
-#pragma unroll
-                    for (int t = sub; t <= P; t += TPC) q[(m + t) * S::LDQ] = fma(-s, v[t], q[(m + t) * S::LDQ]);
-                __syncwarp();
-            }
-            if (live)
-                for (int r = sub; r < 2 * P; r += TPC) Qg[r * (2 * MAXP) + c] = q[r * S::LDQ];
-        }
-    }
     trace_pt(tr, 7);
     for (int t = tid; t < P; t += K3T) st->res[t] = sRes[t];
     if (s_hcap > 0)
