@@ -63,7 +63,7 @@ struct Kfn {  // per-p kernel table
     void (*k3b)(DevState*);
     void (*k4b)(K4bArgs);
     size_t smem1, smem2, smem3, smem4b;
-    int nt1, nt2, nt4b;
+    int nt1, nt2, nt4b, nt1pre;
     bool fused;   // K1 applies the M/X update of block k-2 in graph mode (DMMA K1)
     // f3 (prec_kernels.cuh): Z = L^-T V (backward), AV = L^-1 (A Z) (SpMM + forward), Y = L^-1 X
     void (*tbwd)(TriArgs);
@@ -90,6 +90,7 @@ Kfn make_kfn(int q) {
     f.smem_gram = f.smem_mat = 0;
     f.k1 = k1_spmm<P, true>;
     f.nt1 = NT;
+    f.nt1pre = NT;
     f.smem1 = K1Smem<P>::bytes;
     f.k1plain = k1_spmm<P, false>;
     f.k2 = k2_orth<P>;
@@ -114,6 +115,7 @@ Kfn make_kfn(int q) {
             else if constexpr (P <= 16) f.red2f = k_red2f_t<P, DM<P>::FR, DM<P>::NC>;
             if constexpr (P <= 16) f.fac2 = k_fac2<P, DM<P>::FR, DM<P>::NC>;
             f.smem1pre = K1DSmem<P, true>::bytes;
+            f.nt1pre = K1DSmem<P, true>::WARPS * 32;
             if constexpr (P >= 16) {
                 f.k1u = k1u_update<P>;
                 f.smem1u = UpdB<P>::bytes;
@@ -239,6 +241,7 @@ struct bminres_ctx {
     bool red2_fac = false;   // reduce2 factors the new block once (k_red2f)
     bool xdefer = false;   // fused updates defer X in pairs
     int nb1a = 0;
+    int k1a_ku = 0;   // K1a chunk length in row groups per warp (0: the kernel's default)
     double* AV = nullptr;
     bool pdl = true;   // programmatic dependent launch of the block-step kernels
     int gblocks = 3;   // block steps per captured graph (per solve: choose_gblocks)
@@ -527,7 +530,8 @@ void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
         // (BMINRES_K1A_CPS, experiment: fewer K1a CTAs per SM, so the update branch's CTA fits beside them)
         if (const char* ce = getenv("BMINRES_K1A_CPS")) oa = std::min(oa, std::max(1, atoi(ce)));
         h->nb1a = h->n_sm * std::max(1, oa) - 1;   // one CTA slot left for K3b (side stream)
-        const int o1p = std::min(cap, occ_of((const void*)h->kf.k1pre, h->kf.nt1, h->kf.smem1pre));
+        if (const char* ke = getenv("BMINRES_K1A_KU")) h->k1a_ku = std::max(0, atoi(ke));
+        const int o1p = std::min(cap, occ_of((const void*)h->kf.k1pre, h->kf.nt1pre, h->kf.smem1pre));
         h->nb1 = (std::min(NB_MAX, h->n_sm * o1p) - (o1p > 1 ? h->csz : 0)) / h->csz * h->csz;
     }
     // BMINRES_WS (experiment): the warp-specialised K1 in place of K1a + K1 on a single rank (a row
@@ -913,6 +917,7 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
         // (BMINRES_K1A_DYN, experiment: chunks in order from st->k1a_ctr -- for K1a beside the update
         // branch; alone it measured slower, 3.09 vs 2.63 ms at config 4)
         aa.dyn = getenv("BMINRES_K1A_DYN") ? 1 : 0;
+        aa.ku = h->k1a_ku;
         cudaStream_t keep = h->stream;
         h->stream = s;
         auto k1a_launch = [&](const K1Args& args) {
@@ -955,7 +960,7 @@ void launch_k1(bminres_ctx* h, cudaStream_t s, const StepPtrs& sp, long long n, 
         if (upd_branch) CK(cudaStreamWaitEvent(s, h->ev_u1, 0));   // the update read V_{k-2}
         {
             TimeMark tm(h, fuse ? PH_EPI_FUSED : PH_EPI);
-            launch_cluster(h, h->kf.k1pre, h->nb1, h->kf.nt1, h->kf.smem1pre, a, "k1_dmma(split)");
+            launch_cluster(h, h->kf.k1pre, h->nb1, h->kf.nt1pre, h->kf.smem1pre, a, "k1_dmma(split)");
         }
         h->stream = keep;
         launch_reduce(h, s, 1, k);

@@ -630,10 +630,16 @@ struct UpdB {
     // p = 32: sixteen warps of 8-row tiles (single-staged: shared-memory budget) -- twice the warps
     // in flight per SM of sixteen-row tiles, at 82 registers (config 4: 4.83 -> 4.56 ms per launch;
     // 8 rows double-staged: 5.13 ms); p = 16: eight warps of 16 rows, double-staged
-    static constexpr int WARPS = P >= 32 ? 16 : 8;
+#ifndef K1U_WARPS32
+#define K1U_WARPS32 16
+#endif
+#ifndef K1U_NS32
+#define K1U_NS32 1
+#endif
+    static constexpr int WARPS = P >= 32 ? K1U_WARPS32 : 8;
     static constexpr int TRU = P >= 32 ? 8 : 16;
     static constexpr int MC = TRU / 8;
-    static constexpr int NS = P >= 32 ? 1 : 2;     // cp.async stages per warp (shared-memory budget)
+    static constexpr int NS = P >= 32 ? K1U_NS32 : 2;     // cp.async stages per warp (shared-memory budget)
     static constexpr int RS = P + 4;
     static constexpr int TILE = TRU * RS;
     static constexpr int SLOT = 4 * TILE;          // V_b, M_{b-2} (-> M_b), M_{b-1}, X
@@ -802,6 +808,9 @@ __global__ void __launch_bounds__(UpdB<P>::WARPS * 32, 1) k1u_update(K1Args a) {
 // Order: CTA chunks of WARPS*KU consecutive row groups, round-robin over the CTAs -- neighbouring
 // rows stay in one SM's L1 and all SMs sweep the matrix together, so far (z-plane) neighbours are
 // re-read from L2.
+#ifndef K1A_STREAM
+#define K1A_STREAM 0
+#endif
 template <int P>
 struct K1aCfg {
     // a lane gathers 32 bytes of a row per entry (one 256-bit load, LDG.E.ENL2.256) when 4 | p:
@@ -852,7 +861,7 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
     // rows: all n, or (row partition, halo overlap) the interior range / the boundary rows around it
     const long long nr = a.nrows >= 0 ? a.nrows : a.n;
     const long long ngroups = (nr + RPW - 1) / RPW;
-    const long long chunk = (long long)nw * KU;
+    const long long chunk = (long long)nw * (a.ku > 0 ? a.ku : KU);
     // chunk order: static round robin over the CTAs, or (dyn) taken in increasing order from a
     // counter by whichever CTA is resident -- all resident CTAs then sweep the rows together even
     // when some become resident late (K1a running beside the update kernel), so the far stencil
@@ -889,8 +898,15 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
 #pragma unroll
             for (int t = 0; t < CH; ++t) {
                 const bool pr = kb + t < r1;
+#if K1A_STREAM
+                // A is read once per block step: evict-first, so it does not push the gathered V_k
+                // rows (re-read as stencil neighbours planes later) out of L2
+                c[t] = pr ? __ldcs(a.col + kb + t) : -1;
+                av[t] = pr ? __ldcs(a.val + kb + t) : 0.0;
+#else
                 c[t] = pr ? __ldg(a.col + kb + t) : -1;
                 av[t] = pr ? __ldg(a.val + kb + t) : 0.0;
+#endif
             }
             double xv[CH][VEC];
 #pragma unroll
@@ -912,8 +928,14 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
         if (live) {
             double* y = a.Y + i * P + c0;   // Y = the AV panel
             if constexpr (VEC == 4) {
+#if K1A_STREAM
+                // (the AV panel is read once, by K1's epilogue: streaming stores)
+                __stcs(reinterpret_cast<double2*>(y), make_double2(acc[0], acc[1]));
+                __stcs(reinterpret_cast<double2*>(y + 2), make_double2(acc[2], acc[3]));
+#else
                 *reinterpret_cast<double2*>(y) = make_double2(acc[0], acc[1]);
                 *reinterpret_cast<double2*>(y + 2) = make_double2(acc[2], acc[3]);
+#endif
             } else {
                 stv<VEC>(y, acc);
             }
@@ -936,7 +958,13 @@ template <int P, bool PRE = false>
 struct K1DSmem {
     // p = 32: one 512-thread CTA per SM (16 warps, <= 128 registers) instead of one 256-thread
     // CTA at 209 registers -- the gathers need the warps; the fused update single-staged
-    static constexpr int WARPS = P >= 32 ? 16 : 8;
+#ifndef K1PRE_WARPS32
+#define K1PRE_WARPS32 16
+#endif
+#ifndef K1PRE_NSP32
+#define K1PRE_NSP32 1
+#endif
+    static constexpr int WARPS = (PRE && P >= 32) ? K1PRE_WARPS32 : (P >= 32 ? 16 : 8);
 #ifndef K1_DISJ
 #define K1_DISJ 1
 #endif
@@ -946,11 +974,18 @@ struct K1DSmem {
     static constexpr bool DISJ = K1_DISJ && !PRE && P <= 16;
     static constexpr int UNS = (P >= 32 || DISJ) ? 1 : 2;    // cp.async stages of the fused update
     // split mode (PRE): the A V_k rows are staged like the panels; two stages where they fit
-    static constexpr int NSP = (PRE && P < 32) ? 2 : 1;
+    static constexpr int NSP = PRE ? (P < 32 ? 2 : K1PRE_NSP32) : 1;
     static constexpr int pipe = WARPS * 3 * DM<P>::TILE * NSP;   // V_k, V_{k-1} tiles + A V tile per warp
     static constexpr int scr = prologue_scratch<P>() + 2 * P * P;
     static constexpr int upd = UpdSmem<P, WARPS, UNS>::doubles;   // the update runs first, then the SpMM
-    static constexpr int region = DISJ ? pipe + scr + upd : ((pipe + scr > upd) ? pipe + scr : upd);
+#ifndef K1PRE_OVL
+#define K1PRE_OVL 0
+#endif
+    // (split mode, p = 32, K1PRE_OVL: the prologue scratch overlays the pipeline, whose first tiles
+    // are then issued after the prologue -- room for a second stage)
+    static constexpr bool OVL = PRE && P >= 32 && K1PRE_OVL;
+    static constexpr int region = OVL ? ((pipe > scr ? pipe : scr) > upd ? (pipe > scr ? pipe : scr) : upd)
+                                      : DISJ ? pipe + scr + upd : ((pipe + scr > upd) ? pipe + scr : upd);
     static constexpr size_t bytes = sizeof(double) * (2 * DM<P>::FR + region + P * P + P);
 };
 
@@ -964,13 +999,13 @@ struct K1DSmem {
 // q+2 are loaded.  The SpMM of the warp's first tile runs before the prologue (the Cholesky of
 // the previous block's Gram), which only the epilogue needs.
 template <int P, bool PRE = false>
-__global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dmma(K1Args a) {
+__global__ void __launch_bounds__(K1DSmem<P, PRE>::WARPS * 32, P <= 16 ? 2 : 1) k1_dmma(K1Args a) {
     using D = DM<P>;
     // gather mapping: 32 bytes per lane and entry (256-bit loads) at p = 8 and 16 (config 2:
     // 108.8k -> 112.8k it/s; config 3: 86k -> 95k); 16 bytes at p = 32 (spills at 128 registers)
     using C = K1Gather<P>;
     using KS = K1DSmem<P, PRE>;
-    constexpr int WARPS = K1DSmem<P>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
+    constexpr int WARPS = K1DSmem<P, PRE>::WARPS, TR = D::TR, RS = D::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int E = P * P + P;
     // CSR entries per gather batch: 7 at p = 8 (a 7-point stencil row in one batch, 28 doubles in
@@ -988,7 +1023,7 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
     double* fT = dynd1;            // Tr_k
     double* fD = fT + FR;          // -(Tr_{k-1} C_{k-1}^T)
     double* pipe = fD + FR;
-    double* scr = pipe + KS::pipe;
+    double* scr = KS::OVL ? pipe : pipe + KS::pipe;
     double* sAcc = pipe + KS::region;
     // each CTA owns a contiguous slab of tiles (its warps interleave inside it), so the
     // gathers of neighbouring rows (stencil offsets +-1, +-nx) hit this SM's L1
@@ -1151,21 +1186,30 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
             const bool rok = row < a.n;
             double w[NC][2];
 #pragma unroll
-            for (int nc = 0; nc < NC; ++nc) {
-                w[nc][0] = w[nc][1] = 0.0;
-                // W = (A V_k) Tr_k = A U_k, the raw candidates; ||A u_j||^2 (C14).  Tr_k = C_{k-1}^{-1}
-                // (or I) is upper triangular: k-chunks below the column block are zero
+            for (int nc = 0; nc < NC; ++nc) w[nc][0] = w[nc][1] = 0.0;
+            // W = (A V_k) Tr_k = A U_k, the raw candidates; ||A u_j||^2 (C14).  Tr_k = C_{k-1}^{-1}
+            // (or I) is upper triangular: k-chunks below the column block are zero.  k-chunks
+            // outermost: one A-fragment load feeds every column block (per output the DMMAs still
+            // accumulate in increasing kc, the Tr_k products before the D products)
 #pragma unroll
-                for (int kc = 0; kc < KC; ++kc)
-                    if (kc <= 2 * nc + 1)
-                        dmma(w[nc][0], w[nc][1], tAV[(r0 + fr) * RS + kc * 4 + fc], fT[(kc * NC + nc) * 32 + lane]);
+            for (int kc = 0; kc < KC; ++kc) {
+                const double aA = tAV[(r0 + fr) * RS + kc * 4 + fc];
+#pragma unroll
+                for (int nc = 0; nc < NC; ++nc)
+                    if (kc <= 2 * nc + 1) dmma(w[nc][0], w[nc][1], aA, fT[(kc * NC + nc) * 32 + lane]);
+            }
+#pragma unroll
+            for (int nc = 0; nc < NC; ++nc) {
                 om[nc][0] = fma(w[nc][0], w[nc][0], om[nc][0]);
                 om[nc][1] = fma(w[nc][1], w[nc][1], om[nc][1]);
-                // W -= U_{k-1} C_{k-1}^T = V_{k-1} D  (h_{i,j} = h_{j,i})
-                if (has_prev) {
+            }
+            // W -= U_{k-1} C_{k-1}^T = V_{k-1} D  (h_{i,j} = h_{j,i})
+            if (has_prev) {
 #pragma unroll
-                    for (int kc = 0; kc < KC; ++kc)
-                        dmma(w[nc][0], w[nc][1], tP[(r0 + fr) * RS + kc * 4 + fc], fD[(kc * NC + nc) * 32 + lane]);
+                for (int kc = 0; kc < KC; ++kc) {
+                    const double aP = tP[(r0 + fr) * RS + kc * 4 + fc];
+#pragma unroll
+                    for (int nc = 0; nc < NC; ++nc) dmma(w[nc][0], w[nc][1], aP, fD[(kc * NC + nc) * 32 + lane]);
                 }
             }
             __syncwarp();
@@ -1210,11 +1254,17 @@ __global__ void __launch_bounds__(K1DSmem<P>::WARPS * 32, P <= 16 ? 2 : 1) k1_dm
         pdl_wait();   // A V_k (k1a) and, through it, red2 of block k-1 are complete
         if (blockIdx.x == 0 && threadIdx.x == 0) st->k1a_ctr[0] = st->k1a_ctr[1] = 0ull;   // for K1a(k+1)
         trace_pt(tr, 2);
+        if constexpr (!KS::OVL) {
 #pragma unroll
-        for (int s = 0; s < NSP; ++s) stage3(s);   // the first tiles stream in during the prologue
+            for (int s = 0; s < NSP; ++s) stage3(s);   // the first tiles stream in during the prologue
+        }
         if (!prologue()) {
             cp_wait<0>();
             return;
+        }
+        if constexpr (KS::OVL) {
+#pragma unroll
+            for (int s = 0; s < NSP; ++s) stage3(s);
         }
         trace_pt(tr, 3);
         for (long long it = 0; it < my_tiles; ++it) {

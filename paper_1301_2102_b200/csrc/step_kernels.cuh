@@ -53,6 +53,7 @@ struct K1Args {
     // for v < nrows; nrows < 0: all n rows
     long long r0 = 0, nrows = -1, gap_at = -1, gap = 0;
     int dyn = 0;          // K1a: CTA chunks taken from st->k1a_ctr[dyn - 1] in order (0: static round robin)
+    int ku = 0;           // K1a: row groups per warp per CTA chunk (0: K1aCfg<P>::KU)
 };
 
 template <int P>

@@ -14,7 +14,7 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 CMD="python bench.py --steps 1 --warmup 1 --iters 400 --no-kernel-timing --no-e2e --no-cpu-baseline"
 $CMD > $OUT/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1; echo "ncu-launch rc=$?"
 if [ "$FULL" = full ]; then
-  CMD2="python bench.py --steps 1 --warmup 1 --iters 800 --no-kernel-timing --no-e2e --no-cpu-baseline"
+  CMD2="python bench.py --steps 1 --warmup 1 --iters 800 --no-kernel-timing --no-e2e --no-cpu-baseline --secondary none --time-to-tol none --precond none"
   $CMD2 > $OUT/plain2.log 2>&1 && timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k1_|k2_|k3b_|k4b_|k_reduce" -s 300 -c 12 \
     -o $OUT/full $CMD2 > $OUT/ncu_full.log 2>&1; echo "ncu-full rc=$?"
 fi
