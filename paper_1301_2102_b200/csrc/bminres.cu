@@ -1639,6 +1639,7 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
     // reduce2 factors the new block once (a row partition: k_fac2 after the allreduce of the totals)
     h->red2_fac = h->kf.red2f && !getenv("BMINRES_NO_RED2F");
     init.red2_fac = h->red2_fac ? 1 : 0;
+    init.fac_blk = -1;
     init.fac_bad = 0;
     init.given_blk = -1;
     init.policy = o.policy;

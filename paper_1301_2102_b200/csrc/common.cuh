@@ -89,6 +89,7 @@ struct DevState {
     // coef_k in the state, and K1(k+1)'s fragments of Tr_{k+1} and -(Tr_k C_k^T) below; fac_bad:
     // breakdown / cancellation of the block (published as by K1's own prologue)
     int red2_fac, fac_bad;
+    long long fac_blk;   // the block whose C_k (Ck[k & 1]) / fac_bad reduce2 (or k_fac2) last stored
     // block-size reduction ("shrink", policy 1): lane m of every block
     // >= absent_from[m] holds a removed (zero) basis vector -- A 0 = 0, so a removed lane stays
     // removed; KINF: present.  The block form keeps p columns; removed ones are zero.
@@ -617,6 +618,7 @@ __device__ void red2_factor(DevState* st, int par, double* sm, unsigned long lon
     if (bad) {
         if (threadIdx.x == 0) {
             st->fac_bad = 1;
+            st->fac_blk = k;
             publish_breakdown(st, k);
         }
         trace_pt(tr, 5);
@@ -634,7 +636,10 @@ __device__ void red2_factor(DevState* st, int par, double* sm, unsigned long lon
         st->fT[t] = sCi[r * P + c];
         st->fD[t] = -sD[r * P + c];
     }
-    if (threadIdx.x == 0) st->fac_bad = 0;
+    if (threadIdx.x == 0) {
+        st->fac_bad = 0;
+        st->fac_blk = k;   // (K3b(k), launched after this kernel completes, loads C_k instead of refactoring)
+    }
     trace_pt(tr, 5);
 }
 

@@ -532,6 +532,11 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         bool bad = false;
         if (s_given) {
             load_pp<P>(sCc, st->Ck[par]);
+        } else if (st->red2_fac && st->fac_blk == k) {
+            // reduce2 (k_red2f / k_fac2) already factored these totals with the same code
+            // (factor_block): its C_k, bitwise what this CTA would compute (p = 16: 6.7 -> ~1 us)
+            bad = st->fac_bad != 0;
+            if (!bad) load_pp<P>(sCc, st->Ck[par]);
         } else {
             const int Q = st->q_live;
             double* sRed = scr;
