@@ -644,7 +644,13 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 for (int q = 0; q < P; ++q) tc[q] = cl ? sT[q * LD + c] : 0.0;
             }
             const double bet_c = cl ? sBeta[c] : 0.0;
-    #pragma unroll
+            // The window of reflector m (frame rows 2p+m .. 3p+m) is always hc[0 .. p]: after each
+            // reflector row m is final -- stored -- and the column shifts up by one row.  So the
+            // reflector loop indexes the registers with compile-time offsets only and stays a loop
+            // (fully unrolled it was 19k instructions, fetched cold on every launch: config 3's K3b
+            // took 86 us instead of 37)
+            int sh = 0;   // rows stored (and shifted out)
+    #pragma unroll 1
             for (int m = 0; m < P; ++m) {
                 const long long j = j0 + m;
                 if (j > maxit) {
@@ -670,11 +676,11 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
     #pragma unroll
                 for (int q = 1; q <= P; ++q) {
                     if (q & 1)
-                        x2a = fma(hc[m + q], hc[m + q], x2a);
+                        x2a = fma(hc[q], hc[q], x2a);
                     else
-                        x2b = fma(hc[m + q], hc[m + q], x2b);
+                        x2b = fma(hc[q], hc[q], x2b);
                 }
-                const double alpha = __shfl_sync(FULL, hc[m], m);
+                const double alpha = __shfl_sync(FULL, hc[0], m);
                 const double x2 = __shfl_sync(FULL, x2a + x2b, m);
                 K3P(0)
                 // dlarfg (C20): beta = -sign(alpha) ||(alpha, x)||, tau = (beta - alpha)/beta,
@@ -706,7 +712,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                 double vq[P + 1];   // v = (1, x scl)
                 vq[0] = 1.0;
     #pragma unroll
-                for (int q = 1; q <= P; ++q) vq[q] = __shfl_sync(FULL, hc[m + q], m) * scl;
+                for (int q = 1; q <= P; ++q) vq[q] = __shfl_sync(FULL, hc[q], m) * scl;
                 if (lane == 0) {
                     sRd[m] = rbeta;   // 1 / r_jj for R_kk^{-1}
                     double* vj = sVb + m * (P + 2);
@@ -722,14 +728,14 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                     if (c > m) {   // later columns of this block
                         double sp[4] = {0.0, 0.0, 0.0, 0.0};
     #pragma unroll
-                        for (int q = 0; q <= P; ++q) sp[q & 3] = fma(vq[q], hc[m + q], sp[q & 3]);
+                        for (int q = 0; q <= P; ++q) sp[q & 3] = fma(vq[q], hc[q], sp[q & 3]);
                         const double s = ((sp[0] + sp[1]) + (sp[2] + sp[3])) * tj;
     #pragma unroll
-                        for (int q = 0; q <= P; ++q) hc[m + q] = fma(-s, vq[q], hc[m + q]);
+                        for (int q = 0; q <= P; ++q) hc[q] = fma(-s, vq[q], hc[q]);
                     } else if (c == m) {   // the pivot column becomes (beta, 0, ..., 0)
-                        hc[m] = beta;
+                        hc[0] = beta;
     #pragma unroll
-                        for (int q = 1; q <= P; ++q) hc[m + q] = 0.0;
+                        for (int q = 1; q <= P; ++q) hc[q] = 0.0;
                     }
                     // [T; 0] -> reflector j -> z_j^T = row 0, new tail = rows 1..p
                     double s0 = 0.0, s1 = 0.0, r2a = 0.0, r2b = 0.0, tl;
@@ -777,6 +783,12 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
                     sRes[c] = rel;
                     sHist[m * P + c] = rel;
                 }
+                // row m of every column is final: store it, shift the window up
+                if (cl) sH[(2 * P + m) * LD + c] = hc[0];
+    #pragma unroll
+                for (int r = 0; r < 2 * P - 1; ++r) hc[r] = hc[r + 1];
+                hc[2 * P - 1] = 0.0;
+                sh = m + 1;
                 const double mx2 = warp_max(rel2);
                 K3P(3)
                 m_last = m;
@@ -791,7 +803,8 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
             }
             if (cl) {
     #pragma unroll
-                for (int r = 0; r < 2 * P; ++r) sH[(2 * P + r) * LD + c] = hc[r];
+                for (int r = 0; r < 2 * P; ++r)
+                    if (sh + r < 2 * P) sH[(2 * P + sh + r) * LD + c] = hc[r];
                 if constexpr (TREG) {
     #pragma unroll
                     for (int q = 0; q < P; ++q) sT[q * LD + c] = tc[q];

@@ -10,8 +10,12 @@ os.environ["BMINRES_TRACE"] = launch
 os.environ["BMINRES_TRACE_FILE"] = f
 import torch, synth
 from paper_1301_2102_b200 import DeviceCsr, Solver
-A = synth.laplacian_3d(40, shift=3.0)
-B = synth.gaussian_rhs(A.n, p, seed=1)
+if os.environ.get("K3B_CFG3"):   # config 3's problem (2-D 512^2, dependent right-hand sides, eps = 0)
+    pr = synth.config(3)
+    A, B = pr.A, pr.B
+else:
+    A = synth.laplacian_3d(40, shift=3.0)
+    B = synth.gaussian_rhs(A.n, p, seed=1)
 dA, dB = DeviceCsr.from_host(A, "cuda:0"), torch.from_numpy(B).to("cuda:0")
 res = []
 for graphs in (False, True):
