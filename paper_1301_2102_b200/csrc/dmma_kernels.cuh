@@ -269,8 +269,11 @@ struct K2DSmem {
     // outermost so every A fragment feeds NC DMMAs -- at p = 32 the 8-row version was bound by
     // shared-memory bandwidth, two LDS.64 per DMMA)
     static constexpr int TR = 16, MC = TR / 8, RS = DM<P>::RS, TILE = TR * RS;
+#ifndef K2_NS32
+#define K2_NS32 2
+#endif
     static constexpr int WARPS = P >= 32 ? 4 : (P >= 16 ? 8 : 4);
-    static constexpr int NS = P >= 16 ? 2 : NSTAGE;   // cp.async stages (shared-memory budget)
+    static constexpr int NS = P >= 32 ? K2_NS32 : (P >= 16 ? 2 : NSTAGE);   // cp.async stages (shared-memory budget)
     static constexpr int RSQ = 12;                        // pool tile row stride (8 columns + pad)
     static constexpr int TQ = TR * RSQ;
     static constexpr int STG = 2 * TILE + TQ;         // one stage of one warp

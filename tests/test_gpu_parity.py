@@ -677,3 +677,30 @@ def test_full_size_solve_to_tol(cfg, eps):
         assert g["status"] == "OK" and g["p"] == P.p and g["n"] == P.n
         assert_hist_close(r.history, np.array(g["history_first50"]))
         _count_gate(r.iterations, g, P.tol)
+
+
+@pytest.mark.parametrize("p", [8, 16])
+def test_reduce2_factorisation_reused_bitwise(p, monkeypatch):
+    """reduce2 factors each new block once (k_red2f: C_k, Tr_{k+1}, D) and K3b(k) loads its C_k
+    (fac_blk = k) instead of refactoring; BMINRES_NO_RED2F switches both K1 and K3b back to
+    factoring the same totals themselves with the same factor_block code.  The solves agree
+    bitwise -- a plain 3-D run to convergence and one with a mid-solve exact dependence (j = 9:
+    the block's factorisation fails, fac_bad, the column path runs, then reduce2 factors again)."""
+    A = synth.laplacian_3d(14, shift=2.2)
+    rng = np.random.default_rng(p)
+    B1 = rng.standard_normal((A.n, p))
+    D = synth.csr_to_dense(A)
+    b = rng.standard_normal(A.n)
+    B2 = np.stack([b, D @ (D @ b)] + [rng.standard_normal(A.n) for _ in range(p - 2)], axis=1)
+    for B, tol in ((B1, 1e-10), (B2, 1e-10)):
+        base = gpu_solve(A, B, tol=tol, maxit=1200)
+        monkeypatch.setenv("BMINRES_NO_RED2F", "1")
+        try:
+            alt = gpu_solve(A, B, tol=tol, maxit=1200)
+        finally:
+            monkeypatch.delenv("BMINRES_NO_RED2F")
+        assert base.status_name == alt.status_name and base.iterations == alt.iterations
+        assert [(e["j"], e["col"], e["action"]) for e in base.events] == \
+               [(e["j"], e["col"], e["action"]) for e in alt.events]
+        np.testing.assert_array_equal(base.history, alt.history)
+        np.testing.assert_array_equal(base.X, alt.X)
