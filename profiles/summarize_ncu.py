@@ -27,6 +27,9 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_sb"),
     ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_sb"),
     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA pipe busy %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem wavefronts %"),
 ]
 KNAMES = {"k1_dmma": "spmm_fused", "k2_row": "orth", "k2_dmma": "orth", "k_reduce": "reduce", "k1_spmm": "spmm", "k2_orth": "orth", "k3b_smallqr": "smallqr", "k4a_basis": "basis",
           "k4b_update": "update", "k3_smallqr": "smallqr", "k4_update": "update"}
@@ -38,7 +41,10 @@ def short(name):
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):   # an `ncu -i R --page raw --csv` export
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
@@ -55,7 +61,7 @@ def to_us(v, unit):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--rep", required=True)
+    ap.add_argument("--rep", required=True, help=".ncu-rep, or its --page raw --csv export")
     ap.add_argument("--launches")
     ap.add_argument("--workload", default="cfg2_lap3d_64_shift3")
     ap.add_argument("--traffic-json")
