@@ -504,9 +504,18 @@ __device__ __forceinline__ void k2_stopped(DevState* st) {
 }
 
 // Publish a breakdown of block b (main branch stops; the host runs the column path).
-__device__ __forceinline__ void publish_breakdown(DevState* st, long long b) {
+//
+// run_main is cleared only by main-branch kernels (reduce2's factorisation, K1's prologue), so every
+// main-branch kernel reads it after griddepcontrol.wait with its predecessors complete and all CTAs
+// of a launch see the same value -- the CTAs of a cluster must take the same early exit, since a
+// reducing kernel's leader reads its peers' shared memory in cluster_partials.  K3b (side stream)
+// reports its breakdowns to the host only (side_only): had it cleared run_main, the flag could
+// change between two CTAs' reads of one launch, and a cluster split that way read an exited CTA's
+// shared memory ("unspecified launch failure": p = 8 with K1 / K3b factoring, BMINRES_NO_RED2F, a
+// mid-solve dependence; test_reduce2_factorisation_reused_bitwise).
+__device__ __forceinline__ void publish_breakdown(DevState* st, long long b, bool side_only = false) {
     st->need_slow = 1;
-    st->run_main = 0;
+    if (!side_only) st->run_main = 0;
     st->bd_at = b;
     st->hflags->bd_at = b;
     st->hflags->need_slow = 1;

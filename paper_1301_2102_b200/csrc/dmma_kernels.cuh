@@ -295,10 +295,6 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
     constexpr int WARPS = S::WARPS, TR = S::TR, MC = S::MC, RS = S::RS, KC = D::KC, NC = D::NC, FR = D::FR;
     constexpr int RSQ = S::RSQ, TILE = S::TILE;
     DevState* st = a.st;
-    if (!st->run_main) {
-        k2_stopped(st);
-        return;
-    }
     unsigned long long* tr = trace_begin(st, TR_K2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int fr = lane >> 2, fc = lane & 3;
@@ -334,6 +330,11 @@ __global__ void __launch_bounds__(K2DSmem<P>::WARPS * 32) k2_dmma(K2Args a) {
 #pragma unroll
     for (int s = 0; s < S::NS - 1; ++s) issue(s, s);
     pdl_wait();   // red1 (reduce1) is ready
+    if (!st->run_main) {   // (stopped; uniform over the launch: see publish_breakdown)
+        cp_wait<0>();
+        k2_stopped(st);
+        return;
+    }
     trace_pt(tr, 1);
     {
         // G = Tr_k^T (V_k^T W) from K1's partials; G_s: lower triangle mirrored (the paper
@@ -1090,7 +1091,9 @@ __global__ void __launch_bounds__(K1DSmem<P, PRE>::WARPS * 32, P <= 16 ? 2 : 1) 
         }
     }
     trace_pt(tr, 1);
-    if (!st->run_main) return;
+    // (the stopped-main-branch exit is taken after griddepcontrol.wait, where every CTA reads the
+    // same run_main -- see publish_breakdown; the first SpMM tile below only reads V_k into
+    // shared memory)
     const bool has_prev = st->k_main > 1;
     double g[NC][NC][2], om[NC][2];
 #pragma unroll
@@ -1255,6 +1258,7 @@ __global__ void __launch_bounds__(K1DSmem<P, PRE>::WARPS * 32, P <= 16 ? 2 : 1) 
             cp_commit();
         };
         pdl_wait();   // A V_k (k1a) and, through it, red2 of block k-1 are complete
+        if (!st->run_main) return;
         if (blockIdx.x == 0 && threadIdx.x == 0) st->k1a_ctr[0] = st->k1a_ctr[1] = 0ull;   // for K1a(k+1)
         trace_pt(tr, 2);
         if constexpr (!KS::OVL) {
@@ -1283,6 +1287,10 @@ __global__ void __launch_bounds__(K1DSmem<P, PRE>::WARPS * 32, P <= 16 ? 2 : 1) 
         long long q = 0;
         for (; q < G && q < nq; ++q) process_group(q);
         pdl_wait();   // red2 (reduce2 of block k-1) is ready
+        if (!st->run_main) {
+            cp_wait<0>();
+            return;
+        }
         trace_pt(tr, 2);
         if (!prologue()) {
             cp_wait<0>();
@@ -1408,8 +1416,8 @@ __global__ void __launch_bounds__(K1WS<P>::THREADS, 1) k1_ws(K1Args a) {
     double* ring = fD + FR;         // NSLOT x T x RS: A V_k rows, overwritten by W rows
     double* stg = ring + S::ring;   // consumer staging
     double* sAcc = fD + FR + S::body;
-    if (!st->run_main) return;
     pdl_wait();   // V_k (K2 of block k-1), the reduce2 totals / fragments, the update kernel are complete
+    if (!st->run_main) return;
     trace_pt(tr, 2);
     const bool has_prev = st->k_main > 1;
     // ---- prologue (all threads): C_{k-1}, Tr_k, D (the scratch overlays the ring)

@@ -98,10 +98,6 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
     using S = K2RSmem<P>;
     constexpr int NG = P * (P + 1) / 2;
     DevState* st = a.st;
-    if (!st->run_main) {
-        k2_stopped(st);
-        return;
-    }
     unsigned long long* tr = trace_begin(st, TR_K2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int Q = st->q_live, qf = st->q_first, qc = st->pool_cap;
@@ -137,6 +133,14 @@ __global__ void __launch_bounds__(RT, 3) k2_row(K2Args a) {
         for (int s = 0; s < RNS - 1; ++s) issue(s);   // W (K1 completed before reduce1) streams in
     trace_pt(tr, 1);
     pdl_wait();   // red1 (reduce1) is ready
+    // stopped main branch (read after the wait: uniform over the launch, see publish_breakdown);
+    // the prefetched stages land before the CTA exits
+    if (!st->run_main) {
+        for (int s = 0; s < RNS - 1; ++s)
+            if (s < my_tiles) mbar_wait(&bar[s], 0u);
+        k2_stopped(st);
+        return;
+    }
     trace_pt(tr, 2);
     {
         // G = Tr_k^T (V_k^T W) from K1's partials; E = -(Tr_k G_s), F = -(Tr_k coef_{k-1})

@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(K3T) k3b_smallqr(DevState* st) {
         if (bad) {   // breakdown of block k: the host runs the column path, then re-runs this block
             if (tid == 0) {
                 st->side_go = 0;
-                publish_breakdown(st, k);
+                publish_breakdown(st, k, true);   // (to the host; the main branch finds it itself)
             }
             return;
         }
