@@ -704,3 +704,34 @@ def test_reduce2_factorisation_reused_bitwise(p, monkeypatch):
                [(e["j"], e["col"], e["action"]) for e in alt.events]
         np.testing.assert_array_equal(base.history, alt.history)
         np.testing.assert_array_equal(base.X, alt.X)
+
+
+@pytest.mark.parametrize("p,use_graphs", [(16, True), (32, True), (32, False)])
+def test_mid_solve_breakdown_large_p(p, use_graphs, monkeypatch):
+    """An exact dependence in the first block (B = [b, A^2 b, ...]: the candidate from A u_1
+    deflates at j = p + 1) at p = 16 and 32, solved to tol 1e-8: at p = 32 K1's prologue factors
+    each block (no reduce2 factorisation) and K3b on the side stream finds the same breakdown --
+    the case where K3b used to clear run_main under a running K2.  Against the
+    oracle: status, counts (+-2%), events, histories (1e-9 over 50 iterations), true residual
+    <= tol, X; p = 16 also bitwise with reduce2's factorisation switched off."""
+    A = synth.laplacian_3d(14, shift=1.3)
+    D = synth.csr_to_dense(A)
+    rng = np.random.default_rng(7 + p)
+    b = rng.standard_normal(A.n)
+    B = np.stack([b, D @ (D @ b)] + [rng.standard_normal(A.n) for _ in range(p - 2)], axis=1)
+    tol, maxit = 1e-8, 100 * p
+    r = gpu_solve(A, B, tol=tol, maxit=maxit, use_graphs=use_graphs)
+    ref = oracle.solve(A, B, tol=tol, maxit=maxit)
+    assert r.status_name == ref.status_name == "OK"
+    assert_counts_close(r.iterations, ref.iterations)
+    same_events(r.events, ref.events)
+    assert [(e["j"], e["action"]) for e in r.events] == [(p + 1, 1)]
+    assert_hist_close(r.history, ref.history)
+    assert max(r.stats["true_res"]) <= tol * 1.5
+    np.testing.assert_allclose(r.X, ref.X, rtol=1e-5, atol=1e-6 * np.abs(ref.X).max())
+    if p == 16:
+        monkeypatch.setenv("BMINRES_NO_RED2F", "1")
+        r2 = gpu_solve(A, B, tol=tol, maxit=maxit, use_graphs=use_graphs)
+        assert r2.iterations == r.iterations
+        np.testing.assert_array_equal(r2.history, r.history)
+        np.testing.assert_array_equal(r2.X, r.X)
