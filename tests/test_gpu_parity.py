@@ -735,3 +735,24 @@ def test_mid_solve_breakdown_large_p(p, use_graphs, monkeypatch):
         assert r2.iterations == r.iterations
         np.testing.assert_array_equal(r2.history, r.history)
         np.testing.assert_array_equal(r2.X, r.X)
+
+
+@pytest.mark.parametrize("p,split", [(16, 2), (16, 1), (32, 2), (32, 1)])
+def test_long_history_parity_large_p(p, split):
+    """Twenty block steps at p = 16 and 32 on a problem of several thousand tiles (3-D 32^3 with a
+    ragged last plane: n = 32*32*31 rows), through the fused K1 (split_spmm = 2) and through the
+    split pair K1a + K1 with the separate update kernel (split_spmm = 1: config 4's and 5's launch
+    configuration) -- 50 iterations are only 1.5 block steps at p = 32, so this is the run that takes
+    the steady-state kernels (two previous blocks' reflectors, paired X updates, both graph
+    parities) against the oracle: the bar's 1e-9 over ALL 20p iterations (measured: 6e-14 at
+    j = 640), events, and X to 1e-9 (measured 7e-14)."""
+    A = synth.laplacian_3d(32, 32, 31, shift=2.1)
+    B = synth.gaussian_rhs(A.n, p, seed=100 + p)
+    maxit = 20 * p
+    r = gpu_solve(A, B, tol=0.0, maxit=maxit, split_spmm=split)
+    ref = oracle.solve(A, B, tol=0.0, maxit=maxit)
+    assert r.status_name == ref.status_name == "MAXIT"
+    assert r.iterations == ref.iterations == maxit
+    same_events(r.events, ref.events)
+    assert_hist_close(r.history, ref.history, upto=maxit)
+    np.testing.assert_allclose(r.X, ref.X, rtol=1e-9, atol=1e-11 * np.abs(ref.X).max())
