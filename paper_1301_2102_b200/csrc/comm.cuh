@@ -126,6 +126,7 @@ struct NcclApi {
     int (*groupStart)() = nullptr;
     int (*groupEnd)() = nullptr;
     int (*commDestroy)(void*) = nullptr;
+    int (*commSplit)(void* comm, int color, int key, void** newcomm, void* config) = nullptr;   // optional (NCCL >= 2.18)
     const char* (*errStr)(int) = nullptr;
     bool load(std::string& err) {
         if (so) return true;
@@ -147,6 +148,7 @@ struct NcclApi {
         groupStart = (int (*)())dlsym(so, "ncclGroupStart");
         groupEnd = (int (*)())dlsym(so, "ncclGroupEnd");
         commDestroy = (int (*)(void*))dlsym(so, "ncclCommDestroy");
+        commSplit = (int (*)(void*, int, int, void**, void*))dlsym(so, "ncclCommSplit");
         errStr = (const char* (*)(int))dlsym(so, "ncclGetErrorString");
         if (!getUniqueId || !commInitRank || !allReduce || !send || !recv || !groupStart || !groupEnd ||
             !commDestroy) {
@@ -169,7 +171,17 @@ struct NcclId {
 };
 
 struct NcclTransport : Transport {
-    void* comm = nullptr;
+    void* comm = nullptr;    // the allreduces (and the plan's all-to-all)
+    // The halo exchange gets a communicator of its own (ncclCommSplit of comm, same ranks): NCCL
+    // serialises the operations of ONE communicator in issue order even across streams, so with a
+    // shared communicator reduce2's allreduce, issued on the main stream right after the exchange
+    // went to hstream, would wait for the whole exchange and the overlap with the update and the
+    // interior SpMM would start only after it.  Both communicators see their operations in the
+    // same order on every rank (the host code is deterministic and K3b's decisions are replicated),
+    // and no kernel of the solver spins on another kernel, so the two NCCL kernels can never wait
+    // on each other.  Without ncclCommSplit (or with BMINRES_NCCL_ONE_COMM=1) the exchange shares
+    // comm (correct, serialised).
+    void* hcomm = nullptr;
     long long* dbuf = nullptr;   // device staging of the plan lists
     size_t dcap = 0;
     bool init(const unsigned char id[128], int rank_, int world_, std::string& err) {
@@ -192,9 +204,23 @@ struct NcclTransport : Transport {
             err = std::string("ncclCommInitRank: ") + (a.errStr ? a.errStr(r) : std::to_string(r));
             return false;
         }
+        const char* one = getenv("BMINRES_NCCL_ONE_COMM");
+        if (a.commSplit && !(one && one[0] == '1')) {
+            // (collective; a failure is an error rather than a silent fallback, which could leave
+            // the ranks with different communicators for the same exchange)
+            const int r2 = a.commSplit(comm, 0, rank, &hcomm, nullptr);
+            if (r2 != 0) {
+                hcomm = nullptr;
+                err = std::string("ncclCommSplit (halo communicator; BMINRES_NCCL_ONE_COMM=1 shares one): ") +
+                      (a.errStr ? a.errStr(r2) : std::to_string(r2));
+                return false;
+            }
+        }
         return true;
     }
+    bool two_comms() const { return hcomm != nullptr; }
     ~NcclTransport() override {
+        if (hcomm) nccl_api().commDestroy(hcomm);
         if (comm) nccl_api().commDestroy(comm);
         if (dbuf) cudaFree(dbuf);
     }
@@ -210,14 +236,15 @@ struct NcclTransport : Transport {
     bool exchange(const double* sendbuf, const long long* scount, double* recvbuf, const long long* rcount,
                   cudaStream_t s, std::string& err) override {
         NcclApi& a = nccl_api();
+        void* xc = hcomm ? hcomm : comm;
         if (!check(a.groupStart(), "ncclGroupStart", err)) return false;
         long long so = 0, ro = 0;
         for (int q = 0; q < world; ++q) {
             if (q != rank && scount[q] > 0 &&
-                !check(a.send(sendbuf + so, (size_t)scount[q], NCCL_FLOAT64, q, comm, s), "ncclSend", err))
+                !check(a.send(sendbuf + so, (size_t)scount[q], NCCL_FLOAT64, q, xc, s), "ncclSend", err))
                 return false;
             if (q != rank && rcount[q] > 0 &&
-                !check(a.recv(recvbuf + ro, (size_t)rcount[q], NCCL_FLOAT64, q, comm, s), "ncclRecv", err))
+                !check(a.recv(recvbuf + ro, (size_t)rcount[q], NCCL_FLOAT64, q, xc, s), "ncclRecv", err))
                 return false;
             so += scount[q];
             ro += rcount[q];

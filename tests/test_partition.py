@@ -173,11 +173,14 @@ def test_two_rank_solve_matches_oracle(tmp_path, name, maxit):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("p", [4, 8])
-def test_nccl_transport_world1_bitwise(p):
+@pytest.mark.parametrize("p,one_comm", [(4, False), (8, False), (8, True)])
+def test_nccl_transport_world1_bitwise(p, one_comm, monkeypatch):
     """The partition path with the NCCL transport (allreduce / exchange captured in the graphs) at
-    world = 1 gives bitwise the plain solve's results (a 1-rank sum is exact)."""
+    world = 1 gives bitwise the plain solve's results (a 1-rank sum is exact).  The halo exchange
+    has a communicator of its own (ncclCommSplit); one_comm: shared."""
     import torch
+    if one_comm:
+        monkeypatch.setenv("BMINRES_NCCL_ONE_COMM", "1")
     from paper_1301_2102_b200 import DeviceCsr, Solver
     A = synth.laplacian_3d(14, shift=2.5)
     B = synth.gaussian_rhs(A.n, p, seed=2)
