@@ -30,14 +30,14 @@ def solver():
     s.close()
 
 
-def gpu_solve(A, B, *, pool_size=1, use_graphs=True, X0=None, split_spmm=0, timing=False, **kw):
+def gpu_solve(A, B, *, pool_size=1, use_graphs=True, X0=None, split_spmm=0, timing=False, policy=0, **kw):
     torch = _torch()
     from paper_1301_2102_b200 import DeviceCsr, Solver
     dA = DeviceCsr.from_host(A, "cuda:0")
     dB = torch.from_numpy(np.ascontiguousarray(B)).to("cuda:0")
     X = None if X0 is None else torch.from_numpy(np.ascontiguousarray(X0)).to("cuda:0")
     with Solver(0, pool_size=pool_size, use_graphs=use_graphs, use_x0=X0 is not None, split_spmm=split_spmm,
-                timing=timing) as s:
+                timing=timing, policy=policy) as s:
         r = s.solve(dA, dB, X, raise_on_error=False, **kw)
     r.X = r.X.cpu().numpy()
     return r
@@ -814,3 +814,47 @@ def test_seeded_sweep_irregular_matrices(seed):
                         pool_size=kw["pool_size"])
     atol = 1e-9 * np.abs(ref.X).max() + 50.0 * np.abs(sens.X - ref.X).max()
     np.testing.assert_allclose(r.X, ref.X, rtol=0.0, atol=atol)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_seeded_sweep_dependent_rhs(seed):
+    """Seeded sweep of the dependence paths on irregular matrices: B = [G, G C + eps N] (config 3's
+    recipe: exact and near dependences in the start block, eps in {0, 1e-10}; none at 1e-6) or
+    B = [b, A^2 b, Gaussian ...] (an exact dependence at j = p + 1, inside the first block step),
+    under both policies (0: replacement from the pool, 1: block-size reduction), p in
+    {2, 4, 6, 8, 16, 32}, fused / split kernels, graphs / plain launches -- against the oracle:
+    status, counts, events (step, column, kind, action), histories to 1e-9, X as in
+    test_seeded_sweep_irregular_matrices."""
+    rng = np.random.default_rng(7000 + seed)
+    p = [2, 4, 6, 8, 16, 32][seed % 6]
+    rep = seed // 6
+    policy = (seed + rep) % 2 if seed < 18 else seed % 2
+    n = int(rng.integers(max(400, 10 * p), 4000))
+    A = _irregular_sym_csr(n, rng, hubs=int(rng.integers(0, 3)), empty_rows=0)
+    if seed < 18:
+        eps = [0.0, 1e-10, 1e-6][(seed + rep) % 3]
+        B = synth.dependent_rhs(n, p // 2, eps, seed=seed)
+    else:
+        import scipy.sparse as sp
+        S = sp.csr_matrix((A.data, A.indices, A.indptr), shape=(n, n))
+        b = rng.standard_normal(n)
+        B = np.ascontiguousarray(np.stack([b, S @ (S @ b)] + [rng.standard_normal(n) for _ in range(p - 2)], axis=1))
+    maxit = 3 * p + 20
+    kw = dict(use_graphs=bool(rng.integers(0, 2)), pool_size=min(p // 2 + 1, 8), policy=policy,
+              split_spmm=int(rng.integers(0, 3)) if p >= 8 else 0)
+    r = gpu_solve(A, B, tol=0.0, maxit=maxit, **kw)
+    ref = oracle.solve(A, B, tol=0.0, maxit=maxit, pool_size=kw["pool_size"], policy=policy)
+    assert r.status_name == ref.status_name, (r.status_name, ref.status_name, kw)
+    assert r.iterations == ref.iterations
+    same_events(r.events, ref.events)
+    if seed < 18 and eps <= 1e-10:
+        assert len(ref.events) == p // 2 and all(e["j"] == 0 for e in ref.events)
+    elif seed >= 18:
+        assert [e["j"] for e in ref.events] == [p + 1]
+    assert_hist_close(r.history, ref.history)
+    prng = np.random.default_rng(seed)
+    sens = oracle.solve(A, B * (1.0 + prng.integers(-1, 2, B.shape) * 2.0 ** -52), tol=0.0, maxit=maxit,
+                        pool_size=kw["pool_size"], policy=policy)
+    if [e["j"] for e in sens.events] == [e["j"] for e in ref.events]:
+        atol = 1e-9 * np.abs(ref.X).max() + 50.0 * np.abs(sens.X - ref.X).max()
+        np.testing.assert_allclose(r.X, ref.X, rtol=0.0, atol=atol)
