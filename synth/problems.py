@@ -23,7 +23,7 @@ import numpy as np
 
 __all__ = [
     "Csr", "Problem", "stencil_csr", "laplacian_2d", "laplacian_3d", "gaussian_rhs",
-    "dependent_rhs", "unstructured_csr", "random_sym_sparse", "diag_csr", "dense_to_csr",
+    "dependent_rhs", "unstructured_csr", "random_sym_sparse", "irregular_sym_csr", "diag_csr", "dense_to_csr",
     "csr_to_dense", "config", "CONFIGS",
 ]
 
@@ -196,6 +196,28 @@ def random_sym_sparse(n: int, density: float = 0.15, seed: int = 0, shift: float
     d = rng.uniform(-2.0, 2.0, n) if shift is None else np.full(n, shift)
     M[np.diag_indices(n)] = d
     return dense_to_csr(M)
+
+
+def irregular_sym_csr(n: int, rng, hubs: int = 0, empty_rows: int = 0) -> Csr:
+    """Random sparse symmetric indefinite CSR with an irregular row-length mix (test input only):
+    degrees 0..12 drawn per row, `hubs` rows with up to 300 entries (rows longer than every gather
+    batch), `empty_rows` rows with no entry at all (zero row and column), a diagonal U[-2, 2]."""
+    import scipy.sparse as sp
+    deg = rng.integers(0, 13, n)
+    for h in rng.choice(n, hubs, replace=False):
+        deg[h] = rng.integers(60, min(300, n - 1))
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, rows.size)
+    vals = rng.standard_normal(rows.size) / 3.0
+    S = sp.triu(sp.coo_matrix((vals, (rows, cols)), shape=(n, n)).tocsr(), 1)
+    S = (S + S.T + sp.diags(rng.uniform(-2.0, 2.0, n))).tolil()
+    for e in rng.choice(n, empty_rows, replace=False):
+        S[e, :] = 0.0
+        S[:, e] = 0.0
+    S = S.tocsr()
+    S.eliminate_zeros()
+    S.sort_indices()
+    return Csr(n, S.indptr.astype(np.int32), S.indices.astype(np.int32), S.data.astype(np.float64))
 
 
 def diag_csr(d) -> Csr:

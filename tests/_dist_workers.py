@@ -99,6 +99,14 @@ def problem(name):
     if name == "dep2d":   # config 3's recipe (B = [G, G C + eps N], eps = 0) on a small grid: step-0 events
         A = synth.laplacian_2d(20, shift=2.5)
         return synth.Problem("dep2d", A, synth.dependent_rhs(A.n, 4, 0.0, seed=0), 1e-10, 4000)
+    if name in ("irr8", "irr16s", "irr32s"):
+        # irregular symmetric indefinite matrices (random columns everywhere: every rank reads rows of
+        # every other rank, and no run of rows is interior -- config 5's situation on a partition);
+        # the "s" problems are solved in split mode (the overlap path with an empty interior)
+        p = {"irr8": 8, "irr16s": 16, "irr32s": 32}[name]
+        rng = np.random.default_rng(4000 + p)
+        A = synth.irregular_sym_csr(1500 + 37 * p, rng, hubs=2, empty_rows=0)
+        return synth.Problem(name, A, np.ascontiguousarray(rng.standard_normal((A.n, p))), 0.0, 4000)
     raise ValueError(name)
 
 
@@ -112,7 +120,8 @@ def solve_worker(rank, world, port, outdir, name, maxit):
     A = DeviceCsr.rows_from_host(P.A, off[rank], off[rank + 1], "cuda:0")
     B = torch.from_numpy(np.ascontiguousarray(P.B[off[rank]:off[rank + 1]])).to("cuda:0")
     # slab16: split mode (K1a alone, its interior rows overlapping the halo exchange; the update kernel)
-    with Solver(0, rank=rank, world=world, comm=TorchComm(), split_spmm=1 if name == "slab16" else 0) as s:
+    with Solver(0, rank=rank, world=world, comm=TorchComm(),
+                split_spmm=1 if name in ("slab16", "irr16s", "irr32s") else 0) as s:
         r = s.solve(A, B, tol=P.tol, maxit=maxit, deflation_tol=P.tau)
         X = r.X.cpu().numpy()
     ev = np.array([[e["j"], e["col"], e["kind"], e["action"]] for e in r.events], dtype=np.int64).reshape(-1, 4)

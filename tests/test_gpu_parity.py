@@ -758,26 +758,7 @@ def test_long_history_parity_large_p(p, split):
     np.testing.assert_allclose(r.X, ref.X, rtol=1e-9, atol=1e-11 * np.abs(ref.X).max())
 
 
-def _irregular_sym_csr(n, rng, hubs, empty_rows):
-    """Random sparse symmetric indefinite CSR with an irregular row-length mix (test input only):
-    degrees 0..12 drawn per row, `hubs` rows with up to 300 entries (rows longer than every gather
-    batch), `empty_rows` rows with no entry at all (zero row and column), a diagonal U[-2, 2]."""
-    import scipy.sparse as sp
-    deg = rng.integers(0, 13, n)
-    for h in rng.choice(n, hubs, replace=False):
-        deg[h] = rng.integers(60, min(300, n - 1))
-    rows = np.repeat(np.arange(n), deg)
-    cols = rng.integers(0, n, rows.size)
-    vals = rng.standard_normal(rows.size) / 3.0
-    S = sp.triu(sp.coo_matrix((vals, (rows, cols)), shape=(n, n)).tocsr(), 1)
-    S = (S + S.T + sp.diags(rng.uniform(-2.0, 2.0, n))).tolil()
-    for e in rng.choice(n, empty_rows, replace=False):
-        S[e, :] = 0.0
-        S[:, e] = 0.0
-    S = S.tocsr()
-    S.eliminate_zeros()
-    S.sort_indices()
-    return synth.Csr(n, S.indptr.astype(np.int32), S.indices.astype(np.int32), S.data.astype(np.float64))
+_irregular_sym_csr = synth.irregular_sym_csr
 
 
 @pytest.mark.parametrize("seed", range(24))
