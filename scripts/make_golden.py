@@ -6,6 +6,7 @@ per-iteration algorithm) on the seeded ``synth`` inputs -- never from the CUDA p
 
   python scripts/make_golden.py first50 4      # config 4: first 50 iterations (history, events)
   python scripts/make_golden.py first50 5      # config 5
+  python scripts/make_golden.py first 4 160    # config 4: first 160 iterations (5 block steps at p = 32)
   python scripts/make_golden.py tol 2          # config 2 run to tol 1e-8 (hours, one thread)
   python scripts/make_golden.py tol 3 600000 1e-6   # config 3 at eps = 1e-6
 
@@ -53,13 +54,13 @@ def write(name: str, d: dict) -> None:
     print("wrote", path, flush=True)
 
 
-def first50(cfg) -> None:
+def first50(cfg, N: int = 50) -> None:
     P = synth.config(cfg)
     t0 = time.perf_counter()
-    r = oracle.solve(P.A, P.B, tol=P.tol, maxit=50, tau=P.tau, pool_size=1)
+    r = oracle.solve(P.A, P.B, tol=P.tol, maxit=N, tau=P.tau, pool_size=1)
     dt = time.perf_counter() - t0
-    write(f"{P.name}_first50.json", {
-        "source": f"oracle.solve(synth.config({cfg!r}), tol={P.tol}, maxit=50, tau={P.tau}, pool_size=1, seed=0)",
+    write(f"{P.name}_first{N}.json", {
+        "source": f"oracle.solve(synth.config({cfg!r}), tol={P.tol}, maxit={N}, tau={P.tau}, pool_size=1, seed=0)",
         "workload": P.name, "n": P.n, "p": P.p, "nnz": P.A.nnz,
         "status": r.status, "iterations": r.iterations,
         "history": r.history.tolist(), "events": r.events,
@@ -90,6 +91,8 @@ if __name__ == "__main__":
     cfg = cfg if cfg == "1c" else int(cfg)
     if mode == "first50":
         first50(cfg)
+    elif mode == "first":
+        first50(cfg, int(sys.argv[3]))
     elif mode == "tol":
         to_tol(cfg, int(sys.argv[3]) if len(sys.argv) > 3 else 600_000,
                float(sys.argv[4]) if len(sys.argv) > 4 else None)

@@ -556,6 +556,23 @@ def test_full_size_config_first_50_vs_oracle(cfg):
     np.testing.assert_allclose(r.stats["true_res"], g["true_res"], rtol=1e-8)
 
 
+@pytest.mark.parametrize("cfg,N", [(4, 160), (5, 320)])
+def test_full_size_config_first_blocks_vs_oracle(cfg, N):
+    """As test_full_size_config_first_50_vs_oracle over 5 block steps of config 4 (160 iterations at
+    p = 32) and 20 of config 5 (320 at p = 16) -- past the start-up blocks, into the steady-state
+    kernels of the bench's launch configuration (graphs of both parities, the separate update kernel
+    with its paired X updates, two previous blocks' reflectors): EVERY iteration's residuals to 1e-9
+    against the oracle's golden history (tests/golden/*_first<N>.json, oracle.solve only)."""
+    P = synth.config(cfg)
+    g = _golden(f"{P.name}_first{N}.json")
+    assert g["n"] == P.n and g["p"] == P.p and g["nnz"] == P.A.nnz
+    r = gpu_solve(P.A, P.B, tol=P.tol, maxit=N, deflation_tol=P.tau)
+    assert r.iterations == g["iterations"] == N and r.status == g["status"]
+    assert_hist_close(r.history, np.array(g["history"]), upto=N)
+    same_events(r.events, g["events"])
+    np.testing.assert_allclose(r.stats["true_res"], g["true_res"], rtol=1e-8)
+
+
 def test_singular_r_closed_form():
     """ESINGULAR_R (reading C23): b_1 = the null vector 1 of a 16 x 16 grid graph Laplacian, so
     A u_1 = 0 exactly, the j = 1 candidate is an exact dependence and R_1 is singular: GPU and oracle
