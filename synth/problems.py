@@ -205,7 +205,8 @@ def irregular_sym_csr(n: int, rng, hubs: int = 0, empty_rows: int = 0) -> Csr:
     import scipy.sparse as sp
     deg = rng.integers(0, 13, n)
     for h in rng.choice(n, hubs, replace=False):
-        deg[h] = rng.integers(60, min(300, n - 1))
+        hi = min(300, n - 1)
+        deg[h] = rng.integers(60 if hi > 60 else max(1, hi // 2), hi)   # (small n: a proportionally long row)
     rows = np.repeat(np.arange(n), deg)
     cols = rng.integers(0, n, rows.size)
     vals = rng.standard_normal(rows.size) / 3.0

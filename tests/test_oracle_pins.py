@@ -74,6 +74,29 @@ def test_dense_least_squares(p, seed):
         np.testing.assert_allclose(r.X, Xls, rtol=1e-7, atol=1e-8 * np.abs(Xls).max())
 
 
+@pytest.mark.parametrize("p", [1, 3, 4])
+def test_dense_least_squares_irregular_matrix(p):
+    """P1 on the irregular recipe of the GPU sweeps (synth.irregular_sym_csr: a hub row, an empty
+    row and column -- A singular, the component of b on the empty row is never reduced): the
+    oracle's iterate is still the least-squares minimiser over R(U_j) at every j."""
+    n = 60
+    A = synth.irregular_sym_csr(n, np.random.default_rng(21), hubs=1, empty_rows=1)
+    D = dense(A)
+    assert (np.diff(A.indptr) == 0).sum() == 1
+    B = np.random.default_rng(200 + p).standard_normal((n, p))
+    jmax = 20
+    Q = banded_krylov_basis(D, B, jmax)
+    beta = np.linalg.norm(B, axis=0)
+    for j in range(1, jmax + 1):
+        r = oracle.solve(A, B, tol=0.0, maxit=j, pool_size=0)
+        assert r.iterations == j and r.status_name == "MAXIT"
+        res, Xls = lsq_residuals(D, B, Q, j)
+        np.testing.assert_allclose(r.history[j] * beta, res, rtol=1e-8)
+        np.testing.assert_allclose(r.X, Xls, rtol=1e-7, atol=1e-8 * np.abs(Xls).max())
+    e = int(np.where(np.diff(A.indptr) == 0)[0][0])
+    assert np.all(r.history[jmax] * beta >= np.abs(B[e]) * (1 - 1e-12))   # the empty row's residual stays b_e
+
+
 def test_nonzero_initial_guess():
     """X0 != 0: F0 = B - A X0 generates the space and x_j - x_0 in R(U_j)."""
     n, p = 40, 3
