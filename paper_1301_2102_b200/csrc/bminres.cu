@@ -45,6 +45,7 @@ struct Kfn {  // per-p kernel table
     void (*k1)(K1Args);
     void (*k1plain)(K1Args);
     void (*k1a)(K1Args);     // split mode: the SpMM alone (null: no split kernels for this p)
+    void (*k1a_long)(K1Args) = nullptr;   // its long-row variant (index prefetch; chosen per matrix in bminres_solve)
     void (*k1pre)(K1Args);   // split mode: K1 streaming A V_k
     size_t smem1pre;
     void (*k1u)(K1Args);     // split mode, p >= 16: the M/X update of block k-2 as its own kernel
@@ -107,6 +108,7 @@ Kfn make_kfn(int q) {
             f.smem1 = K1DSmem<P>::bytes;
             f.nt1 = K1DSmem<P>::WARPS * 32;
             f.k1a = k1a_spmm<P>;
+            f.k1a_long = k1a_spmm<P, true>;
             f.k1pre = k1_dmma<P, true>;
             // p <= 16 (the register Cholesky keeps reduce2's serial tail short: config 3 98k -> 106k
             // it/s; with the serial general Cholesky it was a loss)
@@ -241,6 +243,7 @@ struct bminres_ctx {
     bool red2_fac = false;   // reduce2 factors the new block once (k_red2f)
     bool xdefer = false;   // fused updates defer X in pairs
     int nb1a = 0;
+    bool k1a_long = false, k1a_long_ws = false;
     int k1a_ku = 0;   // K1a chunk length in row groups per warp (0: the kernel's default)
     double* AV = nullptr;
     bool pdl = true;   // programmatic dependent launch of the block-step kernels
@@ -435,7 +438,10 @@ void launch_cluster(bminres_ctx* h, K kern, int grid, int nt, size_t smem, A arg
 }
 
 void ensure_workspace(bminres_ctx* h, long long n, int p, int q) {
-    if (h->n_ws == n && h->p_ws == p && h->q_ws == q && h->next_ws == h->n_ext && h->prec.ws == h->prec.active) return;
+    if (h->n_ws == n && h->p_ws == p && h->q_ws == q && h->next_ws == h->n_ext && h->prec.ws == h->prec.active &&
+        h->k1a_long_ws == h->k1a_long)
+        return;
+    h->k1a_long_ws = h->k1a_long;   // (the graphs hold the kernel, the grid its occupancy)
     h->next_ws = h->n_ext;
     h->prec.ws = h->prec.active;
     for (int s = 0; s < 6; ++s) {
@@ -1501,6 +1507,9 @@ int do_solve(bminres_ctx* h, const bminres_csr* A, const double* Bin, double* Xi
         fail(h, BMINRES_EINVAL, "world = 1 needs n_loc = n, row_begin = 0");
     if (p < 1 || p > BMINRES_MAX_P || !kfn_for(p, &h->kf, o.pool_size)) fail(h, BMINRES_EINVAL, "unsupported block size p");
     if (n < p) fail(h, BMINRES_EINVAL, "n < p");
+    // K1a's long-row variant for matrices with >= 12 entries per row on average (dmma_kernels.cuh)
+    h->k1a_long = h->kf.k1a_long != nullptr && A->nnz >= 12 * n && getenv("BMINRES_K1A_PLAIN") == nullptr;
+    if (h->k1a_long) h->kf.k1a = h->kf.k1a_long;
     if (!std::isfinite(tol) || tol < 0 || maxit < 0 || !std::isfinite(tau) || tau < 0)
         fail(h, BMINRES_EINVAL, "tol / maxit / deflation_tol out of range");
     if (A->nnz < 0 || A->nnz >= (1ll << 31)) fail(h, BMINRES_EINVAL, "nnz must be < 2^31");

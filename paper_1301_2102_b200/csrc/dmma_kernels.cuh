@@ -827,6 +827,7 @@ struct K1aCfg {
     static constexpr int CH = VEC == 4 ? 4 : 8;   // CSR entries per gather batch
     static constexpr int KU = 8;                  // row groups per warp per CTA chunk
     static constexpr int MINB = 5;                // CTAs per SM (<= 48 registers)
+    static constexpr int MINB_LONG = 4;           // the long-row variant (<= 64 registers)
 };
 
 template <int P>
@@ -848,8 +849,14 @@ __device__ __forceinline__ void ldg_vec(const double* p, double (&r)[VEC]) {
     }
 }
 
-template <int P>
-__global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
+// LONG: the variant for matrices with long rows (>= 12 entries per row on average, i.e. three or
+// more gather batches per row): the next batch's column indices / values are loaded while this
+// batch's gathers are in flight, so a row's dependent chain is index -> gather -> gather -> ...
+// instead of index -> gather -> index -> gather -> ...; 12 more registers, 4 CTAs per SM instead of 5.
+// Config 5 (~27 entries per row): K1a 1.61 -> 1.47 ms, 5844 -> 6110 it/s; config 4 (7 entries, two
+// batches): 2.98 -> 3.22 ms, so short rows keep the plain variant (same sums in the same order).
+template <int P, bool LONG = false>
+__global__ void __launch_bounds__(NT, LONG ? K1aCfg<P>::MINB_LONG : K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
     using C = K1aCfg<P>;
     constexpr int VEC = C::VEC, LANES = C::LANES, LP = C::LP, RPW = C::RPW;
     constexpr int CH = C::CH, KU = C::KU;
@@ -896,6 +903,47 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
         double acc[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+        if constexpr (LONG) {
+        int c[CH];
+        double av[CH];
+#pragma unroll
+        for (int t = 0; t < CH; ++t) {
+            const bool pr = r0 + t < r1;
+            c[t] = pr ? __ldg(a.col + r0 + t) : -1;
+            av[t] = pr ? __ldg(a.val + r0 + t) : 0.0;
+        }
+        for (int kb = r0; __any_sync(FULL, kb < r1); kb += CH) {
+            double xv[CH][VEC];
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                if (c[t] >= 0) {
+                    ldg_vec<VEC>(a.X + (long long)c[t] * P + c0, xv[t]);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) xv[t][v] = 0.0;
+                }
+            }
+            int cn[CH];
+            double an[CH];
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                const bool pr = kb + CH + t < r1;
+                cn[t] = pr ? __ldg(a.col + kb + CH + t) : -1;
+                an[t] = pr ? __ldg(a.val + kb + CH + t) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < CH; ++t)
+                if (c[t] >= 0) {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
+                }
+#pragma unroll
+            for (int t = 0; t < CH; ++t) {
+                c[t] = cn[t];
+                av[t] = an[t];
+            }
+        }
+        } else {
         for (int kb = r0; __any_sync(FULL, kb < r1); kb += CH) {
             int c[CH];
             double av[CH];
@@ -928,6 +976,7 @@ __global__ void __launch_bounds__(NT, K1aCfg<P>::MINB) k1a_spmm(K1Args a) {
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) acc[v] = fma(av[t], xv[t][v], acc[v]);
                 }
+        }
         }
         if (live) {
             double* y = a.Y + i * P + c0;   // Y = the AV panel

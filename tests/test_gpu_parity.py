@@ -856,3 +856,41 @@ def test_seeded_sweep_dependent_rhs(seed):
     if [e["j"] for e in sens.events] == [e["j"] for e in ref.events]:
         atol = 1e-9 * np.abs(ref.X).max() + 50.0 * np.abs(sens.X - ref.X).max()
         np.testing.assert_allclose(r.X, ref.X, rtol=0.0, atol=atol)
+
+
+@pytest.mark.parametrize("p", [8, 16, 32])
+def test_k1a_long_row_variant_bitwise(p, monkeypatch):
+    """K1a's long-row variant (chosen for matrices with >= 12 entries per row: the next batch's
+    column indices / values are loaded under the current gathers) sums every row in the same order
+    as the plain kernel: config 5's recipe at n = 20,011 (27 entries per row, random long-range
+    columns) in split mode, against the oracle and bitwise against BMINRES_K1A_PLAIN=1, graphs and
+    plain launches; then a short-row matrix on the same handle sizes takes the plain kernel again."""
+    A, B16 = synth.unstructured_csr(20011, seed=5, p=16)
+    assert A.nnz >= 12 * A.n
+    B = np.ascontiguousarray(np.random.default_rng(p).standard_normal((A.n, p)))
+    maxit = 3 * p + 8
+    ref = oracle.solve(A, B, tol=0.0, maxit=maxit)
+    runs = [gpu_solve(A, B, tol=0.0, maxit=maxit, split_spmm=1, use_graphs=g) for g in (True, False)]
+    monkeypatch.setenv("BMINRES_K1A_PLAIN", "1")
+    plain = gpu_solve(A, B, tol=0.0, maxit=maxit, split_spmm=1)
+    monkeypatch.delenv("BMINRES_K1A_PLAIN")
+    for r in runs:
+        assert r.iterations == ref.iterations == maxit
+        assert_hist_close(r.history, ref.history, upto=maxit)
+        np.testing.assert_array_equal(r.history, plain.history)
+        np.testing.assert_array_equal(r.X, plain.X)
+    np.testing.assert_allclose(runs[0].X, ref.X, rtol=1e-7, atol=1e-9 * np.abs(ref.X).max())
+    # one handle: long rows, then short rows of the same n and p (the kernel and its graphs are rebuilt)
+    torch = _torch()
+    from paper_1301_2102_b200 import DeviceCsr, Solver
+    A2 = synth.irregular_sym_csr(A.n, np.random.default_rng(1), hubs=1, empty_rows=0)
+    assert A2.nnz < 12 * A2.n
+    with Solver(0, split_spmm=1) as s:
+        dB = torch.from_numpy(B).to("cuda:0")
+        r1 = s.solve(DeviceCsr.from_host(A, "cuda:0"), dB, tol=0.0, maxit=maxit, raise_on_error=False)
+        r2 = s.solve(DeviceCsr.from_host(A2, "cuda:0"), dB, tol=0.0, maxit=maxit, raise_on_error=False)
+        r3 = s.solve(DeviceCsr.from_host(A, "cuda:0"), dB, tol=0.0, maxit=maxit, raise_on_error=False)
+    np.testing.assert_array_equal(r1.history, plain.history)
+    np.testing.assert_array_equal(r3.history, plain.history)
+    ref2 = oracle.solve(A2, B, tol=0.0, maxit=maxit)
+    assert_hist_close(r2.history, ref2.history, upto=maxit)
