@@ -888,8 +888,12 @@ __global__ void __launch_bounds__(NT, LONG ? K1aCfg<P>::MINB_LONG : K1aCfg<P>::M
     };
     long long cidx = next_chunk(-1);
     int cpos = warp;
+    auto phys = [&](long long c) -> long long { return c; };
+    int pr0 = 0, pr1 = 0;
+    bool have = false;
     for (long long g = cidx * chunk + cpos; g < ngroups || (ctr && cidx * chunk < ngroups);) {
         if (g >= ngroups) {   // (dyn: this warp has no group in the chunk's tail; the others may)
+            have = false;
             cpos = warp;
             cidx = next_chunk(cidx);
             g = cidx * chunk + cpos;
@@ -898,8 +902,38 @@ __global__ void __launch_bounds__(NT, LONG ? K1aCfg<P>::MINB_LONG : K1aCfg<P>::M
         const long long v = g * RPW + rsub;
         const long long i = a.r0 + v + ((a.gap_at >= 0 && v >= a.gap_at) ? a.gap : 0);
         const bool live = act && v < nr;
-        const int r0 = live ? __ldg(a.rowptr + i) : 0;
-        const int r1 = live ? __ldg(a.rowptr + i + 1) : 0;
+        int r0, r1;
+        if (have) {
+            r0 = pr0;
+            r1 = pr1;
+        } else {
+            r0 = live ? __ldg(a.rowptr + i) : 0;
+            r1 = live ? __ldg(a.rowptr + i + 1) : 0;
+        }
+        if constexpr (LONG) {
+            // the next group's row pointers too, where the next group is known (inside the chunk;
+            // static order): config 5 K1a 1.46 -> 1.40 ms (the plain variant loses with it: 48
+            // registers spill, config 4 2.98 -> 3.18 ms)
+            int ncpos = cpos + nw;
+            long long ncidx = cidx;
+            const bool same = ncpos < chunk;
+            if (!same && !ctr) {
+                ncpos = warp;
+                ncidx = cidx + gridDim.x;
+            }
+            have = false;
+            if (same || !ctr) {
+                const long long gn = phys(ncidx) * chunk + ncpos;
+                if (gn < ngroups) {
+                    const long long vn = gn * RPW + rsub;
+                    const long long in = a.r0 + vn + ((a.gap_at >= 0 && vn >= a.gap_at) ? a.gap : 0);
+                    const bool ln = act && vn < nr;
+                    pr0 = ln ? __ldg(a.rowptr + in) : 0;
+                    pr1 = ln ? __ldg(a.rowptr + in + 1) : 0;
+                    have = true;
+                }
+            }
+        }
         double acc[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
