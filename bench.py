@@ -614,7 +614,7 @@ def main():
     ap.add_argument("--config", default="4")
     ap.add_argument("--iters", type=int, default=0, help="banded iterations per step (0: 6400 / 3200 for configs 4 / 5, "
                                                           "2000 otherwise)")
-    ap.add_argument("--secondary", default="2", help="comma-separated configs measured after the main one (N = 1; 'none' to skip)")
+    ap.add_argument("--secondary", default="2,5", help="comma-separated configs measured after the main one (N = 1; 'none' to skip)")
     ap.add_argument("--time-to-tol", default="2", help="config solved to tol at N = 1 ('none' to skip)")
     ap.add_argument("--precond", default="model200,cfg4",
                     help="f3 IC(0)-preconditioned measurements at N = 1 ('none' to skip)")
